@@ -1,0 +1,499 @@
+#!/usr/bin/env python
+"""bench.py -- GA3C hot path (arXiv 1611.06256) on B200.
+
+A STEP is one GA3C iteration of the device-resident hot path for N_A agents
+per GPU (BASELINE.json configs[1] minus the CPU
+environments):
+  t_max predictor batches      forward(N_A frames) + inverse-CDF sampling
+                               (pipeline.cpp:65-93, util.hpp:46-54)
+  n-step returns               for the N_A agent segments (returns.cpp:8-26),
+                               bootstrapped with the value just played (G8)
+  trainer updates              N_A*t_max/min_train_batch updates, each
+                               loss_and_gradients + RMSProp (pipeline.cpp:241-306)
+so every experience is predicted once and trained once: training samples/s
+== predictions/s.  The metric is training samples/s (TPS in samples, G3);
+updates/s and PPS are reported beside it.  Inputs (u8 84x84x4 frames,
+uniform draws, rewards) are synthetic and resident in HBM, cycled over
+enough sets to exceed the 126 MB L2.  Data parallel (N>1): each rank runs its
+own agents (predictors sharded by agent) and every update all-reduces the
+summed gradient over NCCL before the identical RMSProp step.
+
+--impl reference times the reference's CPU path on the host cores (the fp64
+oracle restatement, oracle/libga3c_oracle.so, all host threads) on the same
+config and prints the same JSON line with "impl": "reference".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NETS = {  # name -> (convs, hidden)
+    "dnn_a": ([(16, 8, 4), (32, 4, 2)], [256]),
+    "large1": ([(32, 8, 1), (32, 4, 2), (64, 4, 2)], [256]),
+    "large2": ([(32, 8, 2), (32, 4, 2), (64, 4, 2)], [256]),
+    "large3": ([(32, 8, 3), (32, 4, 2), (64, 4, 2)], [256]),
+    "large4": ([(32, 8, 4), (32, 4, 2), (64, 4, 2)], [256]),
+}
+FRAME = (84, 84, 4)
+FRAME_BYTES = 84 * 84 * 4
+N_ACTIONS = 6
+METRIC = "training samples/s (GA3C TPS in samples; == predictions/s in the balanced loop)"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=300)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--net", default="dnn_a", choices=sorted(NETS))
+    p.add_argument("--agents", type=int, default=128, help="N_A per GPU (PAPER.md:344-348)")
+    p.add_argument("--tmax", type=int, default=5)
+    p.add_argument("--train-batch", type=int, default=40, help="min_train_batch (PAPER.md:655)")
+    p.add_argument("--sets", type=int, default=0, help="input sets cycled (0 = enough to exceed L2)")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=0)
+    p.add_argument("--cpu-seconds", type=float, default=6.0)
+    p.add_argument("--probe", default="auto", help="kernel class for the roofline probe")
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------- helpers
+
+def layer_geometry(net):
+    convs, hidden = NETS[net]
+    h, w, c = FRAME
+    layers = []
+    for co, k, s in convs:
+        oh, ow = (h - k) // s + 1, (w - k) // s + 1
+        layers.append(dict(kind="conv", K=k * k * c, N=co, P=oh * ow, params=co * k * k * c + co))
+        h, w, c = oh, ow, co
+    prev = h * w * c
+    for o in hidden:
+        layers.append(dict(kind="fc", K=prev, N=o, P=1, params=prev * o + o))
+        prev = o
+    heads = dict(K=prev, N=N_ACTIONS + 1, params=(prev + 1) * (N_ACTIONS + 1))
+    return layers, heads
+
+
+def param_count(net):
+    layers, heads = layer_geometry(net)
+    return sum(l["params"] for l in layers) + heads["params"]
+
+
+def work_per_step(net, agents, tmax, tb):
+    """Algorithmic FLOPs (or bytes) per step for each probed kernel class."""
+    layers, heads = layer_geometry(net)
+    n_fwd = agents * tmax            # states forwarded by the predictors
+    n_train = agents * tmax          # samples trained (forward recompute + backward)
+    updates = (agents * tmax) // tb
+    P = param_count(net)
+    w = {}
+    for li, l in enumerate(layers):
+        mac = l["K"] * l["N"] * l["P"]
+        key = "conv_fwd" if l["kind"] == "conv" else "fc_fwd"
+        w[(key, li)] = 2.0 * mac * (n_fwd + n_train)
+        w[("wgrad", li)] = 2.0 * mac * n_train
+        if li > 0:
+            w[("dgrad", li)] = 2.0 * mac * n_train
+    w[("rmsprop", -1)] = 20.0 * P * updates   # read theta, g, d; write theta, g (fp32)
+    return w
+
+
+def fwd_flops_per_sample(net):
+    layers, heads = layer_geometry(net)
+    return sum(2.0 * l["K"] * l["N"] * l["P"] for l in layers) + 2.0 * heads["K"] * heads["N"]
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        rows = list(self.rows)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        util = [float(r[6]) for r in rows if r[6].replace(".", "").isdigit()]
+        loaded = [s for s, u in zip(sm, util) if u > 0] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------- CPU oracle
+
+def cpu_leg(net, agents, tmax, tb, seconds):
+    """The reference CPU path (fp64 oracle restatement) on all host threads:
+    the same GA3C iteration's forward, loss_and_gradients and RMSProp work."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+    convs, hidden = NETS[net]
+    spec = O.make_spec(FRAME, convs, hidden, N_ACTIONS)
+    hp = O.Hyper()
+    th = O.init_model(spec, O.derive_seed(1, [O.SEED_MODEL_INIT])).astype(np.float32).astype(np.float64)
+    threads = os.cpu_count() or 1
+    fb = min(agents, 8)
+    frames = O.synthetic_frames(3, fb)
+    st = O.frames_to_states(frames)
+    acts, rets = O.synthetic_batch(3, fb, N_ACTIONS)
+    fwd_rate, n_fwd = O.throughput(spec, hp, th, st, acts, rets, 0, threads, seconds / 2)
+    tr_rate, n_tr = O.throughput(spec, hp, th, st, acts, rets, 1, threads, seconds / 2)
+    P = th.size
+    g = np.zeros(P)
+    d = np.full(P, 1e-3)
+    t0 = time.perf_counter()
+    reps = 0
+    while time.perf_counter() - t0 < min(1.0, seconds / 6) or reps < 1:
+        O.rmsprop_update(hp, th, g, d)
+        reps += 1
+    t_rms = (time.perf_counter() - t0) / reps
+    n = agents * tmax
+    updates = n // tb
+    t_step = n / fwd_rate + n / tr_rate + updates * t_rms  # rmsprop is serialized (pipeline.cpp:40)
+    return dict(value=n / t_step, fwd_rate=fwd_rate, train_rate=tr_rate, t_rms=t_rms, threads=threads,
+                sample=(f"{net}: {n_fwd} forwards + {n_tr} loss_and_gradients (batch {fb}/thread) on "
+                        f"{threads} threads over {seconds:.0f}s, {reps} single-thread rmsprop_update; "
+                        f"step = {n} predictions + {n} trained samples + {updates} updates"))
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    # bounded: one short warm-up sample, then up to 3 step samples of a few
+    # seconds of CPU work each (the whole arm stays within ~a minute)
+    seconds = max(1.0, args.cpu_seconds / 2)
+    cpu_leg(args.net, args.agents, args.tmax, args.train_batch, 0.5)
+    vals = []
+    for _ in range(max(1, min(args.steps, 3))):
+        r = cpu_leg(args.net, args.agents, args.tmax, args.train_batch, seconds)
+        vals.append(r["value"])
+    v = float(np.median(vals))
+    n = args.agents * args.tmax
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * n / v,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_of(args, 1),
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": r["threads"], "kind": "port",
+                         "sample": r["sample"] + f"; median of {len(vals)} step samples"},
+        "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def config_of(args, world, sets=None):
+    n = args.agents * args.tmax
+    return {"workload": f"GA3C iteration ({args.net}): {args.tmax} predictor batches of {args.agents} "
+                        f"agents + n-step returns + {n // args.train_batch} trainer updates of "
+                        f"{args.train_batch} samples (loss/backward + RMSProp) per GPU",
+            "net": args.net, "agents_per_gpu": args.agents, "t_max": args.tmax,
+            "predictor_batch": args.agents, "min_train_batch": args.train_batch,
+            "global_train_batch": args.train_batch * world, "updates_per_step": n // args.train_batch,
+            "params": param_count(args.net), "parallelism": f"dp{world}",
+            "l2": (f"inputs cycled over {sets} sets = {sets * n * FRAME_BYTES / 1e6:.0f} MB > 126 MB L2"
+                   if sets else "n/a")}
+
+
+# ----------------------------------------------------------------- GPU arm
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1611_06256_b200 import _abi
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    convs, hidden = NETS[args.net]
+    spec = _abi.NetSpec()
+    spec.in_h, spec.in_w, spec.in_c = FRAME
+    spec.n_conv = len(convs)
+    for i, (co, k, s) in enumerate(convs):
+        spec.conv_out[i], spec.conv_k[i], spec.conv_stride[i] = co, k, s
+    spec.n_hidden = len(hidden)
+    for i, h in enumerate(hidden):
+        spec.hidden[i] = h
+    spec.n_actions = N_ACTIONS
+    hyper = _abi.default_hyper()
+    model = _abi.Model(spec, hyper, device=local)
+    NA, T, TB = args.agents, args.tmax, args.train_batch
+    n = NA * T
+    updates = n // TB
+    assert n % TB == 0 and TB % T == 0, "train batch must cover whole agent segments"
+    ctx = _abi.Context(model, max(NA, TB))
+    P = model.P
+    th = np.zeros(P, np.float32)
+    _abi.check(_abi.lib.ga3c_init_params(spec, 1 + rank * 0, None, th.ctypes.data))  # identical replicas
+    model.load(th)
+    slot, _ = model.acquire()
+
+    # ---- synthetic inputs resident in HBM (agent-major frame rings) ----
+    set_bytes = n * FRAME_BYTES
+    sets = args.sets or max(2, int(np.ceil(160e6 / set_bytes)))
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1234 + rank)
+    frames = torch.randint(0, 256, (sets, NA, T) + FRAME, dtype=torch.uint8, device="cuda", generator=g)
+    uni = torch.rand((sets, T, NA), dtype=torch.float64, device="cuda", generator=g)
+    rewards = (torch.rand((sets, NA, T), dtype=torch.float64, device="cuda", generator=g) - 0.5) * 2
+    terminal = (torch.rand((sets, NA), device="cuda", generator=g) < T / 64.0).to(torch.uint8)
+    offsets = torch.arange(0, n + 1, T, dtype=torch.int32, device="cuda")
+    actions = torch.zeros((NA, T), dtype=torch.int32, device="cuda")
+    rets = torch.zeros((NA, T), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    stream = torch.cuda.ExternalStream(ctx.stream)
+
+    grad_view = None
+    if world > 1:
+        class _View:
+            __cuda_array_interface__ = {"shape": (P,), "typestr": "<f4", "data": (ctx.grad_ptr(), False),
+                                        "version": 3, "strides": None}
+        grad_view = torch.as_tensor(_View(), device=f"cuda:{local}")
+
+    fstride = T * FRAME_BYTES
+    lv = ctx.last_values_ptr()
+
+    def step(i):
+        s = i % sets
+        fr = frames[s].data_ptr()
+        for t in range(T):
+            ctx.forward_dev(fr + t * FRAME_BYTES, NA, True, slot=slot, stride=fstride)
+            ctx.sample_dev(uni[s, t].data_ptr(), NA, actions.data_ptr() + 4 * t, stride=T)
+        ctx.compute_returns_dev(rewards[s].data_ptr(), offsets.data_ptr(), NA, terminal[s].data_ptr(), lv,
+                                hyper.gamma, rets.data_ptr())
+        for u in range(updates):
+            ctx.loss_grad_dev(fr + u * TB * FRAME_BYTES, True, actions.data_ptr() + 4 * u * TB,
+                              rets.data_ptr() + 8 * u * TB, TB, slot, apply_clip=world == 1)
+            if grad_view is not None:
+                with torch.cuda.stream(stream):
+                    dist.all_reduce(grad_view)
+                ctx.clip_grad()
+            ctx.apply_rmsprop_dev()
+
+    # ---- warmup + per-kernel breakdown (untimed) ----
+    for i in range(args.warmup):
+        step(i)
+    ctx.sync()
+    breakdown = {}
+    probe_keys = sorted(work_per_step(args.net, NA, T, TB))
+    for tag in ("conv_fwd", "fc_fwd", "heads", "loss_bwd", "wgrad", "dgrad", "splitk", "rmsprop",
+                "returns", "sample", "other"):
+        ctx.time_kernel(tag, -1)
+        step(0)
+        ms, cnt = ctx.kernel_time()
+        breakdown[tag] = round(ms, 4)
+    for (tag, li) in probe_keys:
+        if li >= 0:
+            ctx.time_kernel(tag, li)
+            step(0)
+            ms, cnt = ctx.kernel_time()
+            breakdown[f"{tag}[{li}]"] = round(ms, 4)
+    ctx.time_kernel("none")
+    work = work_per_step(args.net, NA, T, TB)
+    if args.probe == "auto":
+        cand = [(breakdown.get(f"{t}[{l}]" if l >= 0 else t, 0.0), (t, l)) for (t, l) in work]
+        probe = max(cand)[1]
+    else:
+        t, _, l = args.probe.partition(":")
+        probe = (t, int(l) if l else -1)
+    ctx.time_kernel(probe[0], probe[1])
+    ctx.sync()
+
+    # ---- timed region ----
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctx.sync()
+    l0 = ctx.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for i in range(args.steps):
+        step(args.warmup + i)
+    ev1.record(stream)
+    ev1.synchronize()
+    ctx.sync()
+    launches = ctx.launches() - l0
+    ms_total = ev0.elapsed_time(ev1)
+    probe_ms, probe_n = ctx.kernel_time()
+    ctx.time_kernel("none")
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([ms_total], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+        dist.barrier()
+    ms_step = ms_total / args.steps
+    value = world * n / (ms_step / 1e3)
+
+    hbm, bf16, bf16_sus, peak_src = measured_peaks()
+    w = work[probe] * args.steps
+    if probe[0] == "rmsprop":
+        achieved = w / (probe_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s"}
+    else:
+        achieved = w / (probe_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s"}
+    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": None,
+                 "kernel": f"{probe[0]}[layer {probe[1]}]", "launches": probe_n,
+                 "avg_launch_us": 1e3 * probe_ms / max(1, probe_n),
+                 "share_of_step": probe_ms / ms_total,
+                 "peak_source": f"{peak_src} ({'HBM copy' if probe[0] == 'rmsprop' else 'cuBLAS bf16 burst'})"})
+
+    # ---- end to end through the C ABI with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world, grad_view,
+                      stream, dist)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        r = cpu_leg(args.net, NA, T, TB, args.cpu_seconds)
+        cpu = {"value": r["value"], "unit": "samples/s", "cores": r["threads"], "kind": "port",
+               "sample": r["sample"]}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (u8 84x84x4 frames, seeded weights)",
+            "config": config_of(args, world, sets),
+            "pps": value, "tps_updates_per_s": updates / (ms_step / 1e3),
+            "fwd_mflop_per_prediction": fwd_flops_per_sample(args.net) / 1e6,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk, "kernel_breakdown_ms_per_step": breakdown,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world, grad_view, stream, dist):
+    """Same iteration through the reference-facing host-buffer C ABI calls:
+    every step copies its frames host->device (pinned), reads pi/V back,
+    samples on the host (util.hpp:46-54), computes returns through the ABI
+    and trains through ga3c_loss_grad_u8 + ga3c_apply_rmsprop."""
+    import torch
+    NA, T, TB = args.agents, args.tmax, args.train_batch
+    n = NA * T
+    updates = n // TB
+    k = args.e2e_steps or max(3, min(args.steps, 30))
+    hs = min(sets, 2)
+    fr_agent = [frames[s].cpu().pin_memory().numpy() for s in range(hs)]           # [NA][T] frames
+    fr_time = [frames[s].transpose(0, 1).contiguous().cpu().pin_memory().numpy() for s in range(hs)]
+    u_h = uni[:hs].cpu().numpy()
+    r_h = rewards[:hs].cpu().numpy()
+    term_h = terminal[:hs].cpu().numpy()
+    off = np.arange(0, n + 1, T, dtype=np.int32)
+    h2d = d2h = 0
+
+    def one(i):
+        nonlocal h2d, d2h
+        s = i % hs
+        acts = np.zeros((NA, T), np.int32)
+        v = None
+        for t in range(T):
+            pi, v, _ = ctx.forward(fr_time[s][t])
+            cdf = np.cumsum(pi.astype(np.float64), 1)
+            a = (u_h[s, t][:, None] < cdf).argmax(1)
+            a[~(u_h[s, t][:, None] < cdf).any(1)] = N_ACTIONS - 1
+            acts[:, t] = a
+        rets = ctx.compute_returns(r_h[s].reshape(-1), off, term_h[s], v.astype(np.float64), hyper.gamma)
+        for u in range(updates):
+            sl = slice(u * TB // T, (u + 1) * TB // T)
+            ctx.loss_grad(fr_agent[s][sl].reshape(TB, -1), acts[sl].reshape(-1), rets[u * TB:(u + 1) * TB],
+                          apply_clip=world == 1, want_grad=False)
+            if grad_view is not None:
+                with torch.cuda.stream(stream):
+                    dist.all_reduce(grad_view)
+                ctx.clip_grad()
+            ctx.apply_rmsprop()
+        h2d = T * NA * FRAME_BYTES + n * FRAME_BYTES + n * (8 + 4 + 8) + NA * (1 + 8) + 4 * (NA + 1)
+        d2h = T * NA * (N_ACTIONS + 1) * 4 + n * 8 + updates * (3 * 8 + 4)
+
+    for i in range(2):
+        one(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(k):
+        one(i)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([dt], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    return {"value": world * n * k / dt, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": k, "ms_per_step": 1e3 * dt / k,
+            "path": "ga3c_forward_u8 / ga3c_compute_returns / ga3c_loss_grad_u8 / ga3c_apply_rmsprop "
+                    "(host buffers, pinned)"}
+
+
+if __name__ == "__main__":
+    main()

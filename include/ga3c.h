@@ -1,0 +1,226 @@
+/*
+ * ga3c.h -- C ABI of the B200-native GA3C hot path (libga3c_b200.so).
+ *
+ * This is the drop-in boundary for the reference `qac` library's math layer
+ * (/root/reference/proj/include/qac/nnet.hpp:66-104, returns.hpp:31-32) and
+ * for the device side of its SharedModel / predictor / trainer
+ * (pipeline.hpp:92-120).  Every entry point names the reference interface it
+ * replaces.  Conventions:
+ *   - plain C types only: pointers + sizes, no torch or STL types;
+ *   - int status codes, never exceptions across the ABI.  The C++ adapter
+ *     (paper_1611_06256_b200/csrc/host/qac_b200.hpp) rethrows
+ *     GA3C_INVALID_ARGUMENT as std::invalid_argument, like the reference;
+ *   - caller-owned host buffers, library-owned device buffers;
+ *   - one ga3c_model per device (parameters + RMSProp state, versioned
+ *     snapshots); one ga3c_ctx per predictor/trainer thread (its own CUDA
+ *     stream + workspace).  Calls on distinct contexts may run concurrently;
+ *     apply is serialized inside the model (pipeline.cpp:40).
+ *   - arithmetic is fp32 on the device (reference: fp64); parity tolerances
+ *     are stated in DESIGN.md and tests/.  Returns are fp64, bitwise.
+ * There is no CPU fallback: without a usable sm_100 device every compute
+ * call returns GA3C_CUDA_ERROR.
+ */
+#ifndef GA3C_H
+#define GA3C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GA3C_MAX_CONV 4
+#define GA3C_MAX_HIDDEN 4
+
+/* Status codes. */
+#define GA3C_OK 0
+#define GA3C_INVALID_ARGUMENT 1 /* reference: std::invalid_argument */
+#define GA3C_NONFINITE_INPUT 2  /* reference: std::invalid_argument (non-finite state/return) */
+#define GA3C_CUDA_ERROR 3
+#define GA3C_NCCL_ERROR 4
+#define GA3C_NOT_APPLIED 5      /* rmsprop rejected a non-finite gradient (nnet.cpp:299-301) */
+#define GA3C_OUT_OF_MEMORY 6
+
+/* Network spec.  Extends NetworkSpec (nnet.hpp:14-18) with VALID NHWC conv
+ * layers.  The reference's {input_dim, hidden_dims, n_actions}
+ * is in_h = in_w = 1, in_c = input_dim, n_conv = 0; its flat parameter layout
+ * (nnet.cpp:29-45) is reproduced exactly, conv layers first as
+ * W[Cout][k][k][Cin] (OHWI) then b[Cout]; FC layers consume the NHWC flatten. */
+typedef struct ga3c_net_spec {
+  int in_h, in_w, in_c;
+  int n_conv;
+  int conv_out[GA3C_MAX_CONV];
+  int conv_k[GA3C_MAX_CONV];
+  int conv_stride[GA3C_MAX_CONV];
+  int n_hidden;
+  int hidden[GA3C_MAX_HIDDEN];
+  int n_actions;
+} ga3c_net_spec;
+
+/* Hyperparams (nnet.hpp:20-31), same field order and defaults. */
+typedef struct ga3c_hyper {
+  double gamma;             /* 0.99 */
+  int t_max;                /* 5 */
+  double beta;              /* 0.01 entropy bonus */
+  double eps_log;           /* 1e-6 */
+  double eta;               /* 3e-4 */
+  double alpha;             /* 0.99 rmsprop decay */
+  double eps_rms;           /* 1e-8 */
+  double value_loss_weight; /* 0.5 */
+  double grad_clip_norm;    /* 0 = off */
+  int clip_rewards;         /* 0 */
+} ga3c_hyper;
+
+typedef struct ga3c_model ga3c_model;
+typedef struct ga3c_ctx ga3c_ctx;
+
+const char* ga3c_status_string(int status);
+void ga3c_default_hyper(ga3c_hyper* hp);
+
+/* ---------------------------------------------------- spec and layout */
+/* nnet::validate(NetworkSpec) nnet.cpp:123-130 / validate(Hyperparams) :131-145 */
+int ga3c_validate_spec(const ga3c_net_spec* spec);
+int ga3c_validate_hyper(const ga3c_hyper* hp);
+/* nnet::param_count nnet.hpp:71 (0 if the spec is invalid) */
+size_t ga3c_param_count(const ga3c_net_spec* spec);
+size_t ga3c_input_dim(const ga3c_net_spec* spec);
+/* nnet::init_model nnet.hpp:75 / nnet.cpp:152-168 (host, mt19937_64).
+ * theta64 (nullable) receives the fp64 draws, theta32 (nullable) their fp32
+ * rounding -- the values the device computes with. */
+int ga3c_init_params(const ga3c_net_spec* spec, uint64_t seed, double* theta64, float* theta32);
+
+/* ------------------------------------------- SharedModel (device side) */
+/* SharedModel ctor pipeline.hpp:94: params + rms accumulator live on `device`. */
+ga3c_model* ga3c_model_create(const ga3c_net_spec* spec, const ga3c_hyper* hp, int device,
+                              int* status);
+void ga3c_model_destroy(ga3c_model* m);
+/* Install theta (fp32, P values), g (nullable = zeros, init_rms nnet.cpp:170)
+ * and version as a new snapshot. */
+int ga3c_model_load(ga3c_model* m, const float* theta, const float* g, uint64_t version);
+/* Copy the latest snapshot out (ModelState/RmsState nnet.hpp:35-44). */
+int ga3c_model_read(ga3c_model* m, float* theta, float* g, uint64_t* version);
+/* SharedModel::version pipeline.hpp:98 */
+uint64_t ga3c_model_version(ga3c_model* m);
+size_t ga3c_model_param_count(ga3c_model* m);
+/* SharedModel::snapshot pipeline.hpp:96: pin the latest immutable parameter
+ * slot; it cannot be recycled until released. */
+int ga3c_snapshot_acquire(ga3c_model* m, int* slot, uint64_t* version);
+int ga3c_snapshot_release(ga3c_model* m, int slot);
+const char* ga3c_model_last_error(ga3c_model* m);
+
+/* ------------------------------------------------ per-thread contexts */
+ga3c_ctx* ga3c_ctx_create(ga3c_model* m, int max_batch, int* status);
+void ga3c_ctx_destroy(ga3c_ctx* c);
+void* ga3c_ctx_stream(ga3c_ctx* c); /* cudaStream_t */
+int ga3c_ctx_sync(ga3c_ctx* c);
+/* Number of kernels this context has launched (evidence counter). */
+uint64_t ga3c_ctx_launches(ga3c_ctx* c);
+
+/* ------------------------------------------------------------ forward */
+/* nnet::forward nnet.hpp:81 / nnet.cpp:174-191 on snapshot `slot` (-1 =
+ * latest, pinned for the call).  Host buffers, blocking.  States are NHWC;
+ * u8 frames mean x = k/256 (exact in fp32).  pi: B x n_actions, v: B.
+ * version_used (nullable) receives the snapshot version (PredictionResponse
+ * model_version, pipeline.hpp:32). */
+int ga3c_forward_u8(ga3c_ctx* c, int slot, const uint8_t* frames, int B, float* pi, float* v,
+                    uint64_t* version_used);
+int ga3c_forward_f32(ga3c_ctx* c, int slot, const float* states, int B, float* pi, float* v,
+                     uint64_t* version_used);
+/* Device-resident variant: all pointers are device memory; asynchronous on
+ * the context stream; `slot` must be pinned by the caller.  state_stride =
+ * elements between consecutive states (0 = dense), so a batch can be read
+ * straight out of a per-agent frame ring.  d_pi / d_v (nullable) receive
+ * copies; the sampler can also read the context's own last output. */
+int ga3c_forward_dev(ga3c_ctx* c, int slot, const void* d_states, int states_are_u8,
+                     long long state_stride, int B, float* d_pi, float* d_v);
+
+/* --------------------------------------------------- loss + gradients */
+/* nnet::loss_and_gradients nnet.hpp:94 / nnet.cpp:201-291 on snapshot `slot`.
+ * Summed (not averaged) gradient over the batch; the result stays in the
+ * context's gradient buffer and is copied to dtheta (nullable).
+ * scalars (nullable) = {policy_loss, value_loss, entropy}.  apply_clip = 0
+ * defers the optional global-norm clip (nnet.cpp:281-289) so a data-parallel
+ * caller can clip after the allreduce (ga3c_clip_grad). */
+int ga3c_loss_grad_u8(ga3c_ctx* c, int slot, const uint8_t* frames, const int32_t* actions,
+                      const double* returns, int B, int apply_clip, float* dtheta,
+                      double* scalars);
+int ga3c_loss_grad_f32(ga3c_ctx* c, int slot, const float* states, const int32_t* actions,
+                       const double* returns, int B, int apply_clip, float* dtheta,
+                       double* scalars);
+/* Device-resident variant (async); all pointers are device memory. */
+int ga3c_loss_grad_dev(ga3c_ctx* c, int slot, const void* d_states, int states_are_u8,
+                       long long state_stride, const int32_t* d_actions, const double* d_returns,
+                       int B, int apply_clip);
+/* The context's device gradient buffer (P floats) -- e.g. for an NCCL
+ * allreduce(sum) across data-parallel replicas. */
+float* ga3c_ctx_grad(ga3c_ctx* c);
+/* The context's fp64 copy of the last forward's values V (device, B
+ * doubles): the bootstrap input of ga3c_compute_returns_dev (the reference
+ * seeds a cut segment with the value just played, pipeline.cpp:193-196). */
+const double* ga3c_ctx_last_values(ga3c_ctx* c);
+/* Copy the last gradient and scalars to the host (blocking). */
+int ga3c_ctx_read_grad(ga3c_ctx* c, float* dtheta, double* scalars);
+/* Optional global-norm clip of the context gradient (nnet.cpp:281-289). */
+int ga3c_clip_grad(ga3c_ctx* c);
+
+/* ------------------------------------------------------------ rmsprop */
+/* SharedModel::apply pipeline.cpp:37-63 -> nnet::rmsprop_update
+ * nnet.cpp:293-312: one non-centred RMSProp step on the LATEST parameters,
+ * written out of place into a fresh slot and published as version+1.
+ * dtheta: host gradient (P floats), or NULL to use the context gradient.
+ * applied = 0 (status GA3C_NOT_APPLIED) when any gradient component is
+ * non-finite; nothing changes then.  applied_on (nullable) = the version the
+ * step was applied on top of. */
+int ga3c_apply_rmsprop(ga3c_ctx* c, const float* dtheta, int* applied, uint64_t* applied_on);
+/* Stream-ordered device loop variant: updates the latest slot IN PLACE from
+ * the context gradient, gated by the on-device non-finite flag; no host
+ * synchronisation.  Only valid while no other thread reads the model. */
+int ga3c_apply_rmsprop_dev(ga3c_ctx* c);
+/* On-device update counter of ga3c_apply_rmsprop_dev (blocking read). */
+int ga3c_ctx_read_dev_version(ga3c_ctx* c, uint64_t* version);
+
+/* ------------------------------------------------------------ returns */
+/* returns::compute_returns returns.hpp:31 / returns.cpp:8-26, batched over
+ * n_seg segments: segment s covers rewards[seg_offsets[s] .. seg_offsets[s+1]).
+ * fp64 with the reference's operation order (bitwise).  Host buffers. */
+int ga3c_compute_returns(ga3c_ctx* c, const double* rewards, const int32_t* seg_offsets,
+                         int n_seg, const uint8_t* terminal, const double* bootstrap,
+                         double gamma, double* out);
+/* Device variant (async, no validation); d_out feeds ga3c_loss_grad_dev. */
+int ga3c_compute_returns_dev(ga3c_ctx* c, const double* d_rewards, const int32_t* d_seg_offsets,
+                             int n_seg, const uint8_t* d_terminal, const double* d_bootstrap,
+                             double gamma, double* d_out);
+
+/* ------------------------------------------------------ timing probe */
+/* Kernel classes for the roofline probe. */
+#define GA3C_K_NONE 0
+#define GA3C_K_CONV_FWD 1
+#define GA3C_K_FC_FWD 2
+#define GA3C_K_HEADS 3
+#define GA3C_K_LOSS_BWD 4
+#define GA3C_K_WGRAD 5
+#define GA3C_K_DGRAD 6
+#define GA3C_K_SPLITK 7
+#define GA3C_K_RMSPROP 8
+#define GA3C_K_RETURNS 9
+#define GA3C_K_SAMPLE 10
+#define GA3C_K_OTHER 11
+/* Bracket every subsequent launch of kernel class `tag` (trunk layer `layer`,
+ * -1 = any) with CUDA events on the context stream (GA3C_K_NONE disables). */
+int ga3c_ctx_time_kernel(ga3c_ctx* c, int tag, int layer);
+/* Sum of the bracketed device durations since the last call (blocking). */
+int ga3c_ctx_kernel_time(ga3c_ctx* c, double* total_ms, uint64_t* launches);
+
+/* ----------------------------------------------------------- sampling */
+/* qac::sample_index util.hpp:46-54 per row: the first a with u < sum_{<=a} pi
+ * accumulated in fp64.  d_pi = NULL samples the context's last forward output
+ * using its fp64 softmax; otherwise the fp32 rows of d_pi.  Device buffers,
+ * async. */
+int ga3c_sample_actions_dev(ga3c_ctx* c, const float* d_pi, const double* d_u, int B,
+                            int n_actions, int32_t* d_actions, int action_stride);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GA3C_H */

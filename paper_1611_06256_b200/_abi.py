@@ -1,0 +1,338 @@
+"""ctypes binding of the C ABI in include/ga3c.h (libga3c_b200.so).
+
+This is the Python side of the drop-in boundary: the same entry points a
+maintainer would bind from the reference's pybind11 module
+(proj/bindings/qac_module.cpp) -- see INTEGRATION.md.  There is no CPU path:
+if the shared library is missing this module raises ImportError, and every
+compute call raises RuntimeError when no sm_100 device is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libga3c_b200.so")
+
+MAX_CONV = 4
+MAX_HIDDEN = 4
+
+OK = 0
+INVALID_ARGUMENT = 1
+NONFINITE_INPUT = 2
+CUDA_ERROR = 3
+NCCL_ERROR = 4
+NOT_APPLIED = 5
+OUT_OF_MEMORY = 6
+
+
+class NetSpec(C.Structure):
+    """ga3c_net_spec (include/ga3c.h)."""
+
+    _fields_ = [
+        ("in_h", C.c_int), ("in_w", C.c_int), ("in_c", C.c_int),
+        ("n_conv", C.c_int),
+        ("conv_out", C.c_int * MAX_CONV),
+        ("conv_k", C.c_int * MAX_CONV),
+        ("conv_stride", C.c_int * MAX_CONV),
+        ("n_hidden", C.c_int),
+        ("hidden", C.c_int * MAX_HIDDEN),
+        ("n_actions", C.c_int),
+    ]
+
+
+class HyperC(C.Structure):
+    """ga3c_hyper (include/ga3c.h) = Hyperparams nnet.hpp:20-31."""
+
+    _fields_ = [
+        ("gamma", C.c_double), ("t_max", C.c_int), ("beta", C.c_double),
+        ("eps_log", C.c_double), ("eta", C.c_double), ("alpha", C.c_double),
+        ("eps_rms", C.c_double), ("value_loss_weight", C.c_double),
+        ("grad_clip_norm", C.c_double), ("clip_rewards", C.c_int),
+    ]
+
+
+_P = C.c_void_p
+_SIGS = {
+    "ga3c_status_string": (C.c_char_p, [C.c_int]),
+    "ga3c_default_hyper": (None, [C.POINTER(HyperC)]),
+    "ga3c_validate_spec": (C.c_int, [C.POINTER(NetSpec)]),
+    "ga3c_validate_hyper": (C.c_int, [C.POINTER(HyperC)]),
+    "ga3c_param_count": (C.c_size_t, [C.POINTER(NetSpec)]),
+    "ga3c_input_dim": (C.c_size_t, [C.POINTER(NetSpec)]),
+    "ga3c_init_params": (C.c_int, [C.POINTER(NetSpec), C.c_uint64, _P, _P]),
+    "ga3c_model_create": (_P, [C.POINTER(NetSpec), C.POINTER(HyperC), C.c_int, C.POINTER(C.c_int)]),
+    "ga3c_model_destroy": (None, [_P]),
+    "ga3c_model_load": (C.c_int, [_P, _P, _P, C.c_uint64]),
+    "ga3c_model_read": (C.c_int, [_P, _P, _P, C.POINTER(C.c_uint64)]),
+    "ga3c_model_version": (C.c_uint64, [_P]),
+    "ga3c_model_param_count": (C.c_size_t, [_P]),
+    "ga3c_snapshot_acquire": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_uint64)]),
+    "ga3c_snapshot_release": (C.c_int, [_P, C.c_int]),
+    "ga3c_model_last_error": (C.c_char_p, [_P]),
+    "ga3c_ctx_create": (_P, [_P, C.c_int, C.POINTER(C.c_int)]),
+    "ga3c_ctx_destroy": (None, [_P]),
+    "ga3c_ctx_stream": (_P, [_P]),
+    "ga3c_ctx_sync": (C.c_int, [_P]),
+    "ga3c_ctx_launches": (C.c_uint64, [_P]),
+    "ga3c_forward_u8": (C.c_int, [_P, C.c_int, _P, C.c_int, _P, _P, C.POINTER(C.c_uint64)]),
+    "ga3c_forward_f32": (C.c_int, [_P, C.c_int, _P, C.c_int, _P, _P, C.POINTER(C.c_uint64)]),
+    "ga3c_forward_dev": (C.c_int, [_P, C.c_int, _P, C.c_int, C.c_longlong, C.c_int, _P, _P]),
+    "ga3c_loss_grad_u8": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, C.c_int, _P, _P]),
+    "ga3c_loss_grad_f32": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, C.c_int, _P, _P]),
+    "ga3c_loss_grad_dev": (C.c_int, [_P, C.c_int, _P, C.c_int, C.c_longlong, _P, _P, C.c_int, C.c_int]),
+    "ga3c_ctx_grad": (_P, [_P]),
+    "ga3c_ctx_last_values": (_P, [_P]),
+    "ga3c_ctx_read_grad": (C.c_int, [_P, _P, _P]),
+    "ga3c_clip_grad": (C.c_int, [_P]),
+    "ga3c_apply_rmsprop": (C.c_int, [_P, _P, C.POINTER(C.c_int), C.POINTER(C.c_uint64)]),
+    "ga3c_apply_rmsprop_dev": (C.c_int, [_P]),
+    "ga3c_ctx_read_dev_version": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
+    "ga3c_compute_returns": (C.c_int, [_P, _P, _P, C.c_int, _P, _P, C.c_double, _P]),
+    "ga3c_compute_returns_dev": (C.c_int, [_P, _P, _P, C.c_int, _P, _P, C.c_double, _P]),
+    "ga3c_sample_actions_dev": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, _P, C.c_int]),
+    "ga3c_ctx_time_kernel": (C.c_int, [_P, C.c_int, C.c_int]),
+    "ga3c_ctx_kernel_time": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
+}
+
+K_TAGS = {"none": 0, "conv_fwd": 1, "fc_fwd": 2, "heads": 3, "loss_bwd": 4, "wgrad": 5, "dgrad": 6,
+          "splitk": 7, "rmsprop": 8, "returns": 9, "sample": 10, "other": 11}
+
+EXPORTED = tuple(_SIGS)
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback for the GA3C hot path)")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in _SIGS.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+class GA3CError(RuntimeError):
+    def __init__(self, status, msg=""):
+        self.status = status
+        super().__init__(f"{lib.ga3c_status_string(status).decode()}: {msg}")
+
+
+class InvalidArgument(GA3CError, ValueError):
+    """Where the reference throws std::invalid_argument (pybind -> ValueError)."""
+
+
+def check(status, msg=""):
+    if status == OK:
+        return
+    if status in (INVALID_ARGUMENT, NONFINITE_INPUT):
+        raise InvalidArgument(status, msg)
+    raise GA3CError(status, msg)
+
+
+def ptr(a):
+    """Device/host pointer of a numpy array or torch tensor (None -> NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+def default_hyper():
+    h = HyperC()
+    lib.ga3c_default_hyper(C.byref(h))
+    return h
+
+
+class Model:
+    """ga3c_model: device parameters + rms state, versioned snapshots."""
+
+    def __init__(self, spec: NetSpec, hyper: HyperC, device: int = 0):
+        st = C.c_int(0)
+        self.spec, self.hyper = spec, hyper
+        self.h = lib.ga3c_model_create(C.byref(spec), C.byref(hyper), device, C.byref(st))
+        if not self.h:
+            check(st.value, lib.ga3c_model_last_error(None).decode())
+        self.P = int(lib.ga3c_model_param_count(self.h))
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.ga3c_model_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def error(self):
+        return lib.ga3c_model_last_error(self.h).decode()
+
+    def load(self, theta, g=None, version=0):
+        theta = np.ascontiguousarray(theta, np.float32)
+        g = None if g is None else np.ascontiguousarray(g, np.float32)
+        assert theta.size == self.P
+        check(lib.ga3c_model_load(self.h, ptr(theta), ptr(g), version), self.error())
+
+    def read(self):
+        th = np.zeros(self.P, np.float32)
+        g = np.zeros(self.P, np.float32)
+        v = C.c_uint64(0)
+        check(lib.ga3c_model_read(self.h, ptr(th), ptr(g), C.byref(v)), self.error())
+        return th, g, v.value
+
+    def version(self):
+        return int(lib.ga3c_model_version(self.h))
+
+    def acquire(self):
+        s, v = C.c_int(0), C.c_uint64(0)
+        check(lib.ga3c_snapshot_acquire(self.h, C.byref(s), C.byref(v)))
+        return s.value, v.value
+
+    def release(self, slot):
+        check(lib.ga3c_snapshot_release(self.h, slot))
+
+
+class Context:
+    """ga3c_ctx: one CUDA stream + workspace for batches up to max_batch."""
+
+    def __init__(self, model: Model, max_batch: int):
+        st = C.c_int(0)
+        self.model = model
+        self.h = lib.ga3c_ctx_create(model.h, max_batch, C.byref(st))
+        if not self.h:
+            check(st.value, lib.ga3c_model_last_error(model.h).decode())
+        self.max_batch = max_batch
+        self.A = model.spec.n_actions
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.ga3c_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    @property
+    def stream(self):
+        return lib.ga3c_ctx_stream(self.h)
+
+    def sync(self):
+        check(lib.ga3c_ctx_sync(self.h), self.model.error())
+
+    def launches(self):
+        return int(lib.ga3c_ctx_launches(self.h))
+
+    # --- host-buffer calls (blocking) -------------------------------------
+    def forward(self, states, slot=-1):
+        """states: (B, H*W*C) or (B,H,W,C) uint8 frames or float32 states."""
+        states = np.ascontiguousarray(states)
+        B = states.shape[0]
+        pi = np.zeros((B, self.A), np.float32)
+        v = np.zeros(B, np.float32)
+        ver = C.c_uint64(0)
+        if states.dtype == np.uint8:
+            rc = lib.ga3c_forward_u8(self.h, slot, ptr(states), B, ptr(pi), ptr(v), C.byref(ver))
+        else:
+            states = np.ascontiguousarray(states, np.float32)
+            rc = lib.ga3c_forward_f32(self.h, slot, ptr(states), B, ptr(pi), ptr(v), C.byref(ver))
+        check(rc, self.model.error())
+        return pi, v, ver.value
+
+    def loss_grad(self, states, actions, returns, slot=-1, apply_clip=True, want_grad=True):
+        states = np.ascontiguousarray(states)
+        B = states.shape[0]
+        actions = np.ascontiguousarray(actions, np.int32)
+        returns = np.ascontiguousarray(returns, np.float64)
+        if actions.size != B or returns.size != B:
+            raise InvalidArgument(INVALID_ARGUMENT, "returns/experiences length mismatch")
+        d = np.zeros(self.model.P, np.float32) if want_grad else None
+        sc = np.zeros(3, np.float64)
+        if states.dtype == np.uint8:
+            rc = lib.ga3c_loss_grad_u8(self.h, slot, ptr(states), ptr(actions), ptr(returns), B,
+                                       int(apply_clip), ptr(d), ptr(sc))
+        else:
+            states = np.ascontiguousarray(states, np.float32)
+            rc = lib.ga3c_loss_grad_f32(self.h, slot, ptr(states), ptr(actions), ptr(returns), B,
+                                        int(apply_clip), ptr(d), ptr(sc))
+        check(rc, self.model.error())
+        return d, sc
+
+    def apply_rmsprop(self, dtheta=None):
+        """SharedModel::apply -> (applied, applied_on_version)."""
+        d = None if dtheta is None else np.ascontiguousarray(dtheta, np.float32)
+        ap, on = C.c_int(0), C.c_uint64(0)
+        rc = lib.ga3c_apply_rmsprop(self.h, ptr(d), C.byref(ap), C.byref(on))
+        if rc == NOT_APPLIED:
+            return False, None
+        check(rc, self.model.error())
+        return bool(ap.value), on.value
+
+    def compute_returns(self, rewards, seg_offsets, terminal, bootstrap, gamma):
+        r = np.ascontiguousarray(rewards, np.float64)
+        off = np.ascontiguousarray(seg_offsets, np.int32)
+        term = np.ascontiguousarray(terminal, np.uint8)
+        boot = np.ascontiguousarray(bootstrap, np.float64)
+        out = np.zeros(r.size, np.float64)
+        check(lib.ga3c_compute_returns(self.h, ptr(r), ptr(off), len(off) - 1, ptr(term), ptr(boot),
+                                       float(gamma), ptr(out)), self.model.error())
+        return out
+
+    def read_grad(self):
+        d = np.zeros(self.model.P, np.float32)
+        sc = np.zeros(3, np.float64)
+        check(lib.ga3c_ctx_read_grad(self.h, ptr(d), ptr(sc)), self.model.error())
+        return d, sc
+
+    # --- device-resident calls (async on self.stream) ----------------------
+    def forward_dev(self, d_states, B, u8, d_pi=None, d_v=None, slot=None, stride=0):
+        s = self.model.acquire()[0] if slot is None else slot
+        rc = lib.ga3c_forward_dev(self.h, s, d_states, int(u8), stride, B, d_pi, d_v)
+        if slot is None:
+            self.model.release(s)  # caller owns ordering (single-threaded device loop)
+        check(rc, self.model.error())
+
+    def loss_grad_dev(self, d_states, u8, d_actions, d_returns, B, slot, apply_clip=True, stride=0):
+        check(lib.ga3c_loss_grad_dev(self.h, slot, d_states, int(u8), stride, d_actions, d_returns, B,
+                                     int(apply_clip)), self.model.error())
+
+    def apply_rmsprop_dev(self):
+        check(lib.ga3c_apply_rmsprop_dev(self.h), self.model.error())
+
+    def compute_returns_dev(self, d_rew, d_off, n_seg, d_term, d_boot, gamma, d_out):
+        check(lib.ga3c_compute_returns_dev(self.h, d_rew, d_off, n_seg, d_term, d_boot, float(gamma),
+                                           d_out), self.model.error())
+
+    def sample_dev(self, d_u, B, d_actions, d_pi=None, stride=1):
+        check(lib.ga3c_sample_actions_dev(self.h, d_pi, d_u, B, self.A, d_actions, stride),
+              self.model.error())
+
+    def last_values_ptr(self):
+        return lib.ga3c_ctx_last_values(self.h)
+
+    def grad_ptr(self):
+        return lib.ga3c_ctx_grad(self.h)
+
+    def clip_grad(self):
+        check(lib.ga3c_clip_grad(self.h), self.model.error())
+
+    def time_kernel(self, tag, layer=-1):
+        check(lib.ga3c_ctx_time_kernel(self.h, K_TAGS[tag] if isinstance(tag, str) else tag, layer))
+
+    def kernel_time(self):
+        """(total_ms, launches) of the probed kernel class since the last call."""
+        ms, n = C.c_double(0), C.c_uint64(0)
+        check(lib.ga3c_ctx_kernel_time(self.h, C.byref(ms), C.byref(n)), self.model.error())
+        return ms.value, n.value
+
+    def dev_version(self):
+        v = C.c_uint64(0)
+        check(lib.ga3c_ctx_read_dev_version(self.h, C.byref(v)), self.model.error())
+        return v.value

@@ -1,0 +1,1053 @@
+// engine.cu -- device engine and C ABI of libga3c_b200.so (include/ga3c.h).
+//
+// ga3c_model  = the device side of SharedModel (pipeline.hpp:92-111): a ring
+//               of immutable parameter slots {theta, g, version}.  Readers pin
+//               a slot; apply() writes the RMSProp step out of place into a
+//               free slot and publishes it, so a forward pass never sees a torn
+//               update (pipeline.hpp:87-91) and the step lands on the LATEST
+//               parameters while the gradient came from an older snapshot
+//               (pipeline.cpp:285-287 vs 43-48).
+// ga3c_ctx    = one predictor/trainer thread: a CUDA stream plus the
+//               activation/gradient workspace for up to max_batch states.
+//
+// Forward (nnet.cpp:91-119) is a chain of implicit-GEMM launches, one per
+// trunk layer, then the fused FC-finalize + heads + softmax kernel.
+// loss_and_gradients (nnet.cpp:201-291) re-runs that forward keeping the
+// activations, then the fused loss/heads-backward kernel and, per trunk layer
+// from the top, a weight-gradient GEMM (bias gradient folded in as a ones
+// column) and an input-gradient kernel gated by the previous activation.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "ga3c.h"
+#include "kernels.cuh"
+#include "layout.hpp"
+
+using namespace ga3c;
+
+namespace {
+
+constexpr int kNumSMs = 148;
+constexpr std::size_t kPartFloats = std::size_t(32) << 20;  // split-K scratch per ctx (128 MB)
+constexpr int kMaxActions = 64;
+
+struct Slot {
+  float* theta = nullptr;
+  float* g = nullptr;
+  std::uint64_t version = 0;
+  int refs = 0;
+};
+
+}  // namespace
+
+struct ga3c_model {
+  ga3c_net_spec spec{};
+  ga3c_hyper hp{};
+  Layout lo;
+  int device = 0;
+  std::mutex read_m;    // guards slots[].refs / version / cur  (pipeline.cpp:22-25)
+  std::mutex update_m;  // serializes writers                   (pipeline.cpp:40)
+  std::vector<Slot> slots;
+  int cur = 0;
+  std::mutex err_m;
+  std::string last_error;
+  void set_error(const std::string& e) {
+    std::lock_guard<std::mutex> lk(err_m);
+    last_error = e;
+  }
+};
+
+struct ga3c_ctx {
+  ga3c_model* m = nullptr;
+  cudaStream_t stream = nullptr;
+  int max_batch = 0;
+  void* d_in = nullptr;
+  float* act[GA3C_MAX_CONV + GA3C_MAX_HIDDEN] = {};
+  float* dx[2] = {};
+  float* hin = nullptr;  // f32 copy of a raw input feeding the heads directly
+  float* pi32 = nullptr;
+  double* pi64 = nullptr;
+  float* v = nullptr;
+  double* v64 = nullptr;
+  float* dhead = nullptr;
+  double* scal = nullptr;
+  double* scal_sum = nullptr;
+  int32_t* d_actions = nullptr;
+  double* d_rets = nullptr;
+  float* grad = nullptr;
+  int* flag = nullptr;
+  unsigned long long* dev_version = nullptr;
+  float* part = nullptr;
+  double* clip_part = nullptr;
+  // returns / host staging
+  double* r_rew = nullptr;
+  int32_t* r_off = nullptr;
+  uint8_t* r_term = nullptr;
+  double* r_boot = nullptr;
+  double* r_out = nullptr;
+  std::size_t r_cap = 0, r_seg_cap = 0;
+  int* h_flag = nullptr;  // pinned
+  std::uint64_t launches = 0;
+  std::string last_error;
+  // kernel timing probe (ga3c_ctx_time_kernel)
+  int timed_tag = 0, timed_layer = -1;
+  std::vector<cudaEvent_t> events;
+  std::size_t ev_used = 0;
+};
+
+namespace {
+
+#define GA3C_CUDA(call)                                                               \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) {                                                          \
+      set_err(std::string(#call) + ": " + cudaGetErrorString(e_));                    \
+      return GA3C_CUDA_ERROR;                                                         \
+    }                                                                                 \
+  } while (0)
+
+thread_local std::string g_tls_error;
+
+
+// --------------------------------------------------------------- GEMMs
+
+struct SplitPlan {
+  int splits = 1;
+  int k_chunk = 0;
+};
+
+SplitPlan plan_splits(int M, int N, int K, bool allow_split) {
+  SplitPlan p;
+  const int tiles = ((M + kBM - 1) / kBM) * ((N + kBN - 1) / kBN);
+  int s = 1;
+  if (allow_split) {
+    s = std::max(1, (2 * kNumSMs + tiles - 1) / tiles);
+    s = std::min(s, std::max(1, K / 128));
+    while (s > 1 && static_cast<std::size_t>(s) * M * N > kPartFloats) --s;
+  }
+  int kc = (K + s - 1) / s;
+  kc = ((kc + kBK - 1) / kBK) * kBK;
+  if (kc <= 0) kc = kBK;
+  p.k_chunk = kc;
+  p.splits = std::max(1, (K + kc - 1) / kc);
+  return p;
+}
+
+// Brackets one launch with CUDA events when (tag, layer) is the probed kernel
+// class; always counts the launch.
+struct Launch {
+  ga3c_ctx* c;
+  bool on;
+  Launch(ga3c_ctx* c_, int tag, int layer) : c(c_) {
+    on = c->timed_tag == tag && (c->timed_layer < 0 || c->timed_layer == layer);
+    if (on) {
+      while (c->events.size() < c->ev_used + 2) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        c->events.push_back(e);
+      }
+      cudaEventRecord(c->events[c->ev_used], c->stream);
+    }
+  }
+  ~Launch() {
+    if (on) {
+      cudaEventRecord(c->events[c->ev_used + 1], c->stream);
+      c->ev_used += 2;
+    }
+    c->launches++;
+  }
+};
+
+template <class LA, class LB, class Epi>
+void launch_gemm(ga3c_ctx* c, int tag, int layer, const LA& la, const LB& lb, const Epi& epi, int M,
+                 int N, int K, const SplitPlan& p) {
+  dim3 grid((N + kBN - 1) / kBN, (M + kBM - 1) / kBM, p.splits);
+  Launch l(c, tag, layer);
+  gemm_simt_kernel<LA, LB, Epi><<<grid, kThreads, 0, c->stream>>>(la, lb, epi, M, N, K, p.k_chunk);
+}
+
+template <typename T>
+Im2col<T> im2col_of(const Layer& L, const void* x, long long bstride) {
+  Im2col<T> g;
+  g.bstride = bstride > 0 ? bstride : static_cast<long long>(L.ih) * L.iw * L.cin;
+  g.p = static_cast<const T*>(x);
+  g.ih = L.ih;
+  g.iw = L.iw;
+  g.cin = L.cin;
+  g.stride = L.stride;
+  g.ow = L.ow;
+  g.P = L.oh * L.ow;
+  g.rowlen = L.k * L.cin;
+  return g;
+}
+
+template <typename T>
+void conv_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const void* x, float* out,
+                  int B, long long in_stride) {
+  Im2colA<T> a;
+  static_cast<Im2col<T>&>(a) = im2col_of<T>(L, x, in_stride);
+  DenseK w{theta + L.w_off, L.in};
+  const int M = B * L.pixels();
+  launch_gemm(c, GA3C_K_CONV_FWD, li, a, w, EpiBiasRelu{out, theta + L.b_off, L.cout}, M, L.cout,
+              L.in, plan_splits(M, L.cout, L.in, false));
+}
+
+// FC forward.  If `keep_partials` the split-K partials are left in c->part for
+// the fused heads kernel; returns the number of splits used.
+template <typename T>
+int fc_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const void* x, float* out,
+               int B, bool keep_partials, long long in_stride) {
+  DenseKIn<T> a{static_cast<const T*>(x), in_stride > 0 ? static_cast<int>(in_stride) : L.in};
+  DenseK w{theta + L.w_off, L.in};
+  const SplitPlan p = plan_splits(B, L.out, L.in, true);
+  if (keep_partials || p.splits > 1) {
+    launch_gemm(c, GA3C_K_FC_FWD, li, a, w, EpiPartial{c->part, B, L.out}, B, L.out, L.in, p);
+    if (!keep_partials) {
+      const std::size_t n = static_cast<std::size_t>(B) * L.out;
+      Launch l(c, GA3C_K_SPLITK, li);
+      splitk_bias_relu_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(
+          c->part, p.splits, B, L.out, theta + L.b_off, out);
+    }
+  } else {
+    launch_gemm(c, GA3C_K_FC_FWD, li, a, w, EpiBiasRelu{out, theta + L.b_off, L.out}, B, L.out, L.in, p);
+  }
+  return p.splits;
+}
+
+// Weight-gradient GEMM [M rows][N = Kw+1] (+ reduction) into dtheta.
+template <class LA, class LB>
+void wgrad_gemm(ga3c_ctx* c, int li, const LA& la, const LB& lb, const GradMap& gm, int M, int N,
+                int K) {
+  const SplitPlan p = plan_splits(M, N, K, true);
+  if (p.splits == 1) {
+    launch_gemm(c, GA3C_K_WGRAD, li, la, lb, EpiGrad{gm}, M, N, K, p);
+  } else {
+    launch_gemm(c, GA3C_K_WGRAD, li, la, lb, EpiPartial{c->part, M, N}, M, N, K, p);
+    const std::size_t n = static_cast<std::size_t>(M) * N;
+    Launch l(c, GA3C_K_SPLITK, li);
+    splitk_grad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->part, p.splits, M, N, gm);
+  }
+}
+
+template <typename T>
+void layer_wgrad(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const float* dout, int B,
+                 long long in_stride) {
+  GradMap gm{c->grad, c->flag, L.w_off, L.b_off, 0, 0, L.out, L.in};
+  DenseT a{dout, L.out};  // (m = out channel, k = row) -> dout[row][m]
+  if (L.is_conv) {
+    WithOnes<Im2colB<T>> b;
+    static_cast<Im2col<T>&>(b.l) = im2col_of<T>(L, x_in, in_stride);
+    b.n_real = L.in;
+    wgrad_gemm(c, li, a, b, gm, L.out, L.in + 1, B * L.pixels());
+  } else {
+    WithOnes<DenseTIn<T>> b{
+        DenseTIn<T>{static_cast<const T*>(x_in), in_stride > 0 ? static_cast<int>(in_stride) : L.in},
+        L.in};
+    wgrad_gemm(c, li, a, b, gm, L.out, L.in + 1, B);
+  }
+}
+
+void layer_dgrad(ga3c_ctx* c, int li, const Layer& L, const float* theta, const float* dout,
+                 const float* gate, float* din, int B) {
+  if (L.is_conv) {
+    const std::size_t n = static_cast<std::size_t>(B) * L.ih * L.iw * L.cin;
+    Launch l(c, GA3C_K_DGRAD, li);
+    conv_dgrad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(
+        dout, theta + L.w_off, gate, din, B, L.ih, L.iw, L.cin, L.oh, L.ow, L.cout, L.k, L.stride);
+  } else {
+    DenseK a{dout, L.out};
+    DenseT w{theta + L.w_off, L.in};  // (n = i, k = o) -> W[o][i]
+    launch_gemm(c, GA3C_K_DGRAD, li, a, w, EpiGate{din, gate, L.in}, B, L.in, L.out,
+                plan_splits(B, L.in, L.out, false));
+  }
+}
+
+// ------------------------------------------------------------- forward
+
+__global__ void widen_u8_kernel(const uint8_t* __restrict__ x, float* __restrict__ y, std::size_t n) {
+  const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = static_cast<float>(x[i]) * (1.0f / 256.0f);
+}
+
+int run_forward(ga3c_ctx* c, const float* theta, const void* d_in, bool u8, int B,
+                long long in_stride = 0) {
+  const Layout& lo = c->m->lo;
+  const void* x = d_in;
+  bool x_u8 = u8;
+  int n_split = 0;
+  for (int li = 0; li < lo.n_trunk; ++li) {
+    const Layer& L = lo.trunk[li];
+    const bool last = li == lo.n_trunk - 1;
+    if (L.is_conv) {
+      if (x_u8)
+        conv_forward<uint8_t>(c, li, L, theta, x, c->act[li], B, li == 0 ? in_stride : 0);
+      else
+        conv_forward<float>(c, li, L, theta, x, c->act[li], B, li == 0 ? in_stride : 0);
+    } else {
+      const long long st = li == 0 ? in_stride : 0;
+      int s = x_u8 ? fc_forward<uint8_t>(c, li, L, theta, x, c->act[li], B, last, st)
+                   : fc_forward<float>(c, li, L, theta, x, c->act[li], B, last, st);
+      if (last) n_split = s;
+    }
+    x = c->act[li];
+    x_u8 = false;
+  }
+  const int D = lo.head_in();
+  const int A = lo.n_actions;
+  const float* part = nullptr;
+  const float* fc_bias = nullptr;
+  float* h = nullptr;
+  if (lo.n_trunk == 0) {
+    if (u8) {
+      // raw u8 input feeds the heads directly: widen once (k/256 is exact)
+      const std::size_t n = static_cast<std::size_t>(B) * D;
+      Launch l(c, GA3C_K_OTHER, -1);
+      widen_u8_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(
+          static_cast<const uint8_t*>(d_in), c->hin, n);
+      h = c->hin;
+    } else {
+      h = const_cast<float*>(static_cast<const float*>(d_in));
+    }
+  } else {
+    h = c->act[lo.n_trunk - 1];
+    if (!lo.trunk[lo.n_trunk - 1].is_conv) {
+      part = c->part;
+      fc_bias = theta + lo.trunk[lo.n_trunk - 1].b_off;
+    }
+  }
+  const std::size_t smem = (static_cast<std::size_t>(D) + 8 * (A + 1)) * sizeof(float);
+  {
+    Launch l(c, GA3C_K_HEADS, -1);
+    heads_forward_kernel<<<B, 256, smem, c->stream>>>(part, n_split, fc_bias, h, B, D, theta,
+                                                      lo.policy.w_off, lo.policy.b_off, lo.value.w_off,
+                                                      lo.value.b_off, A, c->pi32, c->pi64, c->v, c->v64);
+  }
+  return GA3C_OK;
+}
+
+int run_loss_grad(ga3c_ctx* c, const float* theta, const void* d_in, bool u8, const int32_t* d_act,
+                  const double* d_rets, int B, bool apply_clip, long long in_stride = 0) {
+  ga3c_model* m = c->m;
+  const Layout& lo = m->lo;
+  const int D = lo.head_in();
+  const int A = lo.n_actions;
+  cudaMemsetAsync(c->flag, 0, sizeof(int), c->stream);
+  run_forward(c, theta, d_in, u8, B, in_stride);
+  const float* h = lo.n_trunk ? c->act[lo.n_trunk - 1]
+                              : (u8 ? c->hin : static_cast<const float*>(d_in));
+  float* dh = lo.n_trunk ? c->dx[0] : nullptr;
+  {
+    Launch l(c, GA3C_K_LOSS_BWD, -1);
+    loss_heads_bwd_kernel<<<B, lo.n_trunk ? 256 : 32, 0, c->stream>>>(
+        c->pi64, c->v, d_act, d_rets, h, B, lo.n_trunk ? D : 0, A, theta, lo.policy.w_off,
+        lo.value.w_off, m->hp.beta, m->hp.eps_log, m->hp.value_loss_weight, c->dhead, dh, c->scal);
+  }
+  // heads weight gradient: [A+1][D+1] = dhead^T [h | 1]
+  {
+    GradMap gm{c->grad, c->flag, lo.policy.w_off, lo.policy.b_off, lo.value.w_off, lo.value.b_off, A, D};
+    DenseT a{c->dhead, A + 1};
+    WithOnes<DenseT> b{DenseT{h, D}, D};
+    wgrad_gemm(c, -1, a, b, gm, A + 1, D + 1, B);
+  }
+  int cur = 0;
+  for (int li = lo.n_trunk - 1; li >= 0; --li) {
+    const Layer& L = lo.trunk[li];
+    const void* x_in = li == 0 ? d_in : c->act[li - 1];
+    const bool in_u8 = li == 0 && u8;
+    const long long st = li == 0 ? in_stride : 0;
+    if (in_u8)
+      layer_wgrad<uint8_t>(c, li, L, x_in, c->dx[cur], B, st);
+    else
+      layer_wgrad<float>(c, li, L, x_in, c->dx[cur], B, st);
+    if (li > 0) {
+      layer_dgrad(c, li, L, theta, c->dx[cur], c->act[li - 1], c->dx[cur ^ 1], B);
+      cur ^= 1;
+    }
+  }
+  {
+    Launch l(c, GA3C_K_OTHER, -1);
+    scalars_kernel<<<1, 32, 0, c->stream>>>(c->scal, B, c->scal_sum);
+  }
+  if (apply_clip && m->hp.grad_clip_norm > 0.0) {
+    {
+      Launch l(c, GA3C_K_OTHER, -1);
+      sumsq_kernel<<<kNumSMs, 256, 0, c->stream>>>(c->grad, lo.total, c->clip_part);
+    }
+    Launch l(c, GA3C_K_OTHER, -1);
+    clip_scale_kernel<<<kNumSMs, 256, 0, c->stream>>>(c->grad, lo.total, c->clip_part, kNumSMs,
+                                                      m->hp.grad_clip_norm);
+  }
+  return GA3C_OK;
+}
+
+void launch_rmsprop(ga3c_ctx* c, const Slot& src, const Slot& dst, unsigned long long* ver) {
+  const ga3c_hyper& hp = c->m->hp;
+  const std::size_t n = c->m->lo.total;
+  const float alpha = static_cast<float>(hp.alpha);
+  const float oma = static_cast<float>(1.0 - hp.alpha);
+  const std::size_t n4 = (n + 3) / 4;
+  unsigned blocks = (unsigned)std::min<std::size_t>((n4 + 255) / 256, 8 * kNumSMs);
+  if (blocks == 0) blocks = 1;
+  Launch l(c, GA3C_K_RMSPROP, -1);
+  rmsprop_kernel<<<blocks, 256, 0, c->stream>>>(src.theta, src.g, c->grad, dst.theta, dst.g, n,
+                                                c->flag, ver, alpha, oma, static_cast<float>(hp.eta),
+                                                static_cast<float>(hp.eps_rms));
+}
+
+int set_device(ga3c_model* m) {
+  if (cudaSetDevice(m->device) != cudaSuccess) return GA3C_CUDA_ERROR;
+  return GA3C_OK;
+}
+
+// Allocates (or reuses) a slot with no readers that is not the current one.
+// Caller holds update_m and read_m.
+int free_slot_locked(ga3c_model* m) {
+  for (int i = 0; i < (int)m->slots.size(); ++i)
+    if (i != m->cur && m->slots[i].refs == 0) return i;
+  Slot s;
+  const std::size_t bytes = m->lo.total * sizeof(float);
+  if (cudaMalloc(&s.theta, bytes) != cudaSuccess) return -1;
+  if (cudaMalloc(&s.g, bytes) != cudaSuccess) {
+    cudaFree(s.theta);
+    return -1;
+  }
+  m->slots.push_back(s);
+  return (int)m->slots.size() - 1;
+}
+
+bool all_finite(const float* x, std::size_t n) {
+  for (std::size_t i = 0; i < n; ++i)
+    if (!std::isfinite(x[i])) return false;
+  return true;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+
+extern "C" {
+
+const char* ga3c_status_string(int s) {
+  switch (s) {
+    case GA3C_OK: return "ok";
+    case GA3C_INVALID_ARGUMENT: return "invalid argument";
+    case GA3C_NONFINITE_INPUT: return "non-finite input";
+    case GA3C_CUDA_ERROR: return "cuda error";
+    case GA3C_NCCL_ERROR: return "nccl error";
+    case GA3C_NOT_APPLIED: return "update not applied (non-finite gradient)";
+    case GA3C_OUT_OF_MEMORY: return "out of memory";
+    default: return "unknown status";
+  }
+}
+
+
+void ga3c_default_hyper(ga3c_hyper* hp) {
+  hp->gamma = 0.99;
+  hp->t_max = 5;
+  hp->beta = 0.01;
+  hp->eps_log = 1e-6;
+  hp->eta = 3e-4;
+  hp->alpha = 0.99;
+  hp->eps_rms = 1e-8;
+  hp->value_loss_weight = 0.5;
+  hp->grad_clip_norm = 0.0;
+  hp->clip_rewards = 0;
+}
+
+int ga3c_validate_spec(const ga3c_net_spec* s) {
+  if (!s) return GA3C_INVALID_ARGUMENT;
+  return validate_spec(*s);
+}
+
+int ga3c_validate_hyper(const ga3c_hyper* hp) {
+  if (!hp) return GA3C_INVALID_ARGUMENT;
+  return validate_hyper(*hp);
+}
+
+size_t ga3c_param_count(const ga3c_net_spec* s) {
+  if (!s || validate_spec(*s) != GA3C_OK) return 0;
+  return layout_of(*s).total;
+}
+
+size_t ga3c_input_dim(const ga3c_net_spec* s) {
+  if (!s) return 0;
+  return static_cast<size_t>(s->in_h) * s->in_w * s->in_c;
+}
+
+int ga3c_init_params(const ga3c_net_spec* s, uint64_t seed, double* theta64, float* theta32) {
+  if (!s || validate_spec(*s) != GA3C_OK) return GA3C_INVALID_ARGUMENT;
+  const Layout lo = layout_of(*s);
+  std::vector<double> t(lo.total);
+  init_params(lo, seed, t.data());
+  if (theta64) std::memcpy(theta64, t.data(), lo.total * sizeof(double));
+  if (theta32)
+    for (std::size_t i = 0; i < lo.total; ++i) theta32[i] = static_cast<float>(t[i]);
+  return GA3C_OK;
+}
+
+ga3c_model* ga3c_model_create(const ga3c_net_spec* spec, const ga3c_hyper* hp, int device,
+                              int* status) {
+  auto fail = [&](int st, const char* msg) -> ga3c_model* {
+    g_tls_error = msg;
+    if (status) *status = st;
+    return nullptr;
+  };
+  if (!spec || !hp) return fail(GA3C_INVALID_ARGUMENT, "null spec/hyper");
+  if (validate_spec(*spec) != GA3C_OK) return fail(GA3C_INVALID_ARGUMENT, "invalid NetworkSpec");
+  if (validate_hyper(*hp) != GA3C_OK) return fail(GA3C_INVALID_ARGUMENT, "invalid Hyperparams");
+  if (spec->n_actions > kMaxActions) return fail(GA3C_INVALID_ARGUMENT, "n_actions > 64 unsupported");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return fail(GA3C_CUDA_ERROR, "no CUDA device (this library has no CPU path)");
+  cudaDeviceProp prop{};
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10)
+    return fail(GA3C_CUDA_ERROR, "device is not sm_100 (B200)");
+  if (cudaSetDevice(device) != cudaSuccess) return fail(GA3C_CUDA_ERROR, "cudaSetDevice failed");
+  auto* m = new ga3c_model();
+  m->spec = *spec;
+  m->hp = *hp;
+  m->lo = layout_of(*spec);
+  m->device = device;
+  Slot s;
+  const std::size_t bytes = m->lo.total * sizeof(float);
+  if (cudaMalloc(&s.theta, bytes) != cudaSuccess || cudaMalloc(&s.g, bytes) != cudaSuccess ||
+      cudaMemset(s.theta, 0, bytes) != cudaSuccess || cudaMemset(s.g, 0, bytes) != cudaSuccess) {
+    delete m;
+    return fail(GA3C_OUT_OF_MEMORY, "parameter allocation failed");
+  }
+  m->slots.push_back(s);
+  m->cur = 0;
+  if (status) *status = GA3C_OK;
+  return m;
+}
+
+void ga3c_model_destroy(ga3c_model* m) {
+  if (!m) return;
+  cudaSetDevice(m->device);
+  for (auto& s : m->slots) {
+    cudaFree(s.theta);
+    cudaFree(s.g);
+  }
+  delete m;
+}
+
+int ga3c_model_load(ga3c_model* m, const float* theta, const float* g, uint64_t version) {
+  if (!m || !theta) return GA3C_INVALID_ARGUMENT;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  if (set_device(m)) return GA3C_CUDA_ERROR;
+  std::lock_guard<std::mutex> ulk(m->update_m);
+  int f;
+  {
+    std::lock_guard<std::mutex> lk(m->read_m);
+    f = free_slot_locked(m);
+  }
+  if (f < 0) return GA3C_OUT_OF_MEMORY;
+  const std::size_t bytes = m->lo.total * sizeof(float);
+  GA3C_CUDA(cudaMemcpy(m->slots[f].theta, theta, bytes, cudaMemcpyHostToDevice));
+  if (g)
+    GA3C_CUDA(cudaMemcpy(m->slots[f].g, g, bytes, cudaMemcpyHostToDevice));
+  else
+    GA3C_CUDA(cudaMemset(m->slots[f].g, 0, bytes));
+  std::lock_guard<std::mutex> lk(m->read_m);
+  m->slots[f].version = version;
+  m->cur = f;
+  return GA3C_OK;
+}
+
+int ga3c_model_read(ga3c_model* m, float* theta, float* g, uint64_t* version) {
+  if (!m) return GA3C_INVALID_ARGUMENT;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  if (set_device(m)) return GA3C_CUDA_ERROR;
+  int s;
+  uint64_t v;
+  if (ga3c_snapshot_acquire(m, &s, &v)) return GA3C_INVALID_ARGUMENT;
+  const std::size_t bytes = m->lo.total * sizeof(float);
+  int rc = GA3C_OK;
+  if (theta && cudaMemcpy(theta, m->slots[s].theta, bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+    rc = GA3C_CUDA_ERROR;
+  if (g && cudaMemcpy(g, m->slots[s].g, bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+    rc = GA3C_CUDA_ERROR;
+  if (version) *version = v;
+  ga3c_snapshot_release(m, s);
+  if (rc) set_err("ga3c_model_read: copy failed");
+  return rc;
+}
+
+uint64_t ga3c_model_version(ga3c_model* m) {
+  std::lock_guard<std::mutex> lk(m->read_m);
+  return m->slots[m->cur].version;
+}
+
+size_t ga3c_model_param_count(ga3c_model* m) { return m ? m->lo.total : 0; }
+
+int ga3c_snapshot_acquire(ga3c_model* m, int* slot, uint64_t* version) {
+  if (!m || !slot) return GA3C_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> lk(m->read_m);
+  *slot = m->cur;
+  m->slots[m->cur].refs++;
+  if (version) *version = m->slots[m->cur].version;
+  return GA3C_OK;
+}
+
+int ga3c_snapshot_release(ga3c_model* m, int slot) {
+  if (!m) return GA3C_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> lk(m->read_m);
+  if (slot < 0 || slot >= (int)m->slots.size() || m->slots[slot].refs <= 0)
+    return GA3C_INVALID_ARGUMENT;
+  m->slots[slot].refs--;
+  return GA3C_OK;
+}
+
+const char* ga3c_model_last_error(ga3c_model* m) {
+  if (!m) return g_tls_error.c_str();
+  std::lock_guard<std::mutex> lk(m->err_m);
+  return m->last_error.empty() ? g_tls_error.c_str() : m->last_error.c_str();
+}
+
+ga3c_ctx* ga3c_ctx_create(ga3c_model* m, int max_batch, int* status) {
+  if (!m || max_batch < 1) {
+    if (status) *status = GA3C_INVALID_ARGUMENT;
+    return nullptr;
+  }
+  if (set_device(m)) {
+    if (status) *status = GA3C_CUDA_ERROR;
+    return nullptr;
+  }
+  auto* c = new ga3c_ctx();
+  c->m = m;
+  c->max_batch = max_batch;
+  const Layout& lo = m->lo;
+  const std::size_t B = max_batch;
+  bool ok = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) == cudaSuccess;
+  auto alloc = [&](auto** p, std::size_t bytes) {
+    if (!ok) return;
+    ok = cudaMalloc(reinterpret_cast<void**>(p), std::max<std::size_t>(bytes, 16)) == cudaSuccess;
+  };
+  alloc(&c->d_in, B * lo.in_dim * sizeof(float));
+  for (int i = 0; i < lo.n_trunk; ++i) alloc(&c->act[i], B * lo.trunk[i].out_dim() * sizeof(float));
+  alloc(&c->dx[0], B * lo.max_act_dim() * sizeof(float));
+  alloc(&c->dx[1], B * lo.max_act_dim() * sizeof(float));
+  if (lo.n_trunk == 0) alloc(&c->hin, B * lo.in_dim * sizeof(float));
+  alloc(&c->pi32, B * lo.n_actions * sizeof(float));
+  alloc(&c->pi64, B * lo.n_actions * sizeof(double));
+  alloc(&c->v, B * sizeof(float));
+  alloc(&c->v64, B * sizeof(double));
+  alloc(&c->dhead, B * (lo.n_actions + 1) * sizeof(float));
+  alloc(&c->scal, B * 3 * sizeof(double));
+  alloc(&c->scal_sum, 3 * sizeof(double));
+  alloc(&c->d_actions, B * sizeof(int32_t));
+  alloc(&c->d_rets, B * sizeof(double));
+  alloc(&c->grad, lo.total * sizeof(float));
+  alloc(&c->flag, sizeof(int));
+  alloc(&c->dev_version, sizeof(unsigned long long));
+  alloc(&c->part, kPartFloats * sizeof(float));
+  alloc(&c->clip_part, kNumSMs * sizeof(double));
+  if (ok) ok = cudaMallocHost(&c->h_flag, sizeof(int)) == cudaSuccess;
+  if (ok) ok = cudaMemset(c->dev_version, 0, sizeof(unsigned long long)) == cudaSuccess;
+  if (ok) ok = cudaMemset(c->flag, 0, sizeof(int)) == cudaSuccess;
+  if (ok) {
+    const int max_smem = 200 * 1024;
+    ok = cudaFuncSetAttribute(heads_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              max_smem) == cudaSuccess;
+  }
+  if (!ok) {
+    g_tls_error = "ga3c_ctx_create: device allocation failed";
+    ga3c_ctx_destroy(c);
+    if (status) *status = GA3C_OUT_OF_MEMORY;
+    return nullptr;
+  }
+  if (status) *status = GA3C_OK;
+  return c;
+}
+
+void ga3c_ctx_destroy(ga3c_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->m->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  void* ps[] = {c->d_in, c->dx[0], c->dx[1], c->hin, c->pi32, c->pi64, c->v, c->v64, c->dhead, c->scal,
+                c->scal_sum, c->d_actions, c->d_rets, c->grad, c->flag, c->dev_version, c->part,
+                c->clip_part, c->r_rew, c->r_off, c->r_term, c->r_boot, c->r_out};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  for (auto* a : c->act)
+    if (a) cudaFree(a);
+  if (c->h_flag) cudaFreeHost(c->h_flag);
+  for (auto e : c->events) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+void* ga3c_ctx_stream(ga3c_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+int ga3c_ctx_sync(ga3c_ctx* c) {
+  if (!c) return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  GA3C_CUDA(cudaStreamSynchronize(c->stream));
+  GA3C_CUDA(cudaGetLastError());
+  return GA3C_OK;
+}
+
+uint64_t ga3c_ctx_launches(ga3c_ctx* c) { return c ? c->launches : 0; }
+
+static bool stride_ok(const ga3c_model* m, long long stride) {
+  if (stride == 0) return true;
+  if (stride < m->lo.in_dim) return false;
+  return m->lo.n_trunk > 0 || stride == m->lo.in_dim;
+}
+
+int ga3c_forward_dev(ga3c_ctx* c, int slot, const void* d_states, int states_are_u8,
+                     long long state_stride, int B, float* d_pi, float* d_v) {
+  if (!c || B < 0 || B > c->max_batch || slot < 0 || slot >= (int)c->m->slots.size() ||
+      !stride_ok(c->m, state_stride))
+    return GA3C_INVALID_ARGUMENT;
+  if (B == 0) return GA3C_OK;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  const float* theta = m->slots[slot].theta;
+  run_forward(c, theta, d_states, states_are_u8 != 0, B, state_stride);
+  const int A = m->lo.n_actions;
+  if (d_pi && d_pi != c->pi32)
+    GA3C_CUDA(cudaMemcpyAsync(d_pi, c->pi32, sizeof(float) * B * A, cudaMemcpyDeviceToDevice, c->stream));
+  if (d_v && d_v != c->v)
+    GA3C_CUDA(cudaMemcpyAsync(d_v, c->v, sizeof(float) * B, cudaMemcpyDeviceToDevice, c->stream));
+  GA3C_CUDA(cudaGetLastError());
+  return GA3C_OK;
+}
+
+static int forward_host(ga3c_ctx* c, int slot, const void* states, bool u8, int B, float* pi,
+                        float* v, uint64_t* version_used) {
+  if (!c || B < 0 || B > c->max_batch || (B > 0 && (!states || !pi || !v))) return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  const std::size_t dim = m->lo.in_dim;
+  if (!u8 && !all_finite(static_cast<const float*>(states), dim * B)) return GA3C_NONFINITE_INPUT;
+  if (set_device(m)) return GA3C_CUDA_ERROR;
+  int s = slot;
+  uint64_t ver = 0;
+  const bool pinned_here = slot < 0;
+  if (pinned_here) {
+    ga3c_snapshot_acquire(m, &s, &ver);
+  } else {
+    if (slot >= (int)m->slots.size()) return GA3C_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(m->read_m);
+    ver = m->slots[slot].version;
+  }
+  int rc = GA3C_OK;
+  if (B > 0) {
+    const std::size_t bytes = dim * B * (u8 ? 1 : sizeof(float));
+    if (cudaMemcpyAsync(c->d_in, states, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+      rc = GA3C_CUDA_ERROR;
+    if (!rc) run_forward(c, m->slots[s].theta, c->d_in, u8, B);
+    const int A = m->lo.n_actions;
+    if (!rc && cudaMemcpyAsync(pi, c->pi32, sizeof(float) * B * A, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+      rc = GA3C_CUDA_ERROR;
+    if (!rc && cudaMemcpyAsync(v, c->v, sizeof(float) * B, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+      rc = GA3C_CUDA_ERROR;
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+      rc = GA3C_CUDA_ERROR;
+      set_err(std::string("forward: ") + cudaGetErrorString(e));
+    }
+  }
+  if (pinned_here) ga3c_snapshot_release(m, s);
+  if (version_used) *version_used = ver;
+  return rc;
+}
+
+int ga3c_forward_u8(ga3c_ctx* c, int slot, const uint8_t* frames, int B, float* pi, float* v,
+                    uint64_t* version_used) {
+  return forward_host(c, slot, frames, true, B, pi, v, version_used);
+}
+
+int ga3c_forward_f32(ga3c_ctx* c, int slot, const float* states, int B, float* pi, float* v,
+                     uint64_t* version_used) {
+  return forward_host(c, slot, states, false, B, pi, v, version_used);
+}
+
+int ga3c_loss_grad_dev(ga3c_ctx* c, int slot, const void* d_states, int states_are_u8,
+                       long long state_stride, const int32_t* d_actions, const double* d_returns,
+                       int B, int apply_clip) {
+  if (!c || B < 1 || B > c->max_batch || slot < 0 || slot >= (int)c->m->slots.size() ||
+      !stride_ok(c->m, state_stride))
+    return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  run_loss_grad(c, m->slots[slot].theta, d_states, states_are_u8 != 0, d_actions, d_returns, B,
+                apply_clip != 0, state_stride);
+  GA3C_CUDA(cudaGetLastError());
+  return GA3C_OK;
+}
+
+static int loss_grad_host(ga3c_ctx* c, int slot, const void* states, bool u8,
+                          const int32_t* actions, const double* rets, int B, int apply_clip,
+                          float* dtheta, double* scalars) {
+  if (!c || B < 1 || B > c->max_batch || !states || !actions || !rets) return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  const std::size_t dim = m->lo.in_dim;
+  for (int b = 0; b < B; ++b) {
+    if (!std::isfinite(rets[b])) return GA3C_NONFINITE_INPUT;
+    if (actions[b] < 0 || actions[b] >= m->lo.n_actions) return GA3C_INVALID_ARGUMENT;
+  }
+  if (!u8 && !all_finite(static_cast<const float*>(states), dim * B)) return GA3C_NONFINITE_INPUT;
+  if (set_device(m)) return GA3C_CUDA_ERROR;
+  int s = slot;
+  const bool pinned_here = slot < 0;
+  if (pinned_here) ga3c_snapshot_acquire(m, &s, nullptr);
+  int rc = GA3C_OK;
+  const std::size_t bytes = dim * B * (u8 ? 1 : sizeof(float));
+  if (cudaMemcpyAsync(c->d_in, states, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+      cudaMemcpyAsync(c->d_actions, actions, sizeof(int32_t) * B, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+      cudaMemcpyAsync(c->d_rets, rets, sizeof(double) * B, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+    rc = GA3C_CUDA_ERROR;
+  if (!rc)
+    run_loss_grad(c, m->slots[s].theta, c->d_in, u8, c->d_actions, c->d_rets, B, apply_clip != 0);
+  if (!rc && dtheta &&
+      cudaMemcpyAsync(dtheta, c->grad, sizeof(float) * m->lo.total, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+    rc = GA3C_CUDA_ERROR;
+  if (!rc && scalars &&
+      cudaMemcpyAsync(scalars, c->scal_sum, sizeof(double) * 3, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+    rc = GA3C_CUDA_ERROR;
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    rc = GA3C_CUDA_ERROR;
+    set_err(std::string("loss_grad: ") + cudaGetErrorString(e));
+  }
+  if (pinned_here) ga3c_snapshot_release(m, s);
+  return rc;
+}
+
+int ga3c_loss_grad_u8(ga3c_ctx* c, int slot, const uint8_t* frames, const int32_t* actions,
+                      const double* returns, int B, int apply_clip, float* dtheta, double* scalars) {
+  return loss_grad_host(c, slot, frames, true, actions, returns, B, apply_clip, dtheta, scalars);
+}
+
+int ga3c_loss_grad_f32(ga3c_ctx* c, int slot, const float* states, const int32_t* actions,
+                       const double* returns, int B, int apply_clip, float* dtheta, double* scalars) {
+  return loss_grad_host(c, slot, states, false, actions, returns, B, apply_clip, dtheta, scalars);
+}
+
+float* ga3c_ctx_grad(ga3c_ctx* c) { return c ? c->grad : nullptr; }
+
+const double* ga3c_ctx_last_values(ga3c_ctx* c) { return c ? c->v64 : nullptr; }
+
+int ga3c_ctx_read_grad(ga3c_ctx* c, float* dtheta, double* scalars) {
+  if (!c) return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  if (dtheta)
+    GA3C_CUDA(cudaMemcpyAsync(dtheta, c->grad, sizeof(float) * m->lo.total, cudaMemcpyDeviceToHost, c->stream));
+  if (scalars)
+    GA3C_CUDA(cudaMemcpyAsync(scalars, c->scal_sum, sizeof(double) * 3, cudaMemcpyDeviceToHost, c->stream));
+  GA3C_CUDA(cudaStreamSynchronize(c->stream));
+  return GA3C_OK;
+}
+
+int ga3c_clip_grad(ga3c_ctx* c) {
+  if (!c) return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  if (m->hp.grad_clip_norm > 0.0) {
+    {
+      Launch l(c, GA3C_K_OTHER, -1);
+      sumsq_kernel<<<kNumSMs, 256, 0, c->stream>>>(c->grad, m->lo.total, c->clip_part);
+    }
+    Launch l(c, GA3C_K_OTHER, -1);
+    clip_scale_kernel<<<kNumSMs, 256, 0, c->stream>>>(c->grad, m->lo.total, c->clip_part, kNumSMs,
+                                                      m->hp.grad_clip_norm);
+  }
+  GA3C_CUDA(cudaGetLastError());
+  return GA3C_OK;
+}
+
+int ga3c_apply_rmsprop(ga3c_ctx* c, const float* dtheta, int* applied, uint64_t* applied_on) {
+  if (!c) return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  if (set_device(m)) return GA3C_CUDA_ERROR;
+  const std::size_t n = m->lo.total;
+  std::lock_guard<std::mutex> ulk(m->update_m);
+  int src, dst;
+  {
+    std::lock_guard<std::mutex> lk(m->read_m);
+    src = m->cur;
+    m->slots[src].refs++;
+    dst = free_slot_locked(m);
+  }
+  auto unpin = [&]() {
+    std::lock_guard<std::mutex> lk(m->read_m);
+    m->slots[src].refs--;
+  };
+  if (dst < 0) {
+    unpin();
+    return GA3C_OUT_OF_MEMORY;
+  }
+  if (dtheta) {
+    // host gradient: upload and recompute the non-finite flag on the device
+    if (cudaMemcpyAsync(c->grad, dtheta, n * sizeof(float), cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+        cudaMemsetAsync(c->flag, 0, sizeof(int), c->stream) != cudaSuccess) {
+      unpin();
+      set_err("apply_rmsprop: upload failed");
+      return GA3C_CUDA_ERROR;
+    }
+    Launch l(c, GA3C_K_OTHER, -1);
+    check_finite_kernel<<<kNumSMs, 256, 0, c->stream>>>(c->grad, n, c->flag);
+  }
+  launch_rmsprop(c, m->slots[src], m->slots[dst], nullptr);
+  cudaMemcpyAsync(c->h_flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    unpin();
+    set_err(std::string("apply_rmsprop: ") + cudaGetErrorString(e));
+    return GA3C_CUDA_ERROR;
+  }
+  if (*c->h_flag) {
+    unpin();
+    if (applied) *applied = 0;
+    return GA3C_NOT_APPLIED;
+  }
+  {
+    std::lock_guard<std::mutex> lk(m->read_m);
+    m->slots[dst].version = m->slots[src].version + 1;
+    if (applied_on) *applied_on = m->slots[src].version;
+    m->cur = dst;
+    m->slots[src].refs--;
+  }
+  if (applied) *applied = 1;
+  return GA3C_OK;
+}
+
+int ga3c_apply_rmsprop_dev(ga3c_ctx* c) {
+  if (!c) return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  Slot& s = m->slots[m->cur];
+  launch_rmsprop(c, s, s, c->dev_version);
+  GA3C_CUDA(cudaGetLastError());
+  return GA3C_OK;
+}
+
+int ga3c_ctx_read_dev_version(ga3c_ctx* c, uint64_t* version) {
+  if (!c || !version) return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  unsigned long long v = 0;
+  GA3C_CUDA(cudaMemcpyAsync(&v, c->dev_version, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
+  GA3C_CUDA(cudaStreamSynchronize(c->stream));
+  *version = v;
+  return GA3C_OK;
+}
+
+int ga3c_compute_returns_dev(ga3c_ctx* c, const double* d_rewards, const int32_t* d_off, int n_seg,
+                             const uint8_t* d_terminal, const double* d_bootstrap, double gamma,
+                             double* d_out) {
+  if (!c || n_seg < 0) return GA3C_INVALID_ARGUMENT;
+  if (!(gamma > 0.0) || gamma > 1.0) return GA3C_INVALID_ARGUMENT;
+  if (n_seg == 0) return GA3C_OK;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  {
+    Launch l(c, GA3C_K_RETURNS, -1);
+    returns_kernel<<<(n_seg + 127) / 128, 128, 0, c->stream>>>(d_rewards, d_off, n_seg, d_terminal,
+                                                               d_bootstrap, gamma, d_out);
+  }
+  GA3C_CUDA(cudaGetLastError());
+  return GA3C_OK;
+}
+
+int ga3c_compute_returns(ga3c_ctx* c, const double* rewards, const int32_t* off, int n_seg,
+                         const uint8_t* terminal, const double* bootstrap, double gamma,
+                         double* out) {
+  if (!c || n_seg < 1 || !rewards || !off || !terminal || !bootstrap || !out)
+    return GA3C_INVALID_ARGUMENT;
+  if (!(gamma > 0.0) || gamma > 1.0) return GA3C_INVALID_ARGUMENT;  // returns.cpp:11-12
+  if (off[0] != 0) return GA3C_INVALID_ARGUMENT;
+  for (int s = 0; s < n_seg; ++s) {
+    if (off[s + 1] <= off[s]) return GA3C_INVALID_ARGUMENT;  // empty segment, returns.cpp:10
+    if (!terminal[s] && !std::isfinite(bootstrap[s])) return GA3C_NONFINITE_INPUT;
+  }
+  const int n = off[n_seg];
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(rewards[i])) return GA3C_NONFINITE_INPUT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  if (set_device(m)) return GA3C_CUDA_ERROR;
+  if ((std::size_t)n > c->r_cap) {
+    cudaFree(c->r_rew);
+    cudaFree(c->r_out);
+    c->r_cap = std::max<std::size_t>(n, 1024);
+    GA3C_CUDA(cudaMalloc(&c->r_rew, c->r_cap * sizeof(double)));
+    GA3C_CUDA(cudaMalloc(&c->r_out, c->r_cap * sizeof(double)));
+  }
+  if ((std::size_t)n_seg > c->r_seg_cap) {
+    cudaFree(c->r_off);
+    cudaFree(c->r_term);
+    cudaFree(c->r_boot);
+    c->r_seg_cap = std::max<std::size_t>(n_seg, 256);
+    GA3C_CUDA(cudaMalloc(&c->r_off, (c->r_seg_cap + 1) * sizeof(int32_t)));
+    GA3C_CUDA(cudaMalloc(&c->r_term, c->r_seg_cap));
+    GA3C_CUDA(cudaMalloc(&c->r_boot, c->r_seg_cap * sizeof(double)));
+  }
+  GA3C_CUDA(cudaMemcpyAsync(c->r_rew, rewards, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  GA3C_CUDA(cudaMemcpyAsync(c->r_off, off, (n_seg + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+  GA3C_CUDA(cudaMemcpyAsync(c->r_term, terminal, n_seg, cudaMemcpyHostToDevice, c->stream));
+  GA3C_CUDA(cudaMemcpyAsync(c->r_boot, bootstrap, n_seg * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  int rc = ga3c_compute_returns_dev(c, c->r_rew, c->r_off, n_seg, c->r_term, c->r_boot, gamma, c->r_out);
+  if (rc) return rc;
+  GA3C_CUDA(cudaMemcpyAsync(out, c->r_out, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  GA3C_CUDA(cudaStreamSynchronize(c->stream));
+  return GA3C_OK;
+}
+
+int ga3c_sample_actions_dev(ga3c_ctx* c, const float* d_pi, const double* d_u, int B, int A,
+                            int32_t* d_actions, int action_stride) {
+  if (action_stride < 1) action_stride = 1;
+  if (!c || B < 0 || A < 1) return GA3C_INVALID_ARGUMENT;
+  if (B == 0) return GA3C_OK;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  // the context's own fp64 policy when the caller passes its last output
+  const double* pi64 = (d_pi == nullptr || d_pi == c->pi32) ? c->pi64 : nullptr;
+  {
+    Launch l(c, GA3C_K_SAMPLE, -1);
+    sample_kernel<<<(B + 127) / 128, 128, 0, c->stream>>>(d_pi, pi64, d_u, B, A, d_actions,
+                                                          action_stride);
+  }
+  GA3C_CUDA(cudaGetLastError());
+  return GA3C_OK;
+}
+
+int ga3c_ctx_time_kernel(ga3c_ctx* c, int tag, int layer) {
+  if (!c || tag < 0 || tag > GA3C_K_OTHER) return GA3C_INVALID_ARGUMENT;
+  c->timed_tag = tag;
+  c->timed_layer = layer;
+  c->ev_used = 0;
+  return GA3C_OK;
+}
+
+int ga3c_ctx_kernel_time(ga3c_ctx* c, double* total_ms, uint64_t* launches) {
+  if (!c) return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  GA3C_CUDA(cudaStreamSynchronize(c->stream));
+  double tot = 0.0;
+  for (std::size_t i = 0; i + 1 < c->ev_used; i += 2) {
+    float ms = 0.0f;
+    GA3C_CUDA(cudaEventElapsedTime(&ms, c->events[i], c->events[i + 1]));
+    tot += ms;
+  }
+  if (total_ms) *total_ms = tot;
+  if (launches) *launches = c->ev_used / 2;
+  c->ev_used = 0;
+  return GA3C_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,360 @@
+// kernels.cu -- the non-GEMM kernels of the GA3C hot path (sm_100a).
+//
+//   heads_forward_kernel   FC finalize (split-K reduce + bias + ReLU) fused with
+//                          the policy/value heads and the max-subtracted softmax
+//                          (nnet.cpp:96-117)
+//   loss_heads_bwd_kernel  per-sample A3C loss terms, dL/dpi, softmax Jacobian,
+//                          dV, and the heads' input gradient with the ReLU gate
+//                          (nnet.cpp:229-270)
+//   conv_dgrad_kernel      gather-form col2im of a VALID conv, gated by the
+//                          previous layer's activation (nnet.cpp:267-278)
+//   splitk_* kernels       fixed-order split-K reductions (deterministic)
+//   scalars / clip         loss diagnostics and the optional global-norm clip
+//                          (nnet.cpp:233-235, 281-289)
+//   rmsprop_kernel         fused vectorised non-centred RMSProp with the
+//                          non-finite reject gate (nnet.cpp:293-312)
+//   returns_kernel         n-step returns, fp64 without contraction (returns.cpp:21-24)
+//   sample_kernel          inverse-CDF action sampling (util.hpp:46-54)
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace ga3c {
+
+namespace {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ heads
+// One CTA per sample.  h = ReLU(sum_s part[s][b][:] + bias) when the last
+// trunk layer is an FC whose split-K partials are handed over (part != null),
+// else h is read from h_in.  Then logits/value in fp32 (fixed-order block
+// reduction) and the softmax in fp64: pi64 (internal, for the loss and the
+// sampler) and pi32 (API output).
+__global__ void __launch_bounds__(256)
+heads_forward_kernel(const float* __restrict__ part, int n_split, const float* __restrict__ fc_bias,
+                     float* __restrict__ h_io, int B, int D, const float* __restrict__ theta,
+                     std::size_t wp_off, std::size_t bp_off, std::size_t wv_off, std::size_t bv_off,
+                     int A, float* __restrict__ pi32, double* __restrict__ pi64,
+                     float* __restrict__ v_out, double* __restrict__ v64_out) {
+  extern __shared__ float sm[];
+  float* h = sm;                // D
+  float* red = sm + D;          // [8 warps][A+1]
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float* hrow = h_io + static_cast<std::size_t>(b) * D;
+  for (int o = tid; o < D; o += blockDim.x) {
+    float v;
+    if (part) {
+      float s = 0.0f;
+      for (int k = 0; k < n_split; ++k) s += part[(static_cast<std::size_t>(k) * B + b) * D + o];
+      v = s + fc_bias[o];
+      v = v < 0.0f ? 0.0f : v;
+      hrow[o] = v;
+    } else {
+      v = hrow[o];
+    }
+    h[o] = v;
+  }
+  __syncthreads();
+  for (int j = 0; j <= A; ++j) {
+    const float* w = theta + (j < A ? wp_off + static_cast<std::size_t>(j) * D : wv_off);
+    float s = 0.0f;
+    for (int o = tid; o < D; o += blockDim.x) s = fmaf(w[o], h[o], s);
+    s = warp_sum(s);
+    if (lane == 0) red[warp * (A + 1) + j] = s;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // lanes j < A+1 finish the dot products in warp order, then lane 0 does
+    // the softmax in fp64 (A is small).
+    __shared__ double logit_sh[64];
+    for (int j = lane; j <= A; j += 32) {
+      float s = 0.0f;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w * (A + 1) + j];
+      const float bias = j < A ? theta[bp_off + j] : theta[bv_off];
+      const float z = s + bias;
+      if (j < A)
+        logit_sh[j] = z;
+      else {
+        v_out[b] = z;
+        v64_out[b] = z;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      double m = logit_sh[0];
+      for (int j = 1; j < A; ++j)
+        if (m < logit_sh[j]) m = logit_sh[j];
+      double z = 0.0;
+      double e[64];
+      for (int j = 0; j < A; ++j) {
+        e[j] = exp(logit_sh[j] - m);
+        z += e[j];
+      }
+      for (int j = 0; j < A; ++j) {
+        const double p = e[j] / z;
+        pi64[static_cast<std::size_t>(b) * A + j] = p;
+        pi32[static_cast<std::size_t>(b) * A + j] = static_cast<float>(p);
+      }
+    }
+  }
+}
+
+// -------------------------------------------------------- loss + heads bwd
+// One CTA per sample.  fp64 loss algebra (nnet.cpp:231-254) from pi64 and V,
+// then dh = W_p^T dlogits + W_v dV in fp32, gated by h <= 0.  Writes the
+// per-sample head gradients dhead[b][0..A] (= dlogits, dV) for the heads'
+// weight-gradient GEMM and the per-sample loss scalars.
+__global__ void __launch_bounds__(256)
+loss_heads_bwd_kernel(const double* __restrict__ pi64, const float* __restrict__ v,
+                      const int32_t* __restrict__ actions, const double* __restrict__ rets,
+                      const float* __restrict__ h, int B, int D, int A,
+                      const float* __restrict__ theta, std::size_t wp_off, std::size_t wv_off,
+                      double beta, double eps, double c_v, float* __restrict__ dhead,
+                      float* __restrict__ dh, double* __restrict__ scal) {
+  __shared__ float g_sh[65];
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    const double* p = pi64 + static_cast<std::size_t>(b) * A;
+    const int a = actions[b];
+    const double adv = rets[b] - static_cast<double>(v[b]);
+    const double pa = p[a];
+    double H = 0.0;
+    for (int k = 0; k < A; ++k) H -= p[k] * log(p[k] + eps);  // eps > 0 (validated)
+    scal[3 * b + 0] = -log(pa + eps) * adv - beta * H;
+    scal[3 * b + 1] = adv * adv;
+    scal[3 * b + 2] = H;
+    double dpol[64];
+    for (int k = 0; k < A; ++k) dpol[k] = beta * (log(p[k] + eps) + p[k] / (p[k] + eps));
+    dpol[a] += -adv / (pa + eps);
+    double dot = 0.0;
+    for (int k = 0; k < A; ++k) dot += dpol[k] * p[k];
+    for (int j = 0; j < A; ++j) {
+      const float g = static_cast<float>(p[j] * (dpol[j] - dot));
+      g_sh[j] = g;
+      dhead[static_cast<std::size_t>(b) * (A + 1) + j] = g;
+    }
+    const float dvv = static_cast<float>(-2.0 * c_v * adv);
+    g_sh[A] = dvv;
+    dhead[static_cast<std::size_t>(b) * (A + 1) + A] = dvv;
+  }
+  __syncthreads();
+  const float* hrow = h + static_cast<std::size_t>(b) * D;
+  float* drow = dh + static_cast<std::size_t>(b) * D;
+  for (int o = tid; o < D; o += blockDim.x) {
+    float s = 0.0f;
+    for (int j = 0; j < A; ++j) s = fmaf(g_sh[j], theta[wp_off + static_cast<std::size_t>(j) * D + o], s);
+    s = fmaf(g_sh[A], theta[wv_off + o], s);
+    drow[o] = hrow[o] <= 0.0f ? 0.0f : s;
+  }
+}
+
+// Fixed-order batch sums of the per-sample diagnostics (nnet.cpp:233-235).
+__global__ void scalars_kernel(const double* __restrict__ scal, int B, double* __restrict__ out) {
+  if (threadIdx.x < 3) {
+    double s = 0.0;
+    for (int b = 0; b < B; ++b) s += scal[3 * b + threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+}
+
+// ------------------------------------------------------------ conv dgrad
+// din[b][y][x][ci] = gate > 0 ? sum_{ky,kx,co} dout[b][oy][ox][co] W[co][ky][kx][ci] : 0
+// over the (ky, kx) with y = oy*s + ky, x = ox*s + kx inside the output.
+__global__ void __launch_bounds__(256)
+conv_dgrad_kernel(const float* __restrict__ dout, const float* __restrict__ W,
+                  const float* __restrict__ gate, float* __restrict__ din, int B, int ih, int iw,
+                  int cin, int oh, int ow, int cout, int k, int s) {
+  const std::size_t total = static_cast<std::size_t>(B) * ih * iw * cin;
+  const std::size_t idx = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  if (gate[idx] <= 0.0f) {
+    din[idx] = 0.0f;
+    return;
+  }
+  const int ci = static_cast<int>(idx % cin);
+  std::size_t r = idx / cin;
+  const int x = static_cast<int>(r % iw);
+  r /= iw;
+  const int y = static_cast<int>(r % ih);
+  const int b = static_cast<int>(r / ih);
+  float acc = 0.0f;
+  for (int ky = y % s; ky < k; ky += s) {
+    const int oy = (y - ky) / s;
+    if (oy < 0 || oy >= oh) continue;
+    for (int kx = x % s; kx < k; kx += s) {
+      const int ox = (x - kx) / s;
+      if (ox < 0 || ox >= ow) continue;
+      const float* g = dout + ((static_cast<std::size_t>(b) * oh + oy) * ow + ox) * cout;
+      const float* w = W + (static_cast<std::size_t>(ky) * k + kx) * cin + ci;
+      const std::size_t wstride = static_cast<std::size_t>(k) * k * cin;
+      for (int co = 0; co < cout; ++co) acc = fmaf(__ldg(g + co), __ldg(w + co * wstride), acc);
+    }
+  }
+  din[idx] = acc;
+}
+
+// ------------------------------------------------------- split-K reductions
+__global__ void splitk_bias_relu_kernel(const float* __restrict__ part, int n_split, int M, int N,
+                                        const float* __restrict__ bias, float* __restrict__ out) {
+  const std::size_t total = static_cast<std::size_t>(M) * N;
+  const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  float s = 0.0f;
+  for (int k = 0; k < n_split; ++k) s += part[k * total + i];
+  const float v = s + bias[i % N];
+  out[i] = v < 0.0f ? 0.0f : v;
+}
+
+__global__ void splitk_grad_kernel(const float* __restrict__ part, int n_split, int M, int N,
+                                   GradMap g) {
+  const std::size_t total = static_cast<std::size_t>(M) * N;
+  const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  float s = 0.0f;
+  for (int k = 0; k < n_split; ++k) s += part[k * total + i];
+  g.store(static_cast<int>(i / N), static_cast<int>(i % N), s);
+}
+
+// -------------------------------------------------------------- clipping
+__global__ void sumsq_kernel(const float* __restrict__ g, std::size_t n, double* __restrict__ part) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const double x = g[i];
+    s += x * x;
+  }
+  s = warp_sum_d(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void clip_scale_kernel(float* __restrict__ g, std::size_t n, const double* __restrict__ part,
+                                  int n_part, double clip) {
+  __shared__ double scale_sh;
+  if (threadIdx.x == 0) {
+    double sq = 0.0;
+    for (int i = 0; i < n_part; ++i) sq += part[i];
+    const double norm = sqrt(sq);
+    scale_sh = norm > clip ? clip / norm : 1.0;
+  }
+  __syncthreads();
+  const double scale = scale_sh;
+  if (scale == 1.0) return;
+  for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x)
+    g[i] = static_cast<float>(static_cast<double>(g[i]) * scale);
+}
+
+// --------------------------------------------------------------- rmsprop
+// g' = alpha*g + ((1-alpha)*d)*d ; theta' = theta - (eta*d)/sqrt(g' + eps)
+// One IEEE rounding per operation (explicit _rn intrinsics, no contraction),
+// matching orc_rmsprop_update_f32 bit for bit.  20 B/param of HBM traffic.
+// If *flag is set (a non-finite gradient component) the step is rejected and
+// nothing is written (nnet.cpp:299-301).  Out-of-place or in place.
+__device__ __forceinline__ void rms1(float& th, float& g, float d, float alpha, float oma, float eta,
+                                     float eps) {
+  const float acc = __fadd_rn(__fmul_rn(alpha, g), __fmul_rn(__fmul_rn(oma, d), d));
+  g = acc;
+  th = __fsub_rn(th, __fdiv_rn(__fmul_rn(eta, d), __fsqrt_rn(__fadd_rn(acc, eps))));
+}
+
+__global__ void __launch_bounds__(256)
+rmsprop_kernel(const float* __restrict__ th_in, const float* __restrict__ g_in,
+               const float* __restrict__ d, float* __restrict__ th_out, float* __restrict__ g_out,
+               std::size_t n, const int* __restrict__ flag, unsigned long long* version, float alpha,
+               float oma, float eta, float eps) {
+  if (*flag) return;
+  const std::size_t n4 = n / 4;
+  const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+  const std::size_t t0 = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const float4* T = reinterpret_cast<const float4*>(th_in);
+  const float4* G = reinterpret_cast<const float4*>(g_in);
+  const float4* D = reinterpret_cast<const float4*>(d);
+  float4* TO = reinterpret_cast<float4*>(th_out);
+  float4* GO = reinterpret_cast<float4*>(g_out);
+  for (std::size_t i = t0; i < n4; i += stride) {
+    float4 t = T[i], g = G[i];
+    const float4 dd = __ldcs(D + i);
+    rms1(t.x, g.x, dd.x, alpha, oma, eta, eps);
+    rms1(t.y, g.y, dd.y, alpha, oma, eta, eps);
+    rms1(t.z, g.z, dd.z, alpha, oma, eta, eps);
+    rms1(t.w, g.w, dd.w, alpha, oma, eta, eps);
+    TO[i] = t;
+    GO[i] = g;
+  }
+  for (std::size_t i = n4 * 4 + t0; i < n; i += stride) {
+    float t = th_in[i], g = g_in[i];
+    rms1(t, g, d[i], alpha, oma, eta, eps);
+    th_out[i] = t;
+    g_out[i] = g;
+  }
+  if (version && t0 == 0) *version += 1ull;
+}
+
+// --------------------------------------------------------------- returns
+// returns.cpp:21-24: acc = r_i + gamma * acc, two roundings (no FMA), so the
+// result is bitwise equal to the reference's x86-64 build.
+__global__ void returns_kernel(const double* __restrict__ rewards, const int32_t* __restrict__ off,
+                               int n_seg, const uint8_t* __restrict__ terminal,
+                               const double* __restrict__ bootstrap, double gamma,
+                               double* __restrict__ out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_seg) return;
+  double acc = terminal[s] ? 0.0 : bootstrap[s];
+  for (int i = off[s + 1]; i-- > off[s];) {
+    acc = __dadd_rn(rewards[i], __dmul_rn(gamma, acc));
+    out[i] = acc;
+  }
+}
+
+// --------------------------------------------------------------- sampling
+// util.hpp:46-54 on the fp64 policy (pi64) or the fp32 API output.
+__global__ void sample_kernel(const float* __restrict__ pi32, const double* __restrict__ pi64,
+                              const double* __restrict__ u, int B, int A, int32_t* __restrict__ act,
+                              int act_stride) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const double uu = u[b];
+  double acc = 0.0;
+  int res = A - 1;
+  for (int i = 0; i < A; ++i) {
+    acc += pi64 ? pi64[static_cast<std::size_t>(b) * A + i]
+                : static_cast<double>(pi32[static_cast<std::size_t>(b) * A + i]);
+    if (uu < acc) {
+      res = i;
+      break;
+    }
+  }
+  act[static_cast<std::size_t>(b) * act_stride] = res;
+}
+
+__global__ void check_finite_kernel(const float* __restrict__ x, std::size_t n, int* __restrict__ flag) {
+  for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x)
+    if (!isfinite(x[i])) atomicOr(flag, 1);
+}
+
+}  // namespace ga3c

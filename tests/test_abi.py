@@ -1,0 +1,97 @@
+"""The C-ABI library loads, exports every symbol include/ga3c.h declares, and
+its host-only entry points agree with the reference.  CPU only: no compute
+call is made without a GPU (the compute path has no CPU fallback and must
+fail loudly instead)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import pyoracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "ga3c.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ga3c_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_1611_06256_b200 import _abi
+    names = header_functions()
+    assert len(names) >= 30
+    for n in names:
+        assert hasattr(_abi.lib, n), f"{n} declared in include/ga3c.h but not exported"
+    assert set(names) == set(_abi.EXPORTED), "ctypes signature table out of sync with the header"
+
+
+def test_library_is_sm100a_only():
+    so = os.path.join(ROOT, "paper_1611_06256_b200", "libga3c_b200.so")
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+    assert "sm_90" not in out and "sm_80" not in out
+
+
+def _spec_c(spec):
+    from paper_1611_06256_b200 import _abi
+    s = _abi.NetSpec()
+    C.memmove(C.byref(s), C.byref(spec), C.sizeof(s))
+    return s
+
+
+@pytest.mark.parametrize("spec", [O.dnn_a(), O.dnn_large(1), O.dnn_large(4), O.make_spec(4, [], [8], 3),
+                                  O.make_spec((12, 12, 2), [(4, 4, 2), (6, 3, 1)], [16], 3)])
+def test_param_count_and_init_match_oracle(spec):
+    from paper_1611_06256_b200 import _abi
+    s = _spec_c(spec)
+    P = _abi.lib.ga3c_param_count(C.byref(s))
+    assert P == O.param_count(spec)
+    t64 = np.zeros(P)
+    t32 = np.zeros(P, np.float32)
+    assert _abi.lib.ga3c_init_params(C.byref(s), 1234, t64.ctypes.data, t32.ctypes.data) == 0
+    ref = O.init_model(spec, 1234)
+    assert np.array_equal(t64, ref)
+    assert np.array_equal(t32, ref.astype(np.float32))
+
+
+def test_validation_matches_reference_rules():
+    from paper_1611_06256_b200 import _abi, qac
+    for bad in (qac.NetworkSpec(0, [], 2), qac.NetworkSpec(2, [], 1), qac.NetworkSpec(2, [0], 2)):
+        assert _abi.lib.ga3c_validate_spec(bad.to_c()) == _abi.INVALID_ARGUMENT
+        with pytest.raises(ValueError):
+            qac.param_count(bad)
+    h = qac.Hyperparams()
+    assert _abi.lib.ga3c_validate_hyper(h.to_c()) == 0
+    for kw in (dict(gamma=0.0), dict(alpha=1.0), dict(eps_log=0.0), dict(eta=0.0)):
+        assert _abi.lib.ga3c_validate_hyper(qac.Hyperparams(**kw).to_c()) == _abi.INVALID_ARGUMENT
+    d = _abi.default_hyper()
+    assert (d.gamma, d.t_max, d.beta, d.eta, d.alpha) == (0.99, 5, 0.01, 3e-4, 0.99)
+
+
+def test_qac_api_surface_matches_reference_names():
+    from paper_1611_06256_b200 import qac
+    for name in ("NetworkSpec", "Hyperparams", "param_count", "init_model", "init_rms", "forward",
+                 "policy_entropy", "loss_and_gradients", "rmsprop_update", "compute_returns"):
+        assert hasattr(qac, name)
+    assert qac.param_count(qac.NetworkSpec(4, [8], 3)) == 76
+    m = qac.init_model(qac.NetworkSpec(4, [8], 3), 7)
+    assert m.theta.dtype == np.float32 and m.version == 0
+
+
+def test_no_cpu_fallback_without_gpu():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_1611_06256_b200 import _abi
+    with pytest.raises(_abi.GA3CError):
+        _abi.Model(O_spec_to_abi(), _abi.default_hyper())
+
+
+def O_spec_to_abi():
+    return _spec_c(O.make_spec(4, [], [8], 3))
