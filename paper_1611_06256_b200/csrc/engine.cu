@@ -29,6 +29,8 @@
 #include "ga3c.h"
 #include "kernels.cuh"
 #include "layout.hpp"
+#include "tc_gemm.cuh"
+#include "tc_wgrad.cuh"
 
 using namespace ga3c;
 
@@ -173,6 +175,79 @@ void launch_gemm(ga3c_ctx* c, int tag, int layer, const LA& la, const LB& lb, co
   gemm_simt_kernel<LA, LB, Epi><<<grid, kThreads, 0, c->stream>>>(la, lb, epi, M, N, K, p.k_chunk);
 }
 
+// ------------------------------------------------------ tensor-core GEMMs
+
+template <typename TA, typename TB, int BN, int MODE>
+void tc_launch(ga3c_ctx* c, int tag, int layer, const Seg& A, const Seg& B, int M, int N, int K,
+               int splits, int kc, const TcEpiArgs& epi) {
+  using S = TcShape<TA, TB, BN>;
+  auto kern = tc_kk_gemm_kernel<TA, TB, BN, MODE>;
+  static bool attr_set = false;  // idempotent; racing setters write the same value
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
+    attr_set = true;
+  }
+  dim3 grid((M + 127) / 128, splits, (N + BN - 1) / BN);
+  Launch l(c, tag, layer);
+  kern<<<grid, kTcThreads, S::SMEM, c->stream>>>(A, B, M, N, K, kc, epi);
+}
+
+template <typename TA, typename TB, int MODE>
+void tc_dispatch(ga3c_ctx* c, int tag, int layer, int bn, const Seg& A, const Seg& B, int M, int N,
+                 int K, int splits, int kc, const TcEpiArgs& epi) {
+  switch (bn) {
+    case 16: tc_launch<TA, TB, 16, MODE>(c, tag, layer, A, B, M, N, K, splits, kc, epi); break;
+    case 32: tc_launch<TA, TB, 32, MODE>(c, tag, layer, A, B, M, N, K, splits, kc, epi); break;
+    case 64: tc_launch<TA, TB, 64, MODE>(c, tag, layer, A, B, M, N, K, splits, kc, epi); break;
+    case 128: tc_launch<TA, TB, 128, MODE>(c, tag, layer, A, B, M, N, K, splits, kc, epi); break;
+    default: tc_launch<TA, TB, 256, MODE>(c, tag, layer, A, B, M, N, K, splits, kc, epi); break;
+  }
+}
+
+int tc_bn(int n) {
+  int b = 16;
+  while (b < n && b < 256) b *= 2;
+  return b;
+}
+
+// Every (row, 32-chunk) run must be 16-byte aligned (fp32: 4 elements) or
+// 4-byte aligned (u8), and element offsets must fit the kernel's int32 math.
+bool seg_ok(const Seg& s, int rows_total) {
+  return s.rowlen % 32 == 0 && s.bstride % 4 == 0 && s.rs_y % 4 == 0 && s.rs_x % 4 == 0 &&
+         s.kstride % 4 == 0 && (reinterpret_cast<uintptr_t>(s.p) % 16) == 0 &&
+         static_cast<double>(s.bstride) * (rows_total / std::max(1, s.P) + 1) < 2.0e9;
+}
+
+template <typename T>
+Seg conv_seg(const Layer& L, const void* x, long long bstride) {
+  Seg s;
+  s.p = x;
+  s.bstride = bstride > 0 ? bstride : static_cast<long long>(L.ih) * L.iw * L.cin;
+  s.P = L.oh * L.ow;
+  s.ow = L.ow;
+  s.rs_y = L.stride * L.iw * L.cin;
+  s.rs_x = L.stride * L.cin;
+  s.rowlen = L.k * L.cin;
+  s.kstride = L.iw * L.cin;
+  s.rows = 0;
+  return s;
+}
+
+Seg dense_seg(const void* p, int rows, long long ld, int K, bool u8) {
+  Seg s;
+  s.p = p;
+  s.bstride = ld;
+  s.P = 1;
+  s.ow = 1;
+  s.rs_y = 0;
+  s.rs_x = 0;
+  s.rowlen = K;
+  s.kstride = 0;
+  s.rows = rows;
+  (void)u8;
+  return s;
+}
+
 template <typename T>
 Im2col<T> im2col_of(const Layer& L, const void* x, long long bstride) {
   Im2col<T> g;
@@ -191,6 +266,18 @@ Im2col<T> im2col_of(const Layer& L, const void* x, long long bstride) {
 template <typename T>
 void conv_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const void* x, float* out,
                   int B, long long in_stride) {
+  {
+    Seg A = conv_seg<T>(L, x, in_stride);
+    A.rows = B * L.pixels();
+    Seg W = dense_seg(theta + L.w_off, L.cout, L.in, L.in, false);
+    if (seg_ok(A, A.rows) && L.in % 32 == 0 && L.cout <= 256 && (L.w_off % 4) == 0) {
+      TcEpiArgs e{theta + L.b_off, out, L.cout};
+      const int M = B * L.pixels();
+      tc_dispatch<T, float, TC_EPI_BIAS_RELU>(c, GA3C_K_CONV_FWD, li, tc_bn(L.cout), A, W, M, L.cout,
+                                              L.in, 1, L.in, e);
+      return;
+    }
+  }
   Im2colA<T> a;
   static_cast<Im2col<T>&>(a) = im2col_of<T>(L, x, in_stride);
   DenseK w{theta + L.w_off, L.in};
@@ -204,7 +291,31 @@ void conv_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const
 template <typename T>
 int fc_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const void* x, float* out,
                int B, bool keep_partials, long long in_stride) {
-  DenseKIn<T> a{static_cast<const T*>(x), in_stride > 0 ? static_cast<int>(in_stride) : L.in};
+  const long long ld = in_stride > 0 ? in_stride : L.in;
+  {
+    Seg X = dense_seg(x, B, ld, L.in, sizeof(T) == 1);
+    Seg W = dense_seg(theta + L.w_off, L.out, L.in, L.in, false);
+    if (seg_ok(X, B) && seg_ok(W, L.out) && (L.w_off % 4) == 0) {
+      // swap-AB: the 128-row MMA tile runs over output units, batch is N
+      const int bn = tc_bn(B);
+      const int tiles = ((L.out + 127) / 128) * ((B + bn - 1) / bn);
+      const int chunks = L.in / 32;
+      int splits = std::max(1, std::min(chunks, kNumSMs / std::max(1, tiles)));
+      while (splits > 1 && static_cast<std::size_t>(splits) * B * L.out > kPartFloats) --splits;
+      const int kc = ((chunks + splits - 1) / splits) * 32;
+      splits = (L.in + kc - 1) / kc;
+      TcEpiArgs e{nullptr, c->part, L.out};
+      tc_dispatch<float, T, TC_EPI_PART_T>(c, GA3C_K_FC_FWD, li, bn, W, X, L.out, B, L.in, splits, kc, e);
+      if (!keep_partials) {
+        const std::size_t n = static_cast<std::size_t>(B) * L.out;
+        Launch l(c, GA3C_K_SPLITK, li);
+        splitk_bias_relu_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(
+            c->part, splits, B, L.out, theta + L.b_off, out);
+      }
+      return splits;
+    }
+  }
+  DenseKIn<T> a{static_cast<const T*>(x), static_cast<int>(ld)};
   DenseK w{theta + L.w_off, L.in};
   const SplitPlan p = plan_splits(B, L.out, L.in, true);
   if (keep_partials || p.splits > 1) {
@@ -236,10 +347,59 @@ void wgrad_gemm(ga3c_ctx* c, int li, const LA& la, const LB& lb, const GradMap& 
   }
 }
 
+template <typename TX, int BN>
+void wgrad_tc_launch(ga3c_ctx* c, int li, const WgradArgs& a, dim3 grid) {
+  using S = WgShape<TX, BN>;
+  auto kern = tc_wgrad_kernel<TX, BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
+    attr_set = true;
+  }
+  Launch l(c, GA3C_K_WGRAD, li);
+  kern<<<grid, kTcThreads, S::SMEM, c->stream>>>(a);
+}
+
+// Tensor-core weight gradient; returns false when the shape needs the SIMT path.
+template <typename TX>
+bool layer_wgrad_tc(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const float* dout, int B,
+                    long long in_stride, const GradMap& gm) {
+  const int npix = B * L.pixels();
+  Seg X = L.is_conv ? conv_seg<TX>(L, x_in, in_stride)
+                    : dense_seg(x_in, B, in_stride > 0 ? in_stride : L.in, L.in, sizeof(TX) == 1);
+  X.rows = npix;
+  if (!seg_ok(X, npix) || L.in % 32 != 0 || L.out % 4 != 0 ||
+      (reinterpret_cast<uintptr_t>(dout) % 16) != 0)
+    return false;
+  const int bn = L.out <= 32 ? 32 : (L.out <= 64 ? 64 : 128);
+  const int mtiles = (L.in + 127) / 128;
+  const int ntiles = (L.out + bn - 1) / bn;
+  const int chunks = (npix + 31) / 32;
+  int splits = std::max(1, std::min(chunks, (kNumSMs + mtiles * ntiles - 1) / (mtiles * ntiles)));
+  while (splits > 1 && static_cast<std::size_t>(splits) * L.out * (L.in + 1) > kPartFloats) --splits;
+  const int kc = ((chunks + splits - 1) / splits) * 32;
+  splits = (npix + kc - 1) / kc;
+  WgradArgs a{X, dout, L.out, L.in, npix, kc, c->part, gm, splits == 1};
+  dim3 grid(mtiles, splits, ntiles);
+  switch (bn) {
+    case 32: wgrad_tc_launch<TX, 32>(c, li, a, grid); break;
+    case 64: wgrad_tc_launch<TX, 64>(c, li, a, grid); break;
+    default: wgrad_tc_launch<TX, 128>(c, li, a, grid); break;
+  }
+  if (splits > 1) {
+    const std::size_t n = static_cast<std::size_t>(L.out) * (L.in + 1);
+    Launch l(c, GA3C_K_SPLITK, li);
+    splitk_grad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->part, splits, L.out,
+                                                                          L.in + 1, gm);
+  }
+  return true;
+}
+
 template <typename T>
 void layer_wgrad(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const float* dout, int B,
                  long long in_stride) {
   GradMap gm{c->grad, c->flag, L.w_off, L.b_off, 0, 0, L.out, L.in};
+  if (layer_wgrad_tc<T>(c, li, L, x_in, dout, B, in_stride, gm)) return;
   DenseT a{dout, L.out};  // (m = out channel, k = row) -> dout[row][m]
   if (L.is_conv) {
     WithOnes<Im2colB<T>> b;
