@@ -332,6 +332,15 @@ int fc_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const vo
   return p.splits;
 }
 
+void launch_splitk_grad(ga3c_ctx* c, int li, int splits, int M, int N, const GradMap& gm) {
+  const std::size_t n = static_cast<std::size_t>(M) * N;
+  Launch l(c, GA3C_K_SPLITK, li);
+  if (splits > 16)
+    splitk_grad8_kernel<<<(unsigned)((n + 31) / 32), 256, 0, c->stream>>>(c->part, splits, M, N, gm);
+  else
+    splitk_grad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->part, splits, M, N, gm);
+}
+
 // Weight-gradient GEMM [M rows][N = Kw+1] (+ reduction) into dtheta.
 template <class LA, class LB>
 void wgrad_gemm(ga3c_ctx* c, int li, const LA& la, const LB& lb, const GradMap& gm, int M, int N,
@@ -341,9 +350,7 @@ void wgrad_gemm(ga3c_ctx* c, int li, const LA& la, const LB& lb, const GradMap& 
     launch_gemm(c, GA3C_K_WGRAD, li, la, lb, EpiGrad{gm}, M, N, K, p);
   } else {
     launch_gemm(c, GA3C_K_WGRAD, li, la, lb, EpiPartial{c->part, M, N}, M, N, K, p);
-    const std::size_t n = static_cast<std::size_t>(M) * N;
-    Launch l(c, GA3C_K_SPLITK, li);
-    splitk_grad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->part, p.splits, M, N, gm);
+    launch_splitk_grad(c, li, p.splits, M, N, gm);
   }
 }
 
@@ -375,7 +382,7 @@ bool layer_wgrad_tc(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const
   const int mtiles = (L.in + 127) / 128;
   const int ntiles = (L.out + bn - 1) / bn;
   const int chunks = (npix + 31) / 32;
-  int splits = std::max(1, std::min(chunks, (kNumSMs + mtiles * ntiles - 1) / (mtiles * ntiles)));
+  int splits = std::max(1, std::min(chunks / 2, (kNumSMs + mtiles * ntiles - 1) / (mtiles * ntiles)));
   while (splits > 1 && static_cast<std::size_t>(splits) * L.out * (L.in + 1) > kPartFloats) --splits;
   const int kc = ((chunks + splits - 1) / splits) * 32;
   splits = (npix + kc - 1) / kc;
@@ -387,10 +394,7 @@ bool layer_wgrad_tc(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const
     default: wgrad_tc_launch<TX, 128>(c, li, a, grid); break;
   }
   if (splits > 1) {
-    const std::size_t n = static_cast<std::size_t>(L.out) * (L.in + 1);
-    Launch l(c, GA3C_K_SPLITK, li);
-    splitk_grad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->part, splits, L.out,
-                                                                          L.in + 1, gm);
+    launch_splitk_grad(c, li, splits, L.out, L.in + 1, gm);
   }
   return true;
 }
@@ -416,7 +420,19 @@ void layer_wgrad(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const fl
 
 void layer_dgrad(ga3c_ctx* c, int li, const Layer& L, const float* theta, const float* dout,
                  const float* gate, float* din, int B) {
-  if (L.is_conv) {
+  if (L.is_conv && L.cin % 16 == 0 && L.cout % 4 == 0 && L.w_off % 4 == 0 &&
+      static_cast<std::size_t>(L.cout) * L.k * L.k * 16 * sizeof(float) <= 200 * 1024) {
+    const int npix = B * L.ih * L.iw;
+    const std::size_t smem = static_cast<std::size_t>(L.cout) * L.k * L.k * 16 * sizeof(float);
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(conv_dgrad16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr_set = true;
+    }
+    Launch l(c, GA3C_K_DGRAD, li);
+    conv_dgrad16_kernel<<<dim3((npix + 127) / 128, L.cin / 16), 128, smem, c->stream>>>(
+        dout, theta + L.w_off, gate, din, B, L.ih, L.iw, L.cin, L.oh, L.ow, L.cout, L.k, L.stride);
+  } else if (L.is_conv) {
     const std::size_t n = static_cast<std::size_t>(B) * L.ih * L.iw * L.cin;
     Launch l(c, GA3C_K_DGRAD, li);
     conv_dgrad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(

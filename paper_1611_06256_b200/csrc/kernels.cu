@@ -210,6 +210,79 @@ conv_dgrad_kernel(const float* __restrict__ dout, const float* __restrict__ W,
   din[idx] = acc;
 }
 
+// Input gradient of a VALID conv, one thread per input pixel x 16 input
+// channels (blockIdx.y selects the channel chunk).  The W[co][ky][kx][ci0:+16]
+// slice is staged in shared memory once per CTA; dout rows are read as
+// float4.  Same math and gating as conv_dgrad_kernel, ~30x fewer loads.
+__global__ void __launch_bounds__(128)
+conv_dgrad16_kernel(const float* __restrict__ dout, const float* __restrict__ W,
+                    const float* __restrict__ gate, float* __restrict__ din, int B, int ih, int iw,
+                    int cin, int oh, int ow, int cout, int k, int s) {
+  extern __shared__ float4 wsh4[];  // [cout][k][k][16] floats
+  const int ci0 = blockIdx.y * 16;
+  const int kk2 = k * k;
+  float* wsh = reinterpret_cast<float*>(wsh4);
+  for (int i = threadIdx.x; i < cout * kk2 * 4; i += blockDim.x) {
+    const int q = i & 3, r = i >> 2;  // r = co*kk2 + (ky*k + kx)
+    reinterpret_cast<float4*>(wsh)[i] =
+        *reinterpret_cast<const float4*>(W + static_cast<std::size_t>(r) * cin + ci0 + 4 * q);
+  }
+  __syncthreads();
+  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= B * ih * iw) return;
+  const int x = pix % iw;
+  const int y = (pix / iw) % ih;
+  const int b = pix / (iw * ih);
+  const std::size_t base = static_cast<std::size_t>(pix) * cin + ci0;
+  float4 gt[4];
+  bool any = false;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    gt[q] = *reinterpret_cast<const float4*>(gate + base + 4 * q);
+    any |= gt[q].x > 0.f || gt[q].y > 0.f || gt[q].z > 0.f || gt[q].w > 0.f;
+  }
+  float acc[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+  if (any) {
+    for (int ky = y % s; ky < k; ky += s) {
+      const int oy = (y - ky) / s;
+      if (y < ky || oy >= oh) continue;
+      for (int kx = x % s; kx < k; kx += s) {
+        const int ox = (x - kx) / s;
+        if (x < kx || ox >= ow) continue;
+        const float* g = dout + ((static_cast<std::size_t>(b) * oh + oy) * ow + ox) * cout;
+        const float4* w4 = wsh4 + (ky * k + kx) * 4;
+        for (int co = 0; co < cout; co += 4) {
+          const float4 d = *reinterpret_cast<const float4*>(g + co);
+          const float dv[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float4* wr = w4 + (co + c) * kk2 * 4;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 w = wr[q];
+              acc[4 * q + 0] = fmaf(dv[c], w.x, acc[4 * q + 0]);
+              acc[4 * q + 1] = fmaf(dv[c], w.y, acc[4 * q + 1]);
+              acc[4 * q + 2] = fmaf(dv[c], w.z, acc[4 * q + 2]);
+              acc[4 * q + 3] = fmaf(dv[c], w.w, acc[4 * q + 3]);
+            }
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float4 o;
+    o.x = gt[q].x <= 0.f ? 0.f : acc[4 * q + 0];
+    o.y = gt[q].y <= 0.f ? 0.f : acc[4 * q + 1];
+    o.z = gt[q].z <= 0.f ? 0.f : acc[4 * q + 2];
+    o.w = gt[q].w <= 0.f ? 0.f : acc[4 * q + 3];
+    *reinterpret_cast<float4*>(din + base + 4 * q) = o;
+  }
+}
+
 // ------------------------------------------------------- split-K reductions
 __global__ void splitk_bias_relu_kernel(const float* __restrict__ part, int n_split, int M, int N,
                                         const float* __restrict__ bias, float* __restrict__ out) {
@@ -230,6 +303,28 @@ __global__ void splitk_grad_kernel(const float* __restrict__ part, int n_split, 
   float s = 0.0f;
   for (int k = 0; k < n_split; ++k) s += part[k * total + i];
   g.store(static_cast<int>(i / N), static_cast<int>(i % N), s);
+}
+
+// Many splits: 256 threads = 32 outputs x 8 interleaved sub-sums (split q,
+// q+8, ...) combined in sub-sum order -- a fixed reduction tree, so results
+// are reproducible run to run.
+__global__ void __launch_bounds__(256)
+splitk_grad8_kernel(const float* __restrict__ part, int n_split, int M, int N, GradMap g) {
+  __shared__ float red[8][33];
+  const std::size_t total = static_cast<std::size_t>(M) * N;
+  const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const std::size_t i = static_cast<std::size_t>(blockIdx.x) * 32 + lane;
+  float s = 0.0f;
+  if (i < total)
+    for (int k = q; k < n_split; k += 8) s += part[k * total + i];
+  red[q][lane] = s;
+  __syncthreads();
+  if (q == 0 && i < total) {
+    float t = red[0][lane];
+#pragma unroll
+    for (int r = 1; r < 8; ++r) t += red[r][lane];
+    g.store(static_cast<int>(i / N), static_cast<int>(i % N), t);
+  }
 }
 
 // -------------------------------------------------------------- clipping

@@ -28,9 +28,14 @@ __global__ void conv_dgrad_kernel(const float* dout, const float* W, const float
                                   int B, int ih, int iw, int cin, int oh, int ow, int cout, int k,
                                   int s);
 
+__global__ void conv_dgrad16_kernel(const float* dout, const float* W, const float* gate, float* din,
+                                    int B, int ih, int iw, int cin, int oh, int ow, int cout, int k,
+                                    int s);
+
 __global__ void splitk_bias_relu_kernel(const float* part, int n_split, int M, int N,
                                         const float* bias, float* out);
 __global__ void splitk_grad_kernel(const float* part, int n_split, int M, int N, GradMap g);
+__global__ void splitk_grad8_kernel(const float* part, int n_split, int M, int N, GradMap g);
 
 __global__ void sumsq_kernel(const float* g, std::size_t n, double* part);
 __global__ void clip_scale_kernel(float* g, std::size_t n, const double* part, int n_part,
