@@ -212,6 +212,15 @@ int ga3c_ctx_time_kernel(ga3c_ctx* c, int tag, int layer);
 /* Sum of the bracketed device durations since the last call (blocking). */
 int ga3c_ctx_kernel_time(ga3c_ctx* c, double* total_ms, uint64_t* launches);
 
+/* ------------------------------------------------------- CUDA graphs */
+/* Capture the device-resident calls issued on this context's stream between
+ * begin and end (forward_dev / loss_grad_dev / apply_rmsprop_dev / ...) into
+ * a CUDA graph; launch replays it.  Shapes and pointers are frozen at capture
+ * time.  No host-synchronising call may be made while capturing. */
+int ga3c_ctx_graph_begin(ga3c_ctx* c);
+int ga3c_ctx_graph_end(ga3c_ctx* c, int* graph_id);
+int ga3c_ctx_graph_launch(ga3c_ctx* c, int graph_id);
+
 /* ----------------------------------------------------------- sampling */
 /* qac::sample_index util.hpp:46-54 per row: the first a with u < sum_{<=a} pi
  * accumulated in fp64.  d_pi = NULL samples the context's last forward output

@@ -94,6 +94,9 @@ _SIGS = {
     "ga3c_compute_returns_dev": (C.c_int, [_P, _P, _P, C.c_int, _P, _P, C.c_double, _P]),
     "ga3c_sample_actions_dev": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, _P, C.c_int]),
     "ga3c_ctx_time_kernel": (C.c_int, [_P, C.c_int, C.c_int]),
+    "ga3c_ctx_graph_begin": (C.c_int, [_P]),
+    "ga3c_ctx_graph_end": (C.c_int, [_P, C.POINTER(C.c_int)]),
+    "ga3c_ctx_graph_launch": (C.c_int, [_P, C.c_int]),
     "ga3c_ctx_kernel_time": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
 }
 
@@ -331,6 +334,17 @@ class Context:
         ms, n = C.c_double(0), C.c_uint64(0)
         check(lib.ga3c_ctx_kernel_time(self.h, C.byref(ms), C.byref(n)), self.model.error())
         return ms.value, n.value
+
+    def graph_begin(self):
+        check(lib.ga3c_ctx_graph_begin(self.h), self.model.error())
+
+    def graph_end(self):
+        gid = C.c_int(-1)
+        check(lib.ga3c_ctx_graph_end(self.h, C.byref(gid)), self.model.error())
+        return gid.value
+
+    def graph_launch(self, gid):
+        check(lib.ga3c_ctx_graph_launch(self.h, gid), self.model.error())
 
     def dev_version(self):
         v = C.c_uint64(0)

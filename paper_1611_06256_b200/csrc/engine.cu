@@ -31,6 +31,9 @@
 #include "layout.hpp"
 #include "tc_gemm.cuh"
 #include "tc_wgrad.cuh"
+#include "tc_pipe.cuh"
+#include "tc_ws.cuh"
+#include "pdl.cuh"
 
 using namespace ga3c;
 
@@ -79,6 +82,8 @@ struct ga3c_ctx {
   float* v = nullptr;
   double* v64 = nullptr;
   float* dhead = nullptr;
+  float* dhT = nullptr;  // transposed head-input gradient [D][ldT] (FC dgrad operand)
+  int ldT = 0;
   double* scal = nullptr;
   double* scal_sum = nullptr;
   int32_t* d_actions = nullptr;
@@ -102,6 +107,9 @@ struct ga3c_ctx {
   int timed_tag = 0, timed_layer = -1;
   std::vector<cudaEvent_t> events;
   std::size_t ev_used = 0;
+  // captured CUDA graphs of device-resident step sequences
+  std::vector<cudaGraphExec_t> graphs;
+  bool capturing = false;
 };
 
 namespace {
@@ -117,6 +125,24 @@ namespace {
 
 thread_local std::string g_tls_error;
 
+
+
+// Every kernel goes out with programmatic stream serialization (pdl.cuh).
+template <typename... KArgs, typename... Args>
+void pdl_launch(cudaStream_t st, void (*kern)(KArgs...), dim3 grid, dim3 block, std::size_t smem,
+                Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // --------------------------------------------------------------- GEMMs
 
@@ -172,7 +198,7 @@ void launch_gemm(ga3c_ctx* c, int tag, int layer, const LA& la, const LB& lb, co
                  int N, int K, const SplitPlan& p) {
   dim3 grid((N + kBN - 1) / kBN, (M + kBM - 1) / kBM, p.splits);
   Launch l(c, tag, layer);
-  gemm_simt_kernel<LA, LB, Epi><<<grid, kThreads, 0, c->stream>>>(la, lb, epi, M, N, K, p.k_chunk);
+  pdl_launch(c->stream, gemm_simt_kernel<LA, LB, Epi>, dim3(grid), dim3(kThreads), 0, la, lb, epi, M, N, K, p.k_chunk);
 }
 
 // ------------------------------------------------------ tensor-core GEMMs
@@ -180,8 +206,8 @@ void launch_gemm(ga3c_ctx* c, int tag, int layer, const LA& la, const LB& lb, co
 template <typename TA, typename TB, int BN, int MODE>
 void tc_launch(ga3c_ctx* c, int tag, int layer, const Seg& A, const Seg& B, int M, int N, int K,
                int splits, int kc, const TcEpiArgs& epi) {
-  using S = TcShape<TA, TB, BN>;
-  auto kern = tc_kk_gemm_kernel<TA, TB, BN, MODE>;
+  using S = ws::KKShape<TA, TB, BN>;
+  auto kern = ws::tc_kk_ws_kernel<TA, TB, BN, MODE>;
   static bool attr_set = false;  // idempotent; racing setters write the same value
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
@@ -189,7 +215,7 @@ void tc_launch(ga3c_ctx* c, int tag, int layer, const Seg& A, const Seg& B, int 
   }
   dim3 grid((M + 127) / 128, splits, (N + BN - 1) / BN);
   Launch l(c, tag, layer);
-  kern<<<grid, kTcThreads, S::SMEM, c->stream>>>(A, B, M, N, K, kc, epi);
+  pdl_launch(c->stream, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, A, B, M, N, K, kc, epi);
 }
 
 template <typename TA, typename TB, int MODE>
@@ -200,13 +226,13 @@ void tc_dispatch(ga3c_ctx* c, int tag, int layer, int bn, const Seg& A, const Se
     case 32: tc_launch<TA, TB, 32, MODE>(c, tag, layer, A, B, M, N, K, splits, kc, epi); break;
     case 64: tc_launch<TA, TB, 64, MODE>(c, tag, layer, A, B, M, N, K, splits, kc, epi); break;
     case 128: tc_launch<TA, TB, 128, MODE>(c, tag, layer, A, B, M, N, K, splits, kc, epi); break;
-    default: tc_launch<TA, TB, 256, MODE>(c, tag, layer, A, B, M, N, K, splits, kc, epi); break;
+    default: tc_launch<TA, TB, 128, MODE>(c, tag, layer, A, B, M, N, K, splits, kc, epi); break;
   }
 }
 
-int tc_bn(int n) {
+int tc_bn(int n) {  // N tile; 2*BN (hi|lo concatenated) must fit one MMA (<= 256)
   int b = 16;
-  while (b < n && b < 256) b *= 2;
+  while (b < n && b < 128) b *= 2;
   return b;
 }
 
@@ -270,7 +296,7 @@ void conv_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const
     Seg A = conv_seg<T>(L, x, in_stride);
     A.rows = B * L.pixels();
     Seg W = dense_seg(theta + L.w_off, L.cout, L.in, L.in, false);
-    if (seg_ok(A, A.rows) && L.in % 32 == 0 && L.cout <= 256 && (L.w_off % 4) == 0) {
+    if (seg_ok(A, A.rows) && L.in % 32 == 0 && L.cout <= 128 && L.cout % 4 == 0 && (L.w_off % 4) == 0) {
       TcEpiArgs e{theta + L.b_off, out, L.cout};
       const int M = B * L.pixels();
       tc_dispatch<T, float, TC_EPI_BIAS_RELU>(c, GA3C_K_CONV_FWD, li, tc_bn(L.cout), A, W, M, L.cout,
@@ -295,7 +321,7 @@ int fc_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const vo
   {
     Seg X = dense_seg(x, B, ld, L.in, sizeof(T) == 1);
     Seg W = dense_seg(theta + L.w_off, L.out, L.in, L.in, false);
-    if (seg_ok(X, B) && seg_ok(W, L.out) && (L.w_off % 4) == 0) {
+    if (seg_ok(X, B) && seg_ok(W, L.out) && (L.w_off % 4) == 0 && L.out % 4 == 0) {
       // swap-AB: the 128-row MMA tile runs over output units, batch is N
       const int bn = tc_bn(B);
       const int tiles = ((L.out + 127) / 128) * ((B + bn - 1) / bn);
@@ -309,7 +335,7 @@ int fc_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const vo
       if (!keep_partials) {
         const std::size_t n = static_cast<std::size_t>(B) * L.out;
         Launch l(c, GA3C_K_SPLITK, li);
-        splitk_bias_relu_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(
+        pdl_launch(c->stream, splitk_bias_relu_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, 
             c->part, splits, B, L.out, theta + L.b_off, out);
       }
       return splits;
@@ -323,7 +349,7 @@ int fc_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const vo
     if (!keep_partials) {
       const std::size_t n = static_cast<std::size_t>(B) * L.out;
       Launch l(c, GA3C_K_SPLITK, li);
-      splitk_bias_relu_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(
+      pdl_launch(c->stream, splitk_bias_relu_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, 
           c->part, p.splits, B, L.out, theta + L.b_off, out);
     }
   } else {
@@ -336,9 +362,9 @@ void launch_splitk_grad(ga3c_ctx* c, int li, int splits, int M, int N, const Gra
   const std::size_t n = static_cast<std::size_t>(M) * N;
   Launch l(c, GA3C_K_SPLITK, li);
   if (splits > 16)
-    splitk_grad8_kernel<<<(unsigned)((n + 31) / 32), 256, 0, c->stream>>>(c->part, splits, M, N, gm);
+    pdl_launch(c->stream, splitk_grad8_kernel, dim3((unsigned)((n + 31) / 32)), dim3(256), 0, c->part, splits, M, N, gm);
   else
-    splitk_grad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->part, splits, M, N, gm);
+    pdl_launch(c->stream, splitk_grad_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, c->part, splits, M, N, gm);
 }
 
 // Weight-gradient GEMM [M rows][N = Kw+1] (+ reduction) into dtheta.
@@ -355,16 +381,16 @@ void wgrad_gemm(ga3c_ctx* c, int li, const LA& la, const LB& lb, const GradMap& 
 }
 
 template <typename TX, int BN>
-void wgrad_tc_launch(ga3c_ctx* c, int li, const WgradArgs& a, dim3 grid) {
-  using S = WgShape<TX, BN>;
-  auto kern = tc_wgrad_kernel<TX, BN>;
+void wgrad_tc_launch(ga3c_ctx* c, int li, const WgradArgs& a, dim3 grid, int tag = GA3C_K_WGRAD) {
+  using S = ws::MNShape<TX, BN>;
+  auto kern = ws::tc_mn_ws_kernel<TX, BN>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
     attr_set = true;
   }
-  Launch l(c, GA3C_K_WGRAD, li);
-  kern<<<grid, kTcThreads, S::SMEM, c->stream>>>(a);
+  Launch l(c, tag, li);
+  pdl_launch(c->stream, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, a);
 }
 
 // Tensor-core weight gradient; returns false when the shape needs the SIMT path.
@@ -375,7 +401,7 @@ bool layer_wgrad_tc(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const
   Seg X = L.is_conv ? conv_seg<TX>(L, x_in, in_stride)
                     : dense_seg(x_in, B, in_stride > 0 ? in_stride : L.in, L.in, sizeof(TX) == 1);
   X.rows = npix;
-  if (!seg_ok(X, npix) || L.in % 32 != 0 || L.out % 4 != 0 ||
+  if (!seg_ok(X, npix) || L.in % 32 != 0 || L.out % 4 != 0 || L.w_off % 4 != 0 ||
       (reinterpret_cast<uintptr_t>(dout) % 16) != 0)
     return false;
   const int bn = L.out <= 32 ? 32 : (L.out <= 64 ? 64 : 128);
@@ -386,7 +412,7 @@ bool layer_wgrad_tc(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const
   while (splits > 1 && static_cast<std::size_t>(splits) * L.out * (L.in + 1) > kPartFloats) --splits;
   const int kc = ((chunks + splits - 1) / splits) * 32;
   splits = (npix + kc - 1) / kc;
-  WgradArgs a{X, dout, L.out, L.in, npix, kc, c->part, gm, splits == 1};
+  WgradArgs a{X, dout, L.out, L.out, L.in, npix, kc, c->part, gm, splits == 1, 0, nullptr, nullptr, 0};
   dim3 grid(mtiles, splits, ntiles);
   switch (bn) {
     case 32: wgrad_tc_launch<TX, 32>(c, li, a, grid); break;
@@ -394,7 +420,14 @@ bool layer_wgrad_tc(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const
     default: wgrad_tc_launch<TX, 128>(c, li, a, grid); break;
   }
   if (splits > 1) {
-    launch_splitk_grad(c, li, splits, L.out, L.in + 1, gm);
+    const std::size_t n = static_cast<std::size_t>(L.out) * (L.in + 1);
+    Launch l(c, GA3C_K_SPLITK, li);
+    if (splits > 16)
+      pdl_launch(c->stream, splitk_wgrad8_kernel, dim3((unsigned)((n + 31) / 32)), dim3(256), 0, c->part,
+                 splits, L.out, L.in, gm);
+    else
+      pdl_launch(c->stream, splitk_wgrad_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, c->part,
+                 splits, L.out, L.in, gm);
   }
   return true;
 }
@@ -418,8 +451,30 @@ void layer_wgrad(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const fl
   }
 }
 
+// FC input gradient on the tensor cores, computed transposed:
+//   dX^T[i][b] = sum_o W[o][i] * dh^T[o][b]   (both operands MN-major)
+// with the ReLU gate of the layer below fused into the store.  Needs the
+// transposed output gradient the loss kernel writes for the top FC layer.
+bool fc_dgrad_tc(ga3c_ctx* c, int li, const Layer& L, const float* theta, const float* doutT,
+                 int ldT, const float* gate, float* din, int B) {
+  Seg W = dense_seg(theta + L.w_off, L.out, L.in, L.in, false);
+  W.rows = L.out;
+  if (!seg_ok(W, L.out) || L.in % 32 != 0 || ldT % 4 != 0 || B > 128) return false;
+  const int bn = B <= 32 ? 32 : (B <= 64 ? 64 : 128);
+  WgradArgs a{W, doutT, ldT, B, L.in, L.out, ((L.out + 31) / 32) * 32, nullptr, GradMap{}, 0,
+              1, din, gate, L.in};
+  dim3 grid((L.in + 127) / 128, 1, 1);
+  switch (bn) {
+    case 32: wgrad_tc_launch<float, 32>(c, li, a, grid, GA3C_K_DGRAD); break;
+    case 64: wgrad_tc_launch<float, 64>(c, li, a, grid, GA3C_K_DGRAD); break;
+    default: wgrad_tc_launch<float, 128>(c, li, a, grid, GA3C_K_DGRAD); break;
+  }
+  return true;
+}
+
 void layer_dgrad(ga3c_ctx* c, int li, const Layer& L, const float* theta, const float* dout,
-                 const float* gate, float* din, int B) {
+                 const float* gate, float* din, int B, const float* doutT = nullptr) {
+  if (!L.is_conv && doutT && fc_dgrad_tc(c, li, L, theta, doutT, c->ldT, gate, din, B)) return;
   if (L.is_conv && L.cin % 16 == 0 && L.cout % 4 == 0 && L.w_off % 4 == 0 &&
       static_cast<std::size_t>(L.cout) * L.k * L.k * 16 * sizeof(float) <= 200 * 1024) {
     const int npix = B * L.ih * L.iw;
@@ -430,12 +485,12 @@ void layer_dgrad(ga3c_ctx* c, int li, const Layer& L, const float* theta, const 
       attr_set = true;
     }
     Launch l(c, GA3C_K_DGRAD, li);
-    conv_dgrad16_kernel<<<dim3((npix + 127) / 128, L.cin / 16), 128, smem, c->stream>>>(
+    pdl_launch(c->stream, conv_dgrad16_kernel, dim3(dim3((npix + 63) / 64, L.cin / 16)), dim3(256), smem, 
         dout, theta + L.w_off, gate, din, B, L.ih, L.iw, L.cin, L.oh, L.ow, L.cout, L.k, L.stride);
   } else if (L.is_conv) {
     const std::size_t n = static_cast<std::size_t>(B) * L.ih * L.iw * L.cin;
     Launch l(c, GA3C_K_DGRAD, li);
-    conv_dgrad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(
+    pdl_launch(c->stream, conv_dgrad_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, 
         dout, theta + L.w_off, gate, din, B, L.ih, L.iw, L.cin, L.oh, L.ow, L.cout, L.k, L.stride);
   } else {
     DenseK a{dout, L.out};
@@ -448,6 +503,7 @@ void layer_dgrad(ga3c_ctx* c, int li, const Layer& L, const float* theta, const 
 // ------------------------------------------------------------- forward
 
 __global__ void widen_u8_kernel(const uint8_t* __restrict__ x, float* __restrict__ y, std::size_t n) {
+  pdl_enter();
   const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) y[i] = static_cast<float>(x[i]) * (1.0f / 256.0f);
 }
@@ -485,7 +541,7 @@ int run_forward(ga3c_ctx* c, const float* theta, const void* d_in, bool u8, int 
       // raw u8 input feeds the heads directly: widen once (k/256 is exact)
       const std::size_t n = static_cast<std::size_t>(B) * D;
       Launch l(c, GA3C_K_OTHER, -1);
-      widen_u8_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(
+      pdl_launch(c->stream, widen_u8_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, 
           static_cast<const uint8_t*>(d_in), c->hin, n);
       h = c->hin;
     } else {
@@ -501,7 +557,7 @@ int run_forward(ga3c_ctx* c, const float* theta, const void* d_in, bool u8, int 
   const std::size_t smem = (static_cast<std::size_t>(D) + 8 * (A + 1)) * sizeof(float);
   {
     Launch l(c, GA3C_K_HEADS, -1);
-    heads_forward_kernel<<<B, 256, smem, c->stream>>>(part, n_split, fc_bias, h, B, D, theta,
+    pdl_launch(c->stream, heads_forward_kernel, dim3(B), dim3(256), smem, part, n_split, fc_bias, h, B, D, theta,
                                                       lo.policy.w_off, lo.policy.b_off, lo.value.w_off,
                                                       lo.value.b_off, A, c->pi32, c->pi64, c->v, c->v64);
   }
@@ -514,16 +570,16 @@ int run_loss_grad(ga3c_ctx* c, const float* theta, const void* d_in, bool u8, co
   const Layout& lo = m->lo;
   const int D = lo.head_in();
   const int A = lo.n_actions;
-  cudaMemsetAsync(c->flag, 0, sizeof(int), c->stream);
   run_forward(c, theta, d_in, u8, B, in_stride);
   const float* h = lo.n_trunk ? c->act[lo.n_trunk - 1]
                               : (u8 ? c->hin : static_cast<const float*>(d_in));
   float* dh = lo.n_trunk ? c->dx[0] : nullptr;
   {
     Launch l(c, GA3C_K_LOSS_BWD, -1);
-    loss_heads_bwd_kernel<<<B, lo.n_trunk ? 256 : 32, 0, c->stream>>>(
+    pdl_launch(c->stream, loss_heads_bwd_kernel, dim3(B), dim3(lo.n_trunk ? 256 : 32), 0, 
         c->pi64, c->v, d_act, d_rets, h, B, lo.n_trunk ? D : 0, A, theta, lo.policy.w_off,
-        lo.value.w_off, m->hp.beta, m->hp.eps_log, m->hp.value_loss_weight, c->dhead, dh, c->scal);
+        lo.value.w_off, m->hp.beta, m->hp.eps_log, m->hp.value_loss_weight, c->dhead, dh,
+        lo.n_trunk ? c->dhT : nullptr, c->ldT, c->scal, c->flag);
   }
   // heads weight gradient: [A+1][D+1] = dhead^T [h | 1]
   {
@@ -543,21 +599,22 @@ int run_loss_grad(ga3c_ctx* c, const float* theta, const void* d_in, bool u8, co
     else
       layer_wgrad<float>(c, li, L, x_in, c->dx[cur], B, st);
     if (li > 0) {
-      layer_dgrad(c, li, L, theta, c->dx[cur], c->act[li - 1], c->dx[cur ^ 1], B);
+      const float* doutT = li == lo.n_trunk - 1 ? c->dhT : nullptr;
+      layer_dgrad(c, li, L, theta, c->dx[cur], c->act[li - 1], c->dx[cur ^ 1], B, doutT);
       cur ^= 1;
     }
   }
   {
     Launch l(c, GA3C_K_OTHER, -1);
-    scalars_kernel<<<1, 32, 0, c->stream>>>(c->scal, B, c->scal_sum);
+    pdl_launch(c->stream, scalars_kernel, dim3(1), dim3(32), 0, c->scal, B, c->scal_sum);
   }
   if (apply_clip && m->hp.grad_clip_norm > 0.0) {
     {
       Launch l(c, GA3C_K_OTHER, -1);
-      sumsq_kernel<<<kNumSMs, 256, 0, c->stream>>>(c->grad, lo.total, c->clip_part);
+      pdl_launch(c->stream, sumsq_kernel, dim3(kNumSMs), dim3(256), 0, c->grad, lo.total, c->clip_part);
     }
     Launch l(c, GA3C_K_OTHER, -1);
-    clip_scale_kernel<<<kNumSMs, 256, 0, c->stream>>>(c->grad, lo.total, c->clip_part, kNumSMs,
+    pdl_launch(c->stream, clip_scale_kernel, dim3(kNumSMs), dim3(256), 0, c->grad, lo.total, c->clip_part, kNumSMs,
                                                       m->hp.grad_clip_norm);
   }
   return GA3C_OK;
@@ -572,7 +629,7 @@ void launch_rmsprop(ga3c_ctx* c, const Slot& src, const Slot& dst, unsigned long
   unsigned blocks = (unsigned)std::min<std::size_t>((n4 + 255) / 256, 8 * kNumSMs);
   if (blocks == 0) blocks = 1;
   Launch l(c, GA3C_K_RMSPROP, -1);
-  rmsprop_kernel<<<blocks, 256, 0, c->stream>>>(src.theta, src.g, c->grad, dst.theta, dst.g, n,
+  pdl_launch(c->stream, rmsprop_kernel, dim3(blocks), dim3(256), 0, src.theta, src.g, c->grad, dst.theta, dst.g, n,
                                                 c->flag, ver, alpha, oma, static_cast<float>(hp.eta),
                                                 static_cast<float>(hp.eps_rms));
 }
@@ -816,6 +873,9 @@ ga3c_ctx* ga3c_ctx_create(ga3c_model* m, int max_batch, int* status) {
   alloc(&c->v, B * sizeof(float));
   alloc(&c->v64, B * sizeof(double));
   alloc(&c->dhead, B * (lo.n_actions + 1) * sizeof(float));
+  c->ldT = static_cast<int>((B + 3) / 4 * 4);
+  alloc(&c->dhT, static_cast<std::size_t>(lo.head_in()) * c->ldT * sizeof(float));
+  if (ok) ok = cudaMemset(c->dhT, 0, static_cast<std::size_t>(lo.head_in()) * c->ldT * sizeof(float)) == cudaSuccess;
   alloc(&c->scal, B * 3 * sizeof(double));
   alloc(&c->scal_sum, 3 * sizeof(double));
   alloc(&c->d_actions, B * sizeof(int32_t));
@@ -847,7 +907,7 @@ void ga3c_ctx_destroy(ga3c_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->m->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  void* ps[] = {c->d_in, c->dx[0], c->dx[1], c->hin, c->pi32, c->pi64, c->v, c->v64, c->dhead, c->scal,
+  void* ps[] = {c->d_in, c->dx[0], c->dx[1], c->hin, c->pi32, c->pi64, c->v, c->v64, c->dhead, c->dhT, c->scal,
                 c->scal_sum, c->d_actions, c->d_rets, c->grad, c->flag, c->dev_version, c->part,
                 c->clip_part, c->r_rew, c->r_off, c->r_term, c->r_boot, c->r_out};
   for (void* p : ps)
@@ -856,6 +916,7 @@ void ga3c_ctx_destroy(ga3c_ctx* c) {
     if (a) cudaFree(a);
   if (c->h_flag) cudaFreeHost(c->h_flag);
   for (auto e : c->events) cudaEventDestroy(e);
+  for (auto g : c->graphs) cudaGraphExecDestroy(g);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1034,10 +1095,10 @@ int ga3c_clip_grad(ga3c_ctx* c) {
   if (m->hp.grad_clip_norm > 0.0) {
     {
       Launch l(c, GA3C_K_OTHER, -1);
-      sumsq_kernel<<<kNumSMs, 256, 0, c->stream>>>(c->grad, m->lo.total, c->clip_part);
+      pdl_launch(c->stream, sumsq_kernel, dim3(kNumSMs), dim3(256), 0, c->grad, m->lo.total, c->clip_part);
     }
     Launch l(c, GA3C_K_OTHER, -1);
-    clip_scale_kernel<<<kNumSMs, 256, 0, c->stream>>>(c->grad, m->lo.total, c->clip_part, kNumSMs,
+    pdl_launch(c->stream, clip_scale_kernel, dim3(kNumSMs), dim3(256), 0, c->grad, m->lo.total, c->clip_part, kNumSMs,
                                                       m->hp.grad_clip_norm);
   }
   GA3C_CUDA(cudaGetLastError());
@@ -1075,7 +1136,7 @@ int ga3c_apply_rmsprop(ga3c_ctx* c, const float* dtheta, int* applied, uint64_t*
       return GA3C_CUDA_ERROR;
     }
     Launch l(c, GA3C_K_OTHER, -1);
-    check_finite_kernel<<<kNumSMs, 256, 0, c->stream>>>(c->grad, n, c->flag);
+    pdl_launch(c->stream, check_finite_kernel, dim3(kNumSMs), dim3(256), 0, c->grad, n, c->flag);
   }
   launch_rmsprop(c, m->slots[src], m->slots[dst], nullptr);
   cudaMemcpyAsync(c->h_flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
@@ -1132,7 +1193,7 @@ int ga3c_compute_returns_dev(ga3c_ctx* c, const double* d_rewards, const int32_t
   auto set_err = [&](const std::string& e) { m->set_error(e); };
   {
     Launch l(c, GA3C_K_RETURNS, -1);
-    returns_kernel<<<(n_seg + 127) / 128, 128, 0, c->stream>>>(d_rewards, d_off, n_seg, d_terminal,
+    pdl_launch(c->stream, returns_kernel, dim3((n_seg + 127) / 128), dim3(128), 0, d_rewards, d_off, n_seg, d_terminal,
                                                                d_bootstrap, gamma, d_out);
   }
   GA3C_CUDA(cudaGetLastError());
@@ -1194,7 +1255,7 @@ int ga3c_sample_actions_dev(ga3c_ctx* c, const float* d_pi, const double* d_u, i
   const double* pi64 = (d_pi == nullptr || d_pi == c->pi32) ? c->pi64 : nullptr;
   {
     Launch l(c, GA3C_K_SAMPLE, -1);
-    sample_kernel<<<(B + 127) / 128, 128, 0, c->stream>>>(d_pi, pi64, d_u, B, A, d_actions,
+    pdl_launch(c->stream, sample_kernel, dim3((B + 127) / 128), dim3(128), 0, d_pi, pi64, d_u, B, A, d_actions,
                                                           action_stride);
   }
   GA3C_CUDA(cudaGetLastError());
@@ -1223,6 +1284,42 @@ int ga3c_ctx_kernel_time(ga3c_ctx* c, double* total_ms, uint64_t* launches) {
   if (total_ms) *total_ms = tot;
   if (launches) *launches = c->ev_used / 2;
   c->ev_used = 0;
+  return GA3C_OK;
+}
+
+int ga3c_ctx_graph_begin(ga3c_ctx* c) {
+  if (!c || c->capturing) return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  GA3C_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  c->capturing = true;
+  return GA3C_OK;
+}
+
+int ga3c_ctx_graph_end(ga3c_ctx* c, int* graph_id) {
+  if (!c || !c->capturing) return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  c->capturing = false;
+  cudaGraph_t g = nullptr;
+  GA3C_CUDA(cudaStreamEndCapture(c->stream, &g));
+  cudaGraphExec_t ex = nullptr;
+  cudaError_t err = cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  if (err != cudaSuccess) {
+    set_err(std::string("cudaGraphInstantiate: ") + cudaGetErrorString(err));
+    return GA3C_CUDA_ERROR;
+  }
+  c->graphs.push_back(ex);
+  if (graph_id) *graph_id = static_cast<int>(c->graphs.size()) - 1;
+  return GA3C_OK;
+}
+
+int ga3c_ctx_graph_launch(ga3c_ctx* c, int graph_id) {
+  if (!c || graph_id < 0 || graph_id >= static_cast<int>(c->graphs.size())) return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  GA3C_CUDA(cudaGraphLaunch(c->graphs[graph_id], c->stream));
   return GA3C_OK;
 }
 

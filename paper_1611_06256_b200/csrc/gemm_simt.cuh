@@ -11,6 +11,8 @@
 
 #include <cstdint>
 
+#include "pdl.cuh"
+
 namespace ga3c {
 
 // ------------------------------------------------------------ loaders
@@ -173,6 +175,7 @@ constexpr int kBM = 64, kBN = 64, kBK = 16, kThreads = 256;
 template <class LA, class LB, class Epi>
 __global__ void __launch_bounds__(kThreads)
 gemm_simt_kernel(LA la, LB lb, Epi epi, int M, int N, int K, int k_chunk) {
+  pdl_enter();
   __shared__ __align__(16) float As[2][kBK][kBM + 4];
   __shared__ __align__(16) float Bs[2][kBK][kBN + 4];
   const int tid = threadIdx.x;

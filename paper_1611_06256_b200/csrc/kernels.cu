@@ -20,6 +20,7 @@
 #include <cstdint>
 
 #include "kernels.cuh"
+#include "pdl.cuh"
 
 namespace ga3c {
 
@@ -51,6 +52,7 @@ heads_forward_kernel(const float* __restrict__ part, int n_split, const float* _
                      std::size_t wp_off, std::size_t bp_off, std::size_t wv_off, std::size_t bv_off,
                      int A, float* __restrict__ pi32, double* __restrict__ pi64,
                      float* __restrict__ v_out, double* __restrict__ v64_out) {
+  pdl_enter();
   extern __shared__ float sm[];
   float* h = sm;                // D
   float* red = sm + D;          // [8 warps][A+1]
@@ -60,8 +62,18 @@ heads_forward_kernel(const float* __restrict__ part, int n_split, const float* _
   for (int o = tid; o < D; o += blockDim.x) {
     float v;
     if (part) {
-      float s = 0.0f;
-      for (int k = 0; k < n_split; ++k) s += part[(static_cast<std::size_t>(k) * B + b) * D + o];
+      // 4 interleaved chains (splits k, k+4, ...) combined in a fixed order:
+      // independent loads in flight, reproducible result
+      float c[4] = {0.f, 0.f, 0.f, 0.f};
+      const std::size_t stride = static_cast<std::size_t>(B) * D;
+      const float* pp = part + static_cast<std::size_t>(b) * D + o;
+      int k = 0;
+      for (; k + 4 <= n_split; k += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) c[u] += pp[(k + u) * stride];
+      }
+      for (int u = 0; k < n_split; ++k, ++u) c[u] += pp[k * stride];
+      const float s = (c[0] + c[1]) + (c[2] + c[3]);
       v = s + fc_bias[o];
       v = v < 0.0f ? 0.0f : v;
       hrow[o] = v;
@@ -126,7 +138,12 @@ loss_heads_bwd_kernel(const double* __restrict__ pi64, const float* __restrict__
                       const float* __restrict__ h, int B, int D, int A,
                       const float* __restrict__ theta, std::size_t wp_off, std::size_t wv_off,
                       double beta, double eps, double c_v, float* __restrict__ dhead,
-                      float* __restrict__ dh, double* __restrict__ scal) {
+                      float* __restrict__ dh, float* __restrict__ dhT, int ldT,
+                      double* __restrict__ scal, int* __restrict__ flag) {
+  pdl_enter();
+  // every dtheta writer of this step runs after this kernel: reset the
+  // non-finite flag here (stream order) instead of a separate memset node
+  if (blockIdx.x == 0 && threadIdx.x == 0) *flag = 0;
   __shared__ float g_sh[65];
   const int b = blockIdx.x;
   const int tid = threadIdx.x;
@@ -161,12 +178,15 @@ loss_heads_bwd_kernel(const double* __restrict__ pi64, const float* __restrict__
     float s = 0.0f;
     for (int j = 0; j < A; ++j) s = fmaf(g_sh[j], theta[wp_off + static_cast<std::size_t>(j) * D + o], s);
     s = fmaf(g_sh[A], theta[wv_off + o], s);
-    drow[o] = hrow[o] <= 0.0f ? 0.0f : s;
+    const float g = hrow[o] <= 0.0f ? 0.0f : s;
+    drow[o] = g;
+    if (dhT) dhT[static_cast<std::size_t>(o) * ldT + b] = g;
   }
 }
 
 // Fixed-order batch sums of the per-sample diagnostics (nnet.cpp:233-235).
 __global__ void scalars_kernel(const double* __restrict__ scal, int B, double* __restrict__ out) {
+  pdl_enter();
   if (threadIdx.x < 3) {
     double s = 0.0;
     for (int b = 0; b < B; ++b) s += scal[3 * b + threadIdx.x];
@@ -181,6 +201,7 @@ __global__ void __launch_bounds__(256)
 conv_dgrad_kernel(const float* __restrict__ dout, const float* __restrict__ W,
                   const float* __restrict__ gate, float* __restrict__ din, int B, int ih, int iw,
                   int cin, int oh, int ow, int cout, int k, int s) {
+  pdl_enter();
   const std::size_t total = static_cast<std::size_t>(B) * ih * iw * cin;
   const std::size_t idx = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= total) return;
@@ -210,82 +231,70 @@ conv_dgrad_kernel(const float* __restrict__ dout, const float* __restrict__ W,
   din[idx] = acc;
 }
 
-// Input gradient of a VALID conv, one thread per input pixel x 16 input
-// channels (blockIdx.y selects the channel chunk).  The W[co][ky][kx][ci0:+16]
-// slice is staged in shared memory once per CTA; dout rows are read as
-// float4.  Same math and gating as conv_dgrad_kernel, ~30x fewer loads.
-__global__ void __launch_bounds__(128)
+// Input gradient of a VALID conv.  A CTA covers 64 input pixels x 16 input
+// channels (blockIdx.y = channel chunk); each thread owns one pixel x 4
+// channels.  The W[co][ky][kx][ci0:+16] slice is staged in shared memory
+// once per CTA and dout rows are read as float4.  Same math and gating as
+// conv_dgrad_kernel (nnet.cpp:267-278), with ~30x fewer loads.
+__global__ void __launch_bounds__(256)
 conv_dgrad16_kernel(const float* __restrict__ dout, const float* __restrict__ W,
                     const float* __restrict__ gate, float* __restrict__ din, int B, int ih, int iw,
                     int cin, int oh, int ow, int cout, int k, int s) {
-  extern __shared__ float4 wsh4[];  // [cout][k][k][16] floats
+  pdl_enter();
+  extern __shared__ float4 wsh4[];  // [cout][k][k][4 groups] float4
   const int ci0 = blockIdx.y * 16;
   const int kk2 = k * k;
-  float* wsh = reinterpret_cast<float*>(wsh4);
   for (int i = threadIdx.x; i < cout * kk2 * 4; i += blockDim.x) {
     const int q = i & 3, r = i >> 2;  // r = co*kk2 + (ky*k + kx)
-    reinterpret_cast<float4*>(wsh)[i] =
-        *reinterpret_cast<const float4*>(W + static_cast<std::size_t>(r) * cin + ci0 + 4 * q);
+    wsh4[i] = *reinterpret_cast<const float4*>(W + static_cast<std::size_t>(r) * cin + ci0 + 4 * q);
   }
   __syncthreads();
-  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+  const int grp = threadIdx.x & 3;
+  const int pix = blockIdx.x * 64 + (threadIdx.x >> 2);
   if (pix >= B * ih * iw) return;
   const int x = pix % iw;
   const int y = (pix / iw) % ih;
   const int b = pix / (iw * ih);
-  const std::size_t base = static_cast<std::size_t>(pix) * cin + ci0;
-  float4 gt[4];
-  bool any = false;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    gt[q] = *reinterpret_cast<const float4*>(gate + base + 4 * q);
-    any |= gt[q].x > 0.f || gt[q].y > 0.f || gt[q].z > 0.f || gt[q].w > 0.f;
-  }
-  float acc[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) acc[i] = 0.f;
-  if (any) {
+  const std::size_t base = static_cast<std::size_t>(pix) * cin + ci0 + 4 * grp;
+  const float4 gt = *reinterpret_cast<const float4*>(gate + base);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (gt.x > 0.f || gt.y > 0.f || gt.z > 0.f || gt.w > 0.f) {
     for (int ky = y % s; ky < k; ky += s) {
       const int oy = (y - ky) / s;
       if (y < ky || oy >= oh) continue;
       for (int kx = x % s; kx < k; kx += s) {
         const int ox = (x - kx) / s;
         if (x < kx || ox >= ow) continue;
-        const float* g = dout + ((static_cast<std::size_t>(b) * oh + oy) * ow + ox) * cout;
-        const float4* w4 = wsh4 + (ky * k + kx) * 4;
-        for (int co = 0; co < cout; co += 4) {
-          const float4 d = *reinterpret_cast<const float4*>(g + co);
+        const float4* g4 =
+            reinterpret_cast<const float4*>(dout + ((static_cast<std::size_t>(b) * oh + oy) * ow + ox) * cout);
+        const float4* w4 = wsh4 + (ky * k + kx) * 4 + grp;
+        for (int c4 = 0; c4 < cout / 4; ++c4) {
+          const float4 d = __ldg(g4 + c4);
           const float dv[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const float4* wr = w4 + (co + c) * kk2 * 4;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float4 w = wr[q];
-              acc[4 * q + 0] = fmaf(dv[c], w.x, acc[4 * q + 0]);
-              acc[4 * q + 1] = fmaf(dv[c], w.y, acc[4 * q + 1]);
-              acc[4 * q + 2] = fmaf(dv[c], w.z, acc[4 * q + 2]);
-              acc[4 * q + 3] = fmaf(dv[c], w.w, acc[4 * q + 3]);
-            }
+            const float4 w = w4[(4 * c4 + c) * kk2 * 4];
+            acc.x = fmaf(dv[c], w.x, acc.x);
+            acc.y = fmaf(dv[c], w.y, acc.y);
+            acc.z = fmaf(dv[c], w.z, acc.z);
+            acc.w = fmaf(dv[c], w.w, acc.w);
           }
         }
       }
     }
   }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    float4 o;
-    o.x = gt[q].x <= 0.f ? 0.f : acc[4 * q + 0];
-    o.y = gt[q].y <= 0.f ? 0.f : acc[4 * q + 1];
-    o.z = gt[q].z <= 0.f ? 0.f : acc[4 * q + 2];
-    o.w = gt[q].w <= 0.f ? 0.f : acc[4 * q + 3];
-    *reinterpret_cast<float4*>(din + base + 4 * q) = o;
-  }
+  float4 o;
+  o.x = gt.x <= 0.f ? 0.f : acc.x;
+  o.y = gt.y <= 0.f ? 0.f : acc.y;
+  o.z = gt.z <= 0.f ? 0.f : acc.z;
+  o.w = gt.w <= 0.f ? 0.f : acc.w;
+  *reinterpret_cast<float4*>(din + base) = o;
 }
 
 // ------------------------------------------------------- split-K reductions
 __global__ void splitk_bias_relu_kernel(const float* __restrict__ part, int n_split, int M, int N,
                                         const float* __restrict__ bias, float* __restrict__ out) {
+  pdl_enter();
   const std::size_t total = static_cast<std::size_t>(M) * N;
   const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= total) return;
@@ -297,6 +306,7 @@ __global__ void splitk_bias_relu_kernel(const float* __restrict__ part, int n_sp
 
 __global__ void splitk_grad_kernel(const float* __restrict__ part, int n_split, int M, int N,
                                    GradMap g) {
+  pdl_enter();
   const std::size_t total = static_cast<std::size_t>(M) * N;
   const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= total) return;
@@ -310,6 +320,7 @@ __global__ void splitk_grad_kernel(const float* __restrict__ part, int n_split, 
 // are reproducible run to run.
 __global__ void __launch_bounds__(256)
 splitk_grad8_kernel(const float* __restrict__ part, int n_split, int M, int N, GradMap g) {
+  pdl_enter();
   __shared__ float red[8][33];
   const std::size_t total = static_cast<std::size_t>(M) * N;
   const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
@@ -327,8 +338,53 @@ splitk_grad8_kernel(const float* __restrict__ part, int n_split, int M, int N, G
   }
 }
 
+// Tensor-core weight-gradient partials: weights [split][cout][Kw] (16-byte
+// aligned rows) followed by the bias sums [split][cout].  Output element i of
+// the virtual [cout][Kw+1] matrix (bias in the last column).
+__device__ __forceinline__ float wg_part(const float* __restrict__ part, int s, int n_split, int cout,
+                                         int Kw, int co, int kk) {
+  return kk < Kw ? part[(static_cast<std::size_t>(s) * cout + co) * Kw + kk]
+                 : part[static_cast<std::size_t>(n_split) * cout * Kw + static_cast<std::size_t>(s) * cout + co];
+}
+
+__global__ void splitk_wgrad_kernel(const float* __restrict__ part, int n_split, int cout, int Kw,
+                                    GradMap g) {
+  pdl_enter();
+  const int N = Kw + 1;
+  const std::size_t total = static_cast<std::size_t>(cout) * N;
+  const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int co = static_cast<int>(i / N), kk = static_cast<int>(i % N);
+  float s = 0.0f;
+  for (int k = 0; k < n_split; ++k) s += wg_part(part, k, n_split, cout, Kw, co, kk);
+  g.store(co, kk, s);
+}
+
+__global__ void __launch_bounds__(256)
+splitk_wgrad8_kernel(const float* __restrict__ part, int n_split, int cout, int Kw, GradMap g) {
+  pdl_enter();
+  __shared__ float red[8][33];
+  const int N = Kw + 1;
+  const std::size_t total = static_cast<std::size_t>(cout) * N;
+  const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const std::size_t i = static_cast<std::size_t>(blockIdx.x) * 32 + lane;
+  const int co = static_cast<int>(i / N), kk = static_cast<int>(i % N);
+  float s = 0.0f;
+  if (i < total)
+    for (int k = q; k < n_split; k += 8) s += wg_part(part, k, n_split, cout, Kw, co, kk);
+  red[q][lane] = s;
+  __syncthreads();
+  if (q == 0 && i < total) {
+    float t = red[0][lane];
+#pragma unroll
+    for (int r = 1; r < 8; ++r) t += red[r][lane];
+    g.store(co, kk, t);
+  }
+}
+
 // -------------------------------------------------------------- clipping
 __global__ void sumsq_kernel(const float* __restrict__ g, std::size_t n, double* __restrict__ part) {
+  pdl_enter();
   __shared__ double red[32];
   double s = 0.0;
   for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -348,6 +404,7 @@ __global__ void sumsq_kernel(const float* __restrict__ g, std::size_t n, double*
 
 __global__ void clip_scale_kernel(float* __restrict__ g, std::size_t n, const double* __restrict__ part,
                                   int n_part, double clip) {
+  pdl_enter();
   __shared__ double scale_sh;
   if (threadIdx.x == 0) {
     double sq = 0.0;
@@ -381,6 +438,7 @@ rmsprop_kernel(const float* __restrict__ th_in, const float* __restrict__ g_in,
                const float* __restrict__ d, float* __restrict__ th_out, float* __restrict__ g_out,
                std::size_t n, const int* __restrict__ flag, unsigned long long* version, float alpha,
                float oma, float eta, float eps) {
+  pdl_enter();
   if (*flag) return;
   const std::size_t n4 = n / 4;
   const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
@@ -416,6 +474,7 @@ __global__ void returns_kernel(const double* __restrict__ rewards, const int32_t
                                int n_seg, const uint8_t* __restrict__ terminal,
                                const double* __restrict__ bootstrap, double gamma,
                                double* __restrict__ out) {
+  pdl_enter();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n_seg) return;
   double acc = terminal[s] ? 0.0 : bootstrap[s];
@@ -430,6 +489,7 @@ __global__ void returns_kernel(const double* __restrict__ rewards, const int32_t
 __global__ void sample_kernel(const float* __restrict__ pi32, const double* __restrict__ pi64,
                               const double* __restrict__ u, int B, int A, int32_t* __restrict__ act,
                               int act_stride) {
+  pdl_enter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const double uu = u[b];
@@ -447,6 +507,7 @@ __global__ void sample_kernel(const float* __restrict__ pi32, const double* __re
 }
 
 __global__ void check_finite_kernel(const float* __restrict__ x, std::size_t n, int* __restrict__ flag) {
+  pdl_enter();
   for (std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x)
     if (!isfinite(x[i])) atomicOr(flag, 1);

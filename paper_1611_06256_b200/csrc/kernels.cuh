@@ -20,7 +20,7 @@ __global__ void loss_heads_bwd_kernel(const double* pi64, const float* v, const 
                                       const double* rets, const float* h, int B, int D, int A,
                                       const float* theta, std::size_t wp_off, std::size_t wv_off,
                                       double beta, double eps, double c_v, float* dhead, float* dh,
-                                      double* scal);
+                                      float* dhT, int ldT, double* scal, int* flag);
 
 __global__ void scalars_kernel(const double* scal, int B, double* out);
 
@@ -36,6 +36,8 @@ __global__ void splitk_bias_relu_kernel(const float* part, int n_split, int M, i
                                         const float* bias, float* out);
 __global__ void splitk_grad_kernel(const float* part, int n_split, int M, int N, GradMap g);
 __global__ void splitk_grad8_kernel(const float* part, int n_split, int M, int N, GradMap g);
+__global__ void splitk_wgrad_kernel(const float* part, int n_split, int cout, int Kw, GradMap g);
+__global__ void splitk_wgrad8_kernel(const float* part, int n_split, int cout, int Kw, GradMap g);
 
 __global__ void sumsq_kernel(const float* g, std::size_t n, double* part);
 __global__ void clip_scale_kernel(float* g, std::size_t n, const double* part, int n_part,

@@ -23,7 +23,8 @@ namespace ga3c {
 
 struct WgradArgs {
   Seg X;             // rows = pixels (M), k-runs along kk; X.rows = number of pixels
-  const float* D;    // [pixels][cout] output gradient (already ReLU-gated)
+  const float* D;    // [pixels][ldd] output gradient (already ReLU-gated)
+  int ldd;           // row stride of D
   int cout;          // N' (valid columns)
   int Kw;            // M' = kk extent (k*k*Cin or fan-in)
   int npix;          // reduction length
@@ -31,6 +32,12 @@ struct WgradArgs {
   float* part;       // [split][cout][Kw+1]  (when !direct)
   GradMap gm;        // direct store (when splits == 1)
   int direct;
+  // mode 1 (FC input gradient): out[co * ldo + kk] = gate[...] > 0 ? C' : 0,
+  // no bias column; X = W rows (m = fan-out unit), D = dh^T [fan-out][batch]
+  int mode;
+  float* out;
+  const float* gate;
+  int ldo;
 };
 
 namespace detail {
@@ -77,7 +84,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_wgrad_kernel(WgradArgs a) {
   const int pb = split * a.kc;
   const int pe = min(a.npix, pb + a.kc);
   const int nchunks = (pe - pb + 31) / 32;
-  const bool do_bias = blockIdx.x == 0;
+  const bool do_bias = blockIdx.x == 0 && a.mode == 0;
 
   // X tile: thread -> (pixel row p, 16B vector v), 4 MN atoms g (kk chunks)
   const int xp = tid >> 3, xv = tid & 7;
@@ -122,7 +129,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_wgrad_kernel(WgradArgs a) {
       const int px = p0 + p;
       const int co = n0 + 4 * v;
       dr[j] = (idx < S::BVEC && px < pe && co < a.cout)
-                  ? __ldg(reinterpret_cast<const float4*>(a.D + static_cast<std::size_t>(px) * a.cout + co))
+                  ? __ldg(reinterpret_cast<const float4*>(a.D + static_cast<std::size_t>(px) * a.ldd + co))
                   : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
@@ -234,10 +241,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_wgrad_kernel(WgradArgs a) {
       for (int j = 0; j < 16; ++j) {
         const int co = n0 + c0 + j;
         if (co < a.cout) {
-          if (a.direct)
+          if (a.mode == 1) {
+            const std::size_t o = static_cast<std::size_t>(co) * a.ldo + kk;
+            a.out[o] = __ldg(a.gate + o) <= 0.f ? 0.f : v[j];
+          } else if (a.direct) {
             a.gm.store(co, kk, v[j]);
-          else
+          } else {
             a.part[(static_cast<std::size_t>(split) * a.cout + co) * ldp + kk] = v[j];
+          }
         }
       }
     }

@@ -83,6 +83,19 @@ int main() {
   float hA[128 * 8], hB[32 * 8], ref[128 * 32], hC[128 * 32];
   for (int i = 0; i < 128 * 8; ++i) hA[i] = (float)((i * 37) % 17 - 8);
   for (int i = 0; i < 32 * 8; ++i) hB[i] = (float)((i * 11) % 13 - 6);
+  {  // tf32 operand conversion: truncation or rounding?  x = 1 + 0.75 ulp(tf32)
+    float *dA, *dB, *dC;
+    float a[128 * 8] = {0}, b[32 * 8] = {0}, c[128 * 32];
+    a[0] = 1.0f + 0x1.0p-11f + 0x1.0p-12f;  // A[0][0]
+    b[0] = 1.0f;                            // B[0][0]
+    cudaMalloc(&dA, sizeof(a)); cudaMalloc(&dB, sizeof(b)); cudaMalloc(&dC, sizeof(c));
+    cudaMemcpy(dA, a, sizeof(a), cudaMemcpyHostToDevice);
+    cudaMemcpy(dB, b, sizeof(b), cudaMemcpyHostToDevice);
+    probe<<<1, 128>>>(dA, dB, dC, 0, 0, 0, 0, 0);
+    cudaDeviceSynchronize();
+    cudaMemcpy(c, dC, sizeof(c), cudaMemcpyDeviceToHost);
+    printf("tf32 conversion probe: x=%.9g -> C=%.9g (trunc 1.0, RN %.9g)\n", a[0], c[0], 1.0 + 0x1.0p-10);
+  }
   for (int m = 0; m < 128; ++m)
     for (int n = 0; n < 32; ++n) {
       float s = 0;
