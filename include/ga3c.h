@@ -103,6 +103,7 @@ int ga3c_model_read(ga3c_model* m, float* theta, float* g, uint64_t* version);
 /* SharedModel::version pipeline.hpp:98 */
 uint64_t ga3c_model_version(ga3c_model* m);
 size_t ga3c_model_param_count(ga3c_model* m);
+int ga3c_model_n_actions(ga3c_model* m);
 /* SharedModel::snapshot pipeline.hpp:96: pin the latest immutable parameter
  * slot; it cannot be recycled until released. */
 int ga3c_snapshot_acquire(ga3c_model* m, int* slot, uint64_t* version);
@@ -152,6 +153,23 @@ int ga3c_loss_grad_f32(ga3c_ctx* c, int slot, const float* states, const int32_t
 int ga3c_loss_grad_dev(ga3c_ctx* c, int slot, const void* d_states, int states_are_u8,
                        long long state_stride, const int32_t* d_actions, const double* d_returns,
                        int B, int apply_clip);
+/* Trainer step with on-device n-step returns: the merged batch of n_seg
+ * agent segments (segment s = rows seg_offsets[s] .. seg_offsets[s+1]) is
+ * uploaded with its rewards, terminal flags and bootstrap values;
+ * returns::compute_returns (returns.cpp:8-26) runs per segment on the device
+ * and feeds loss_and_gradients (nnet.cpp:201-291) directly.  Equivalent to
+ * the reference's flush() + trainer_main() pair (pipeline.cpp:207-306).
+ * returns_out (nullable) receives the fp64 returns. */
+int ga3c_loss_grad_segments_u8(ga3c_ctx* c, int slot, const uint8_t* frames, int B,
+                               const int32_t* actions, const double* rewards,
+                               const int32_t* seg_offsets, int n_seg, const uint8_t* terminal,
+                               const double* bootstrap, double gamma, int apply_clip,
+                               double* scalars, double* returns_out);
+int ga3c_loss_grad_segments_f32(ga3c_ctx* c, int slot, const float* states, int B,
+                                const int32_t* actions, const double* rewards,
+                                const int32_t* seg_offsets, int n_seg, const uint8_t* terminal,
+                                const double* bootstrap, double gamma, int apply_clip,
+                                double* scalars, double* returns_out);
 /* The context's device gradient buffer (P floats) -- e.g. for an NCCL
  * allreduce(sum) across data-parallel replicas. */
 float* ga3c_ctx_grad(ga3c_ctx* c);
@@ -228,6 +246,59 @@ int ga3c_ctx_graph_launch(ga3c_ctx* c, int graph_id);
  * async. */
 int ga3c_sample_actions_dev(ga3c_ctx* c, const float* d_pi, const double* d_u, int B,
                             int n_actions, int32_t* d_actions, int action_stride);
+
+/* ------------------------------------------------- host engine (C++) */
+/* pipeline::run (pipeline.hpp:122) / reference::train_sync (reference.hpp:30)
+ * of the B200 host engine (paper_1611_06256_b200/csrc/host): agent threads
+ * on CPU environments, predictor threads batching the PredictionQueue into
+ * device forwards, trainer threads coalescing the TrainingQueue into device
+ * returns + loss/backward + RMSProp, the control thread with the annealer. */
+typedef struct ga3c_pipeline_opts {
+  ga3c_net_spec net;
+  ga3c_hyper hyper;
+  /* EnvSpec (envs.hpp): 0 bandit, 1 catch, 2 delay lab, 3 frame catch (84x84x4
+   * u8), 4 synthetic frames (84x84x4 u8, delay-lab ballast) */
+  int env_kind, n_contexts, env_actions, grid_size;
+  long long step_delay_us;
+  int episode_len, action_repeat;
+  /* KnobConfig (knobs.hpp:9-19) */
+  int n_agents, n_predictors, n_trainers, pred_batch_max, min_train_batch, train_queue_cap, pred_queue_cap;
+  /* StopCondition: 0 = unset */
+  long long max_updates;
+  double max_seconds;
+  double target_score;
+  int has_target_score;
+  unsigned long long seed;
+  int anneal, anneal_batches;
+  double epoch_s;
+  int max_agents, max_predictors, max_trainers;
+  double metrics_interval_s;
+  int greedy, sync_after_submit, capture_trajectory, device;
+} ga3c_pipeline_opts;
+
+typedef struct ga3c_run_report {
+  long long total_updates, skipped_updates, total_predictions, total_episodes;
+  double wall_time_s, avg_tps, avg_pps, avg_samples_per_s, mean_lag, final_rolling_score;
+  long long experiences_produced, experiences_trained, experiences_dropped, experiences_left_queued;
+  int final_n_agents, final_n_predictors, final_n_trainers, final_pred_batch_max, final_min_train_batch;
+  unsigned long long final_version;
+  int n_trajectory, n_anneal, n_frames;
+  double last_frame_tps, last_frame_pps, last_frame_pred_batch_mean;
+} ga3c_run_report;
+
+typedef struct ga3c_anneal_entry {
+  int n_agents, n_predictors, n_trainers, pred_batch_max, min_train_batch;
+  double measured_tps;
+  int accepted;
+} ga3c_anneal_entry;
+
+void ga3c_default_pipeline_opts(ga3c_pipeline_opts* o);
+/* sync_trainer = 1 runs train_sync (zero lag, round-robin agents).  Output
+ * arrays are nullable; capacities bound what is copied.  err receives the
+ * std::invalid_argument / runtime message. */
+int ga3c_pipeline_run(const ga3c_pipeline_opts* o, int sync_trainer, ga3c_run_report* r,
+                      float* final_theta, float* trajectory, int traj_cap, double* episode_scores,
+                      int scores_cap, ga3c_anneal_entry* anneal, int anneal_cap, char* err, int err_len);
 
 #ifdef __cplusplus
 }

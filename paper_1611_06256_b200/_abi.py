@@ -54,6 +54,49 @@ class HyperC(C.Structure):
     ]
 
 
+class PipelineOpts(C.Structure):
+    """ga3c_pipeline_opts (include/ga3c.h)."""
+
+    _fields_ = [
+        ("net", NetSpec), ("hyper", HyperC),
+        ("env_kind", C.c_int), ("n_contexts", C.c_int), ("env_actions", C.c_int), ("grid_size", C.c_int),
+        ("step_delay_us", C.c_longlong), ("episode_len", C.c_int), ("action_repeat", C.c_int),
+        ("n_agents", C.c_int), ("n_predictors", C.c_int), ("n_trainers", C.c_int),
+        ("pred_batch_max", C.c_int), ("min_train_batch", C.c_int), ("train_queue_cap", C.c_int),
+        ("pred_queue_cap", C.c_int),
+        ("max_updates", C.c_longlong), ("max_seconds", C.c_double), ("target_score", C.c_double),
+        ("has_target_score", C.c_int),
+        ("seed", C.c_ulonglong), ("anneal", C.c_int), ("anneal_batches", C.c_int), ("epoch_s", C.c_double),
+        ("max_agents", C.c_int), ("max_predictors", C.c_int), ("max_trainers", C.c_int),
+        ("metrics_interval_s", C.c_double),
+        ("greedy", C.c_int), ("sync_after_submit", C.c_int), ("capture_trajectory", C.c_int), ("device", C.c_int),
+    ]
+
+
+class RunReportC(C.Structure):
+    """ga3c_run_report (include/ga3c.h)."""
+
+    _fields_ = [
+        ("total_updates", C.c_longlong), ("skipped_updates", C.c_longlong),
+        ("total_predictions", C.c_longlong), ("total_episodes", C.c_longlong),
+        ("wall_time_s", C.c_double), ("avg_tps", C.c_double), ("avg_pps", C.c_double),
+        ("avg_samples_per_s", C.c_double), ("mean_lag", C.c_double), ("final_rolling_score", C.c_double),
+        ("experiences_produced", C.c_longlong), ("experiences_trained", C.c_longlong),
+        ("experiences_dropped", C.c_longlong), ("experiences_left_queued", C.c_longlong),
+        ("final_n_agents", C.c_int), ("final_n_predictors", C.c_int), ("final_n_trainers", C.c_int),
+        ("final_pred_batch_max", C.c_int), ("final_min_train_batch", C.c_int),
+        ("final_version", C.c_ulonglong),
+        ("n_trajectory", C.c_int), ("n_anneal", C.c_int), ("n_frames", C.c_int),
+        ("last_frame_tps", C.c_double), ("last_frame_pps", C.c_double), ("last_frame_pred_batch_mean", C.c_double),
+    ]
+
+
+class AnnealEntry(C.Structure):
+    _fields_ = [("n_agents", C.c_int), ("n_predictors", C.c_int), ("n_trainers", C.c_int),
+                ("pred_batch_max", C.c_int), ("min_train_batch", C.c_int), ("measured_tps", C.c_double),
+                ("accepted", C.c_int)]
+
+
 _P = C.c_void_p
 _SIGS = {
     "ga3c_status_string": (C.c_char_p, [C.c_int]),
@@ -69,6 +112,7 @@ _SIGS = {
     "ga3c_model_read": (C.c_int, [_P, _P, _P, C.POINTER(C.c_uint64)]),
     "ga3c_model_version": (C.c_uint64, [_P]),
     "ga3c_model_param_count": (C.c_size_t, [_P]),
+    "ga3c_model_n_actions": (C.c_int, [_P]),
     "ga3c_snapshot_acquire": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_uint64)]),
     "ga3c_snapshot_release": (C.c_int, [_P, C.c_int]),
     "ga3c_model_last_error": (C.c_char_p, [_P]),
@@ -83,6 +127,10 @@ _SIGS = {
     "ga3c_loss_grad_u8": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, C.c_int, _P, _P]),
     "ga3c_loss_grad_f32": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, C.c_int, _P, _P]),
     "ga3c_loss_grad_dev": (C.c_int, [_P, C.c_int, _P, C.c_int, C.c_longlong, _P, _P, C.c_int, C.c_int]),
+    "ga3c_loss_grad_segments_u8": (C.c_int, [_P, C.c_int, _P, C.c_int, _P, _P, _P, C.c_int, _P, _P,
+                                             C.c_double, C.c_int, _P, _P]),
+    "ga3c_loss_grad_segments_f32": (C.c_int, [_P, C.c_int, _P, C.c_int, _P, _P, _P, C.c_int, _P, _P,
+                                              C.c_double, C.c_int, _P, _P]),
     "ga3c_ctx_grad": (_P, [_P]),
     "ga3c_ctx_last_values": (_P, [_P]),
     "ga3c_ctx_read_grad": (C.c_int, [_P, _P, _P]),
@@ -94,6 +142,9 @@ _SIGS = {
     "ga3c_compute_returns_dev": (C.c_int, [_P, _P, _P, C.c_int, _P, _P, C.c_double, _P]),
     "ga3c_sample_actions_dev": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, _P, C.c_int]),
     "ga3c_ctx_time_kernel": (C.c_int, [_P, C.c_int, C.c_int]),
+    "ga3c_default_pipeline_opts": (None, [C.POINTER(PipelineOpts)]),
+    "ga3c_pipeline_run": (C.c_int, [C.POINTER(PipelineOpts), C.c_int, C.POINTER(RunReportC), _P, _P, C.c_int,
+                                    _P, C.c_int, _P, C.c_int, C.c_char_p, C.c_int]),
     "ga3c_ctx_graph_begin": (C.c_int, [_P]),
     "ga3c_ctx_graph_end": (C.c_int, [_P, C.POINTER(C.c_int)]),
     "ga3c_ctx_graph_launch": (C.c_int, [_P, C.c_int]),
@@ -267,6 +318,25 @@ class Context:
                                         int(apply_clip), ptr(d), ptr(sc))
         check(rc, self.model.error())
         return d, sc
+
+    def loss_grad_segments(self, states, actions, rewards, seg_offsets, terminal, bootstrap, gamma,
+                           slot=-1, apply_clip=True):
+        """Trainer step with device-side n-step returns -> (scalars, returns)."""
+        states = np.ascontiguousarray(states)
+        B = states.shape[0]
+        a = np.ascontiguousarray(actions, np.int32)
+        r = np.ascontiguousarray(rewards, np.float64)
+        off = np.ascontiguousarray(seg_offsets, np.int32)
+        term = np.ascontiguousarray(terminal, np.uint8)
+        boot = np.ascontiguousarray(bootstrap, np.float64)
+        sc = np.zeros(3, np.float64)
+        rets = np.zeros(B, np.float64)
+        f = lib.ga3c_loss_grad_segments_u8 if states.dtype == np.uint8 else lib.ga3c_loss_grad_segments_f32
+        if states.dtype != np.uint8:
+            states = np.ascontiguousarray(states, np.float32)
+        check(f(self.h, slot, ptr(states), B, ptr(a), ptr(r), ptr(off), len(off) - 1, ptr(term), ptr(boot),
+                float(gamma), int(apply_clip), ptr(sc), ptr(rets)), self.model.error())
+        return sc, rets
 
     def apply_rmsprop(self, dtheta=None):
         """SharedModel::apply -> (applied, applied_on_version)."""

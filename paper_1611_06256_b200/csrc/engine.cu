@@ -820,6 +820,8 @@ uint64_t ga3c_model_version(ga3c_model* m) {
 
 size_t ga3c_model_param_count(ga3c_model* m) { return m ? m->lo.total : 0; }
 
+int ga3c_model_n_actions(ga3c_model* m) { return m ? m->lo.n_actions : 0; }
+
 int ga3c_snapshot_acquire(ga3c_model* m, int* slot, uint64_t* version) {
   if (!m || !slot) return GA3C_INVALID_ARGUMENT;
   std::lock_guard<std::mutex> lk(m->read_m);
@@ -1321,6 +1323,100 @@ int ga3c_ctx_graph_launch(ga3c_ctx* c, int graph_id) {
   auto set_err = [&](const std::string& e) { m->set_error(e); };
   GA3C_CUDA(cudaGraphLaunch(c->graphs[graph_id], c->stream));
   return GA3C_OK;
+}
+
+// Trainer step on host buffers with the n-step returns computed on the device
+// (returns.cpp:8-26 for every segment, then nnet.cpp:201-291): one upload,
+// returns_kernel -> loss/backward kernels on the context stream, scalars back.
+static int loss_grad_segments(ga3c_ctx* c, int slot, const void* states, bool u8, int B,
+                              const int32_t* actions, const double* rewards, const int32_t* off,
+                              int n_seg, const uint8_t* terminal, const double* bootstrap, double gamma,
+                              int apply_clip, double* scalars, double* returns_out) {
+  if (!c || B < 1 || B > c->max_batch || !states || !actions || !rewards || !off || n_seg < 1 ||
+      !terminal || !bootstrap)
+    return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  if (!(gamma > 0.0) || gamma > 1.0 || off[0] != 0 || off[n_seg] != B) return GA3C_INVALID_ARGUMENT;
+  for (int s = 0; s < n_seg; ++s) {
+    if (off[s + 1] <= off[s]) return GA3C_INVALID_ARGUMENT;
+    if (!terminal[s] && !std::isfinite(bootstrap[s])) return GA3C_NONFINITE_INPUT;
+  }
+  for (int b = 0; b < B; ++b) {
+    if (!std::isfinite(rewards[b])) return GA3C_NONFINITE_INPUT;
+    if (actions[b] < 0 || actions[b] >= m->lo.n_actions) return GA3C_INVALID_ARGUMENT;
+  }
+  const std::size_t dim = m->lo.in_dim;
+  if (!u8 && !all_finite(static_cast<const float*>(states), dim * B)) return GA3C_NONFINITE_INPUT;
+  if (set_device(m)) return GA3C_CUDA_ERROR;
+  if ((std::size_t)B > c->r_cap) {
+    cudaFree(c->r_rew);
+    cudaFree(c->r_out);
+    c->r_cap = std::max<std::size_t>(B, 1024);
+    GA3C_CUDA(cudaMalloc(&c->r_rew, c->r_cap * sizeof(double)));
+    GA3C_CUDA(cudaMalloc(&c->r_out, c->r_cap * sizeof(double)));
+  }
+  if ((std::size_t)n_seg > c->r_seg_cap) {
+    cudaFree(c->r_off);
+    cudaFree(c->r_term);
+    cudaFree(c->r_boot);
+    c->r_seg_cap = std::max<std::size_t>(n_seg, 256);
+    GA3C_CUDA(cudaMalloc(&c->r_off, (c->r_seg_cap + 1) * sizeof(int32_t)));
+    GA3C_CUDA(cudaMalloc(&c->r_term, c->r_seg_cap));
+    GA3C_CUDA(cudaMalloc(&c->r_boot, c->r_seg_cap * sizeof(double)));
+  }
+  int s = slot;
+  const bool pinned_here = slot < 0;
+  if (pinned_here) ga3c_snapshot_acquire(m, &s, nullptr);
+  int rc = GA3C_OK;
+  const std::size_t bytes = dim * B * (u8 ? 1 : sizeof(float));
+  if (cudaMemcpyAsync(c->d_in, states, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+      cudaMemcpyAsync(c->d_actions, actions, sizeof(int32_t) * B, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+      cudaMemcpyAsync(c->r_rew, rewards, sizeof(double) * B, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+      cudaMemcpyAsync(c->r_off, off, sizeof(int32_t) * (n_seg + 1), cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+      cudaMemcpyAsync(c->r_term, terminal, n_seg, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+      cudaMemcpyAsync(c->r_boot, bootstrap, sizeof(double) * n_seg, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+    rc = GA3C_CUDA_ERROR;
+  if (!rc) {
+    {
+      Launch l(c, GA3C_K_RETURNS, -1);
+      pdl_launch(c->stream, returns_kernel, dim3((n_seg + 127) / 128), dim3(128), 0, c->r_rew,
+                 (const int32_t*)c->r_off, n_seg, (const uint8_t*)c->r_term, (const double*)c->r_boot, gamma,
+                 c->d_rets);
+    }
+    run_loss_grad(c, m->slots[s].theta, c->d_in, u8, c->d_actions, c->d_rets, B, apply_clip != 0);
+    if (scalars &&
+        cudaMemcpyAsync(scalars, c->scal_sum, sizeof(double) * 3, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+      rc = GA3C_CUDA_ERROR;
+    if (!rc && returns_out &&
+        cudaMemcpyAsync(returns_out, c->d_rets, sizeof(double) * B, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+      rc = GA3C_CUDA_ERROR;
+  }
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    rc = GA3C_CUDA_ERROR;
+    set_err(std::string("loss_grad_segments: ") + cudaGetErrorString(e));
+  }
+  if (pinned_here) ga3c_snapshot_release(m, s);
+  return rc;
+}
+
+int ga3c_loss_grad_segments_u8(ga3c_ctx* c, int slot, const uint8_t* frames, int B,
+                               const int32_t* actions, const double* rewards,
+                               const int32_t* seg_offsets, int n_seg, const uint8_t* terminal,
+                               const double* bootstrap, double gamma, int apply_clip,
+                               double* scalars, double* returns_out) {
+  return loss_grad_segments(c, slot, frames, true, B, actions, rewards, seg_offsets, n_seg, terminal,
+                            bootstrap, gamma, apply_clip, scalars, returns_out);
+}
+
+int ga3c_loss_grad_segments_f32(ga3c_ctx* c, int slot, const float* states, int B,
+                                const int32_t* actions, const double* rewards,
+                                const int32_t* seg_offsets, int n_seg, const uint8_t* terminal,
+                                const double* bootstrap, double gamma, int apply_clip,
+                                double* scalars, double* returns_out) {
+  return loss_grad_segments(c, slot, states, false, B, actions, rewards, seg_offsets, n_seg, terminal,
+                            bootstrap, gamma, apply_clip, scalars, returns_out);
 }
 
 }  // extern "C"

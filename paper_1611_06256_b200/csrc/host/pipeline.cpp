@@ -1,0 +1,792 @@
+// pipeline.cpp -- the GA3C engine on the B200 C ABI (see ga3c_host.hpp).
+//
+// Thread structure and stop/shutdown protocol follow the reference engine
+// (/root/reference/proj/src/pipeline.cpp:101-612); the math calls go to the
+// device: predictors run ga3c_forward_* on a pinned snapshot slot, trainers
+// run ga3c_loss_grad_segments_* (device n-step returns + loss/backward) on a
+// snapshot and SharedModel::apply (out-of-place RMSProp on the latest slot).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <thread>
+
+#include "ga3c_host.hpp"
+
+namespace ga3c::host {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double seconds_between(Clock::time_point a, Clock::time_point b) {
+  return std::chrono::duration<double>(b - a).count();
+}
+
+void check(int st, ga3c_model* m, const char* what) {
+  if (st == GA3C_OK) return;
+  std::string msg = std::string(what) + ": " + ga3c_status_string(st) + " (" + ga3c_model_last_error(m) + ")";
+  if (st == GA3C_INVALID_ARGUMENT || st == GA3C_NONFINITE_INPUT) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+// RAII per-thread device context (stream + workspace)
+struct Ctx {
+  ga3c_ctx* c = nullptr;
+  int max_batch = 0;
+  ga3c_model* m = nullptr;
+  Ctx(ga3c_model* model, int mb) : m(model) { reset(mb); }
+  ~Ctx() {
+    if (c) ga3c_ctx_destroy(c);
+  }
+  Ctx(const Ctx&) = delete;
+  Ctx& operator=(const Ctx&) = delete;
+  void reset(int mb) {
+    if (c) ga3c_ctx_destroy(c);
+    int st = 0;
+    c = ga3c_ctx_create(m, mb, &st);
+    if (!c) check(st ? st : GA3C_CUDA_ERROR, m, "ga3c_ctx_create");
+    max_batch = mb;
+  }
+  void ensure(int B) {
+    if (B > max_batch) reset(std::max(B, 2 * max_batch));
+  }
+};
+
+// Contiguous host batch of observations for one device call.
+struct HostBatch {
+  bool u8 = false;
+  std::vector<std::uint8_t> b8;
+  std::vector<float> bf;
+  void clear() {
+    b8.clear();
+    bf.clear();
+  }
+  void add(const Observation& o) {
+    if (u8)
+      b8.insert(b8.end(), o.u8.begin(), o.u8.end());
+    else
+      bf.insert(bf.end(), o.f32.begin(), o.f32.end());
+  }
+};
+
+// One trainer step on a merged group of agent segments (flush +
+// trainer_main math, pipeline.cpp:207-237 / 265-287): device returns, loss
+// and gradients on `snap`; the gradient stays in ctx for apply().
+void train_on(Ctx& ctx, int slot, const std::vector<ExperienceBatch>& group, const ga3c_hyper& hp,
+              HostBatch& hb, std::vector<std::int32_t>& acts, std::vector<double>& rew,
+              std::vector<std::int32_t>& off, std::vector<std::uint8_t>& term, std::vector<double>& boot) {
+  hb.clear();
+  acts.clear();
+  rew.clear();
+  off.assign(1, 0);
+  term.clear();
+  boot.clear();
+  hb.u8 = !group.front().experiences.front().state.u8.empty();
+  for (const auto& b : group) {
+    for (const auto& e : b.experiences) {
+      hb.add(e.state);
+      acts.push_back(e.action);
+      rew.push_back(e.reward);
+    }
+    off.push_back(static_cast<std::int32_t>(acts.size()));
+    term.push_back(b.terminal ? 1 : 0);
+    boot.push_back(b.terminal ? 0.0 : b.bootstrap);
+  }
+  const int B = static_cast<int>(acts.size());
+  ctx.ensure(B);
+  const int n_seg = static_cast<int>(term.size());
+  const int st = hb.u8 ? ga3c_loss_grad_segments_u8(ctx.c, slot, hb.b8.data(), B, acts.data(), rew.data(),
+                                                    off.data(), n_seg, term.data(), boot.data(), hp.gamma, 1,
+                                                    nullptr, nullptr)
+                       : ga3c_loss_grad_segments_f32(ctx.c, slot, hb.bf.data(), B, acts.data(), rew.data(),
+                                                     off.data(), n_seg, term.data(), boot.data(), hp.gamma, 1,
+                                                     nullptr, nullptr);
+  check(st, ctx.m, "loss_grad_segments");
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ SharedModel
+SharedModel::SharedModel(const ga3c_net_spec& spec, const ga3c_hyper& hp, int device, std::uint64_t seed) {
+  int st = 0;
+  m_ = ga3c_model_create(&spec, &hp, device, &st);
+  if (!m_) check(st ? st : GA3C_CUDA_ERROR, nullptr, "ga3c_model_create");
+  std::vector<float> th(ga3c_param_count(&spec));
+  check(ga3c_init_params(&spec, seed, nullptr, th.data()), m_, "ga3c_init_params");  // nnet.cpp:152-168
+  check(ga3c_model_load(m_, th.data(), nullptr, 0), m_, "ga3c_model_load");
+}
+
+SharedModel::~SharedModel() { ga3c_model_destroy(m_); }
+
+std::shared_ptr<const SharedModel::Snapshot> SharedModel::snapshot() const {  // pipeline.cpp:22-25
+  Snapshot s{};
+  check(ga3c_snapshot_acquire(m_, &s.slot, &s.version), m_, "snapshot");
+  ga3c_model* m = m_;
+  return std::shared_ptr<const Snapshot>(new Snapshot(s), [m](const Snapshot* p) {
+    ga3c_snapshot_release(m, p->slot);
+    delete p;
+  });
+}
+
+std::uint64_t SharedModel::version() const { return ga3c_model_version(m_); }
+
+std::optional<std::uint64_t> SharedModel::apply(ga3c_ctx* ctx, const std::function<void(SharedModel&)>& on_applied) {
+  std::lock_guard<std::mutex> lk(apply_m_);  // orders on_applied with the publish
+  int applied = 0;
+  std::uint64_t on = 0;
+  const int st = ga3c_apply_rmsprop(ctx, nullptr, &applied, &on);
+  if (st == GA3C_NOT_APPLIED) return std::nullopt;  // nnet.cpp:299-301
+  check(st, m_, "apply_rmsprop");
+  if (on_applied) on_applied(*this);
+  return on;
+}
+
+std::vector<float> SharedModel::read_theta() const {
+  std::vector<float> th(ga3c_model_param_count(m_));
+  check(ga3c_model_read(m_, th.data(), nullptr, nullptr), m_, "model_read");
+  return th;
+}
+
+// -------------------------------------------------------- predictor_loop
+void predictor_loop(BoundedChannel<PredictionRequest>& requests,
+                    std::vector<std::unique_ptr<ResponseSlot<PredictionResponse>>>& slots,
+                    SharedModel& model, ga3c_ctx* ctx, int pred_batch_max, PredictorMetrics& metrics,
+                    const std::atomic<bool>& stop) {
+  std::vector<PredictionRequest> got;
+  HostBatch hb;
+  std::vector<float> pi, v;
+  while (!stop.load(std::memory_order_relaxed)) {
+    auto first = requests.pop(&stop);  // block for the first (pipeline.cpp:72)
+    if (!first) break;
+    got.clear();
+    got.push_back(std::move(*first));
+    while (static_cast<int>(got.size()) < pred_batch_max) {  // drain (pipeline.cpp:76-80)
+      auto more = requests.try_pop();
+      if (!more) break;
+      got.push_back(std::move(*more));
+    }
+    hb.u8 = !got.front().state.u8.empty();
+    hb.clear();
+    for (auto& r : got) hb.add(r.state);
+    const int B = static_cast<int>(got.size());
+    const auto snap = model.snapshot();
+    const int A = ga3c_model_n_actions(model.handle());
+    pi.resize(static_cast<std::size_t>(B) * A);
+    v.resize(B);
+    std::uint64_t ver = 0;
+    const int st = hb.u8 ? ga3c_forward_u8(ctx, snap->slot, hb.b8.data(), B, pi.data(), v.data(), &ver)
+                         : ga3c_forward_f32(ctx, snap->slot, hb.bf.data(), B, pi.data(), v.data(), &ver);
+    check(st, model.handle(), "forward");
+    for (int i = 0; i < B; ++i) {
+      PredictionResponse resp;
+      resp.policy.assign(pi.begin() + static_cast<std::ptrdiff_t>(i) * A,
+                         pi.begin() + static_cast<std::ptrdiff_t>(i + 1) * A);
+      resp.value = v[i];
+      resp.model_version = ver;
+      slots[got[i].agent_id]->put(got[i].ticket, std::move(resp));
+    }
+    metrics.predictions.fetch_add(B, std::memory_order_relaxed);
+    metrics.batches.fetch_add(1, std::memory_order_relaxed);
+  }
+}
+
+// ---------------------------------------------------------------- validate
+void validate(const PipelineOptions& opt) {  // pipeline.cpp:572-603
+  check(ga3c_validate_spec(&opt.net), nullptr, "NetworkSpec");
+  check(ga3c_validate_hyper(&opt.hyper), nullptr, "Hyperparams");
+  validate(opt.env);
+  validate(opt.knobs);
+  if (!opt.stop.max_updates && !opt.stop.max_seconds && !opt.stop.target_score)
+    throw std::invalid_argument("pipeline: no stop condition set");
+  if (opt.stop.max_updates && *opt.stop.max_updates < 1)
+    throw std::invalid_argument("pipeline: max_updates must be >= 1");
+  if (opt.stop.max_seconds && !(*opt.stop.max_seconds > 0.0))
+    throw std::invalid_argument("pipeline: max_seconds must be > 0");
+  if (!(opt.metrics_interval_s > 0.0)) throw std::invalid_argument("pipeline: metrics interval must be > 0");
+  if (opt.anneal) {
+    if (!(opt.epoch_s > 0.0)) throw std::invalid_argument("pipeline: epoch length must be > 0");
+    if (opt.sync_after_submit) throw std::invalid_argument("pipeline: lockstep mode cannot anneal");
+  }
+  if (opt.sync_after_submit && (opt.knobs.n_agents != 1 || opt.knobs.n_predictors != 1 ||
+                                opt.knobs.n_trainers != 1 || opt.knobs.min_train_batch != 1))
+    throw std::invalid_argument(
+        "pipeline: lockstep mode requires one agent, one predictor, one trainer and min_train_batch 1");
+  auto probe = make_env(opt.env);
+  const ga3c_net_spec in = probe->input();
+  if (in.in_h != opt.net.in_h || in.in_w != opt.net.in_w || in.in_c != opt.net.in_c)
+    throw std::invalid_argument("pipeline: net input does not match env observation");
+  if (probe->action_count() != opt.net.n_actions)
+    throw std::invalid_argument("pipeline: net n_actions does not match env action_count");
+}
+
+// ------------------------------------------------------------------ Engine
+namespace {
+
+struct Worker {
+  std::unique_ptr<std::atomic<bool>> stop;
+  std::thread thread;
+};
+
+class Engine {
+ public:
+  explicit Engine(const PipelineOptions& opt)
+      : opt_(opt),
+        slot_cap_(static_cast<std::size_t>(opt.anneal ? std::max(opt.limits.max_agents, opt.knobs.n_agents)
+                                                      : opt.knobs.n_agents)),
+        shared_(opt.net, opt.hyper, opt.device, derive_seed(opt.seed, {kSeedModelInit})),
+        pred_q_(opt.knobs.pred_queue_cap > 0 ? static_cast<std::size_t>(opt.knobs.pred_queue_cap) : slot_cap_),
+        train_q_(static_cast<std::size_t>(opt.knobs.train_queue_cap)),
+        budget_(opt.stop.max_updates ? *opt.stop.max_updates : std::numeric_limits<std::int64_t>::max()) {
+    for (std::size_t i = 0; i < slot_cap_; ++i) slots_.push_back(std::make_unique<ResponseSlot<PredictionResponse>>());
+    if (opt_.capture_trajectory)
+      traj_sink_ = [this](SharedModel& m) {
+        std::lock_guard<std::mutex> lk(traj_m_);
+        trajectory_.push_back(m.read_theta());
+      };
+  }
+
+  ~Engine() {
+    request_stop();
+    join_all();
+  }
+
+  RunReport run_all() {
+    t0_ = Clock::now();
+    {
+      std::lock_guard<std::mutex> lk(workers_m_);
+      for (int i = 0; i < opt_.knobs.n_agents; ++i) add_agent_locked();
+      for (int i = 0; i < opt_.knobs.n_predictors; ++i) add_predictor_locked();
+      for (int i = 0; i < opt_.knobs.n_trainers; ++i) add_trainer_locked();
+    }
+    try {
+      control_loop();
+    } catch (...) {
+      report_error(std::current_exception());
+    }
+    shutdown();
+    if (first_error_) std::rethrow_exception(first_error_);
+    return make_report();
+  }
+
+ private:
+  // ---- agents (pipeline.cpp:153-205)
+  void agent_main(int id, std::atomic<bool>& stop) {
+    try {
+      auto env = make_env(opt_.env);
+      std::mt19937_64 rng(derive_seed(opt_.seed, {kSeedAgentRng, static_cast<std::uint64_t>(id)}));
+      std::uint64_t episode = 0;
+      Observation obs = env->reset(derive_seed(opt_.seed, {kSeedEnvEpisode, static_cast<std::uint64_t>(id), episode}));
+      ExperienceBatch batch;
+      batch.agent_id = id;
+      double score = 0.0;
+      std::int64_t submitted = 0;
+      while (!stop.load(std::memory_order_relaxed)) {
+        auto& slot = *slots_[id];
+        const std::uint64_t ticket = slot.issue_ticket();
+        if (!pred_q_.push(PredictionRequest{id, ticket, obs}, &stop)) break;
+        auto resp = slot.take(ticket, stop);
+        if (!resp) break;
+        const int A = static_cast<int>(resp->policy.size());
+        const int action = opt_.greedy ? argmax_index(resp->policy.data(), A)
+                                       : sample_index(resp->policy.data(), A, rng);
+        StepResult sr = env->step(action);
+        const double reward = opt_.hyper.clip_rewards ? std::clamp(sr.reward, -1.0, 1.0) : sr.reward;
+        batch.experiences.push_back(Experience{std::move(obs), action, reward, resp->value, resp->model_version});
+        produced_.fetch_add(1, std::memory_order_relaxed);
+        score += sr.reward;
+        bool ok = true;
+        if (sr.terminal) {
+          ok = flush(batch, true, 0.0, stop, submitted);
+          record_episode(score);
+          score = 0.0;
+          ++episode;
+          obs = env->reset(derive_seed(opt_.seed, {kSeedEnvEpisode, static_cast<std::uint64_t>(id), episode}));
+        } else {
+          obs = std::move(sr.observation);
+          if (static_cast<int>(batch.experiences.size()) >= opt_.hyper.t_max)
+            ok = flush(batch, false, resp->value, stop, submitted);  // G8: value just played
+        }
+        if (!ok) break;
+      }
+      if (!batch.experiences.empty()) dropped_.fetch_add(static_cast<std::int64_t>(batch.experiences.size()));
+    } catch (...) {
+      report_error(std::current_exception());
+    }
+  }
+
+  bool flush(ExperienceBatch& batch, bool terminal, double bootstrap, std::atomic<bool>& stop,
+             std::int64_t& submitted) {  // pipeline.cpp:207-237 (returns on the trainer's device)
+    batch.terminal = terminal;
+    batch.bootstrap = bootstrap;
+    ExperienceBatch out;
+    out.agent_id = batch.agent_id;
+    std::swap(out, batch);
+    batch.agent_id = out.agent_id;
+    batch.experiences.clear();
+    const auto n = static_cast<std::int64_t>(out.experiences.size());
+    if (!train_q_.push(std::move(out), &stop)) {
+      dropped_.fetch_add(n);
+      return false;
+    }
+    if (opt_.sync_after_submit) {
+      ++submitted;
+      std::unique_lock<std::mutex> lk(gate_m_);
+      gate_cv_.wait(lk, [&] {
+        return gate_updates_.load(std::memory_order_relaxed) >= submitted || stop.load(std::memory_order_relaxed);
+      });
+      if (gate_updates_.load(std::memory_order_relaxed) < submitted) return false;
+    }
+    return true;
+  }
+
+  // ---- trainers (pipeline.cpp:241-306)
+  void trainer_main(std::atomic<bool>& stop) {
+    try {
+      Ctx ctx(shared_.handle(), std::max(64, opt_.knobs.min_train_batch + 4 * opt_.hyper.t_max));
+      HostBatch hb;
+      std::vector<std::int32_t> acts, off;
+      std::vector<double> rew, boot;
+      std::vector<std::uint8_t> term;
+      while (!stop.load(std::memory_order_relaxed)) {
+        auto first = train_q_.pop(&stop);
+        if (!first) break;
+        std::vector<ExperienceBatch> group;
+        std::int64_t total = static_cast<std::int64_t>(first->experiences.size());
+        group.push_back(std::move(*first));
+        bool bail = false;
+        while (total < opt_.knobs.min_train_batch) {
+          auto more = train_q_.pop(&stop);
+          if (!more) {
+            bail = true;
+            break;
+          }
+          total += static_cast<std::int64_t>(more->experiences.size());
+          group.push_back(std::move(*more));
+        }
+        if (bail) {
+          dropped_.fetch_add(total);
+          break;
+        }
+        if (budget_.fetch_sub(1, std::memory_order_acq_rel) <= 0) {
+          budget_.fetch_add(1, std::memory_order_relaxed);
+          dropped_.fetch_add(total);
+          request_stop();
+          break;
+        }
+        const std::size_t backlog = train_q_.size();
+        (void)backlog;
+        const auto snap = shared_.snapshot();
+        train_on(ctx, snap->slot, group, opt_.hyper, hb, acts, rew, off, term, boot);
+        const auto applied_on = shared_.apply(ctx.c, traj_sink_);
+        if (applied_on) {
+          std::uint64_t lag_sum = 0;
+          for (const auto& b : group)
+            for (const auto& e : b.experiences) lag_sum += *applied_on - e.produced_version;
+          bump_gate();
+          lag_sum_.fetch_add(lag_sum, std::memory_order_relaxed);
+          trained_.fetch_add(total, std::memory_order_relaxed);
+          const auto u = updates_.fetch_add(1, std::memory_order_relaxed) + 1;
+          if (opt_.stop.max_updates && u >= *opt_.stop.max_updates) request_stop();
+        } else {
+          budget_.fetch_add(1, std::memory_order_relaxed);
+          skipped_.fetch_add(1, std::memory_order_relaxed);
+        }
+      }
+    } catch (...) {
+      report_error(std::current_exception());
+    }
+  }
+
+  void bump_gate() {
+    gate_updates_.fetch_add(1, std::memory_order_relaxed);
+    if (opt_.sync_after_submit) {
+      std::lock_guard<std::mutex> lk(gate_m_);
+      gate_cv_.notify_all();
+    }
+  }
+
+  void predictor_main(std::atomic<bool>& stop) {
+    try {
+      Ctx ctx(shared_.handle(), opt_.knobs.pred_batch_max);
+      predictor_loop(pred_q_, slots_, shared_, ctx.c, opt_.knobs.pred_batch_max, pmetrics_, stop);
+    } catch (...) {
+      report_error(std::current_exception());
+    }
+  }
+
+  // ---- worker management (pipeline.cpp:318-407)
+  void add_agent_locked() {
+    if (stop_requested_.load()) return;
+    const int id = next_agent_id_++;
+    if (static_cast<std::size_t>(id) >= slot_cap_) throw std::logic_error("pipeline: agent id exceeds slot capacity");
+    auto& w = agents_.emplace_back();
+    w.stop = std::make_unique<std::atomic<bool>>(false);
+    w.thread = std::thread([this, id, s = w.stop.get()] { agent_main(id, *s); });
+    n_a_.fetch_add(1);
+  }
+  void add_predictor_locked() {
+    if (stop_requested_.load()) return;
+    auto& w = predictors_.emplace_back();
+    w.stop = std::make_unique<std::atomic<bool>>(false);
+    w.thread = std::thread([this, s = w.stop.get()] { predictor_main(*s); });
+    n_p_.fetch_add(1);
+  }
+  void add_trainer_locked() {
+    if (stop_requested_.load()) return;
+    auto& w = trainers_.emplace_back();
+    w.stop = std::make_unique<std::atomic<bool>>(false);
+    w.thread = std::thread([this, s = w.stop.get()] { trainer_main(*s); });
+    n_t_.fetch_add(1);
+  }
+  void remove_last(std::deque<Worker>& pool, std::atomic<std::int64_t>& counter) {
+    std::thread t;
+    {
+      std::lock_guard<std::mutex> lk(workers_m_);
+      if (pool.empty()) return;
+      pool.back().stop->store(true);
+      wake_everything();
+      t = std::move(pool.back().thread);
+    }
+    t.join();
+    {
+      std::lock_guard<std::mutex> lk(workers_m_);
+      pool.pop_back();
+      if (&pool == &agents_) --next_agent_id_;
+    }
+    counter.fetch_sub(1);
+  }
+  void wake_everything() {
+    pred_q_.wake_all();
+    train_q_.wake_all();
+    for (auto& s : slots_) s->wake();
+    gate_cv_.notify_all();
+  }
+  void request_stop() {
+    std::lock_guard<std::mutex> lk(workers_m_);
+    stop_requested_.store(true);
+    for (auto* pool : {&agents_, &predictors_, &trainers_})
+      for (auto& w : *pool) w.stop->store(true);
+    wake_everything();
+  }
+  void report_error(std::exception_ptr e) {
+    {
+      std::lock_guard<std::mutex> lk(err_m_);
+      if (!first_error_) first_error_ = e;
+    }
+    request_stop();
+  }
+  void apply_knobs(const KnobConfig& t) {
+    while (n_a_.load() > t.n_agents && !stop_requested_.load()) remove_last(agents_, n_a_);
+    while (n_p_.load() > t.n_predictors && !stop_requested_.load()) remove_last(predictors_, n_p_);
+    while (n_t_.load() > t.n_trainers && !stop_requested_.load()) remove_last(trainers_, n_t_);
+    // batch geometry (only moved with anneal_batches): restart the pools it configures
+    if (t.pred_batch_max != live_.pred_batch_max || t.min_train_batch != live_.min_train_batch) {
+      live_.pred_batch_max = t.pred_batch_max;
+      live_.min_train_batch = t.min_train_batch;
+      opt_.knobs.pred_batch_max = t.pred_batch_max;
+      opt_.knobs.min_train_batch = t.min_train_batch;
+      while (n_p_.load() > 0 && !stop_requested_.load()) remove_last(predictors_, n_p_);
+      while (n_t_.load() > 0 && !stop_requested_.load()) remove_last(trainers_, n_t_);
+    }
+    std::lock_guard<std::mutex> lk(workers_m_);
+    while (n_a_.load() < t.n_agents && !stop_requested_.load()) add_agent_locked();
+    while (n_p_.load() < t.n_predictors && !stop_requested_.load()) add_predictor_locked();
+    while (n_t_.load() < t.n_trainers && !stop_requested_.load()) add_trainer_locked();
+  }
+
+  void record_episode(double score) {
+    std::lock_guard<std::mutex> lk(scores_m_);
+    scores_.push_back(score);
+  }
+  double rolling_score() {
+    std::lock_guard<std::mutex> lk(scores_m_);
+    if (scores_.empty()) return 0.0;
+    const std::size_t n = std::min<std::size_t>(30, scores_.size());
+    double s = 0.0;
+    for (std::size_t i = scores_.size() - n; i < scores_.size(); ++i) s += scores_[i];
+    return s / static_cast<double>(n);
+  }
+  std::int64_t n_episodes() {
+    std::lock_guard<std::mutex> lk(scores_m_);
+    return static_cast<std::int64_t>(scores_.size());
+  }
+
+  MetricsFrame frame(double window) {
+    MetricsFrame f;
+    const auto u = updates_.load(), p = pmetrics_.predictions.load(), b = pmetrics_.batches.load(),
+               tr = trained_.load();
+    const auto now = Clock::now();
+    f.wall_time_s = seconds_between(t0_, now);
+    f.tps = (u - last_u_) / window;
+    f.pps = (p - last_p_) / window;
+    f.samples_per_s = (tr - last_tr_) / window;
+    f.pred_batch_mean = b > last_b_ ? static_cast<double>(p - last_p_) / static_cast<double>(b - last_b_) : 0.0;
+    f.mean_lag = tr > 0 ? static_cast<double>(lag_sum_.load()) / static_cast<double>(tr) : 0.0;
+    f.n_a = static_cast<int>(n_a_.load());
+    f.n_p = static_cast<int>(n_p_.load());
+    f.n_t = static_cast<int>(n_t_.load());
+    f.updates_total = u;
+    f.score_mean = rolling_score();
+    last_u_ = u;
+    last_p_ = p;
+    last_b_ = b;
+    last_tr_ = tr;
+    return f;
+  }
+
+  void control_loop() {  // pipeline.cpp:409-479
+    using namespace std::chrono_literals;
+    live_ = opt_.knobs;
+    auto next_frame = t0_ + std::chrono::duration_cast<Clock::duration>(std::chrono::duration<double>(opt_.metrics_interval_s));
+    auto last_frame = t0_;
+    std::optional<AnnealState> ann;
+    std::optional<KnobConfig> cand;
+    auto epoch_start = t0_;
+    std::int64_t half_updates = -1;
+    Clock::time_point half_time;
+    if (opt_.anneal)
+      ann = make_anneal_state(opt_.knobs, opt_.epoch_s, derive_seed(opt_.seed, {kSeedAnneal}), opt_.limits,
+                              opt_.anneal_batches);
+    while (!stop_requested_.load()) {
+      std::this_thread::sleep_for(2ms);
+      {
+        std::lock_guard<std::mutex> lk(err_m_);
+        if (first_error_) break;
+      }
+      const auto now = Clock::now();
+      if (opt_.stop.max_seconds && seconds_between(t0_, now) >= *opt_.stop.max_seconds) break;
+      if (opt_.stop.max_updates && updates_.load() >= *opt_.stop.max_updates) break;
+      if (opt_.stop.target_score && n_episodes() >= 30 && rolling_score() >= *opt_.stop.target_score) break;
+      if (now >= next_frame) {
+        frames_.push_back(frame(seconds_between(last_frame, now)));
+        last_frame = now;
+        next_frame += std::chrono::duration_cast<Clock::duration>(std::chrono::duration<double>(opt_.metrics_interval_s));
+      }
+      if (ann) {
+        const double into = seconds_between(epoch_start, now);
+        if (half_updates < 0 && into >= opt_.epoch_s / 2.0) {
+          half_updates = updates_.load();
+          half_time = now;
+        } else if (half_updates >= 0 && into >= opt_.epoch_s) {
+          const double measured = static_cast<double>(updates_.load() - half_updates) / seconds_between(half_time, now);
+          if (!cand) {
+            ann->baseline_tps = measured;
+            ann->history.push_back(HistoryEntry{ann->current, measured, true});
+          } else if (!decide(*ann, *cand, measured)) {
+            apply_knobs(ann->current);
+          }
+          cand = propose(*ann);
+          apply_knobs(*cand);
+          epoch_start = Clock::now();
+          half_updates = -1;
+        }
+      }
+    }
+    if (ann) anneal_history_ = ann->history;
+    request_stop();
+  }
+
+  void join_all() {
+    std::vector<std::thread> ts;
+    {
+      std::lock_guard<std::mutex> lk(workers_m_);
+      for (auto* pool : {&agents_, &predictors_, &trainers_})
+        for (auto& w : *pool)
+          if (w.thread.joinable()) ts.push_back(std::move(w.thread));
+    }
+    for (auto& t : ts) t.join();
+  }
+
+  void shutdown() {
+    request_stop();
+    join_all();
+    frames_.push_back(frame(std::max(1e-9, seconds_between(t0_, Clock::now()))));
+    while (auto left = train_q_.try_pop()) left_queued_ += static_cast<std::int64_t>(left->experiences.size());
+  }
+
+  RunReport make_report() {
+    RunReport r;
+    r.total_updates = updates_.load();
+    r.skipped_updates = skipped_.load();
+    r.total_predictions = pmetrics_.predictions.load();
+    {
+      std::lock_guard<std::mutex> lk(scores_m_);
+      r.total_episodes = static_cast<std::int64_t>(scores_.size());
+      r.episode_scores = scores_;
+    }
+    r.wall_time_s = seconds_between(t0_, Clock::now());
+    r.avg_tps = r.total_updates / r.wall_time_s;
+    r.avg_pps = r.total_predictions / r.wall_time_s;
+    r.experiences_trained = trained_.load();
+    r.avg_samples_per_s = r.experiences_trained / r.wall_time_s;
+    r.mean_lag = r.experiences_trained > 0 ? static_cast<double>(lag_sum_.load()) / r.experiences_trained : 0.0;
+    r.final_knobs = opt_.knobs;
+    r.final_knobs.n_agents = static_cast<int>(n_a_.load());
+    r.final_knobs.n_predictors = static_cast<int>(n_p_.load());
+    r.final_knobs.n_trainers = static_cast<int>(n_t_.load());
+    r.final_rolling_score = rolling_score();
+    r.frames = frames_;
+    r.experiences_produced = produced_.load();
+    r.experiences_dropped = dropped_.load();
+    r.experiences_left_queued = left_queued_;
+    r.anneal_history = anneal_history_;
+    {
+      std::lock_guard<std::mutex> lk(traj_m_);
+      r.theta_trajectory = trajectory_;
+    }
+    r.final_theta = shared_.read_theta();
+    r.final_version = shared_.version();
+    return r;
+  }
+
+  PipelineOptions opt_;
+  std::size_t slot_cap_;
+  SharedModel shared_;
+  BoundedChannel<PredictionRequest> pred_q_;
+  BoundedChannel<ExperienceBatch> train_q_;
+  std::vector<std::unique_ptr<ResponseSlot<PredictionResponse>>> slots_;
+  PredictorMetrics pmetrics_;
+  KnobConfig live_;
+
+  std::mutex workers_m_;
+  std::deque<Worker> agents_, predictors_, trainers_;
+  int next_agent_id_ = 0;
+  std::atomic<std::int64_t> n_a_{0}, n_p_{0}, n_t_{0};
+  std::atomic<bool> stop_requested_{false};
+  std::atomic<std::int64_t> gate_updates_{0};
+  std::atomic<std::int64_t> budget_;
+  std::mutex gate_m_;
+  std::condition_variable gate_cv_;
+
+  std::atomic<std::int64_t> updates_{0}, skipped_{0}, produced_{0}, trained_{0}, dropped_{0};
+  std::atomic<std::uint64_t> lag_sum_{0};
+  std::int64_t last_u_ = 0, last_p_ = 0, last_b_ = 0, last_tr_ = 0;
+  std::mutex scores_m_;
+  std::vector<double> scores_;
+
+  std::mutex traj_m_;
+  std::vector<std::vector<float>> trajectory_;
+  std::function<void(SharedModel&)> traj_sink_;
+
+  std::mutex err_m_;
+  std::exception_ptr first_error_;
+  Clock::time_point t0_;
+  std::vector<MetricsFrame> frames_;
+  std::vector<HistoryEntry> anneal_history_;
+  std::int64_t left_queued_ = 0;
+};
+
+}  // namespace
+
+RunReport run(const PipelineOptions& opt) {
+  validate(opt);
+  Engine e(opt);
+  return e.run_all();
+}
+
+// reference.cpp:25-157: one thread, zero policy lag, same seeds and the same
+// device kernels as the pipeline.
+RunReport train_sync(const PipelineOptions& opt) {
+  PipelineOptions o = opt;
+  o.knobs.n_predictors = 1;
+  o.knobs.n_trainers = 1;
+  o.knobs.min_train_batch = 1;
+  o.sync_after_submit = false;
+  o.anneal = false;
+  if (!o.stop.max_updates) throw std::invalid_argument("train_sync: max_updates must be set");
+  validate(o);
+  const auto t0 = Clock::now();
+  SharedModel model(o.net, o.hyper, o.device, derive_seed(o.seed, {kSeedModelInit}));
+  Ctx ctx(model.handle(), std::max(64, 4 * o.hyper.t_max));
+  struct Slot {
+    std::unique_ptr<Env> env;
+    std::mt19937_64 rng;
+    std::uint64_t episode = 0;
+    Observation obs;
+    double score = 0.0;
+  };
+  const int n_agents = o.knobs.n_agents;
+  std::vector<Slot> agents(n_agents);
+  for (int i = 0; i < n_agents; ++i) {
+    agents[i].env = make_env(o.env);
+    agents[i].rng.seed(derive_seed(o.seed, {kSeedAgentRng, static_cast<std::uint64_t>(i)}));
+    agents[i].obs = agents[i].env->reset(derive_seed(o.seed, {kSeedEnvEpisode, static_cast<std::uint64_t>(i), 0}));
+  }
+  RunReport rep;
+  HostBatch hb, one;
+  std::vector<std::int32_t> acts, off;
+  std::vector<double> rew, boot;
+  std::vector<std::uint8_t> term;
+  const int A = o.net.n_actions;
+  std::vector<float> pi(A);
+  float v = 0.f;
+  int turn = 0;
+  while (rep.total_updates < *o.stop.max_updates) {
+    Slot& a = agents[turn];
+    const int agent_id = turn;
+    turn = (turn + 1) % n_agents;
+    ExperienceBatch batch;
+    batch.agent_id = agent_id;
+    while (true) {
+      const auto snap = model.snapshot();
+      std::uint64_t ver = 0;
+      const bool u8 = !a.obs.u8.empty();
+      const int st = u8 ? ga3c_forward_u8(ctx.c, snap->slot, a.obs.u8.data(), 1, pi.data(), &v, &ver)
+                        : ga3c_forward_f32(ctx.c, snap->slot, a.obs.f32.data(), 1, pi.data(), &v, &ver);
+      check(st, model.handle(), "forward");
+      rep.total_predictions += 1;
+      const int action = o.greedy ? argmax_index(pi.data(), A) : sample_index(pi.data(), A, a.rng);
+      StepResult sr = a.env->step(action);
+      const double reward = o.hyper.clip_rewards ? std::clamp(sr.reward, -1.0, 1.0) : sr.reward;
+      batch.experiences.push_back(Experience{std::move(a.obs), action, reward, v, ver});
+      rep.experiences_produced += 1;
+      a.score += sr.reward;
+      if (sr.terminal) {
+        batch.terminal = true;
+        rep.episode_scores.push_back(a.score);
+        a.score = 0.0;
+        ++a.episode;
+        a.obs = a.env->reset(derive_seed(o.seed, {kSeedEnvEpisode, static_cast<std::uint64_t>(agent_id), a.episode}));
+        break;
+      }
+      a.obs = std::move(sr.observation);
+      if (static_cast<int>(batch.experiences.size()) >= o.hyper.t_max) {
+        batch.bootstrap = v;  // the value just played seeds the tail (G8)
+        break;
+      }
+    }
+    const auto snap = model.snapshot();
+    std::vector<ExperienceBatch> group;
+    group.push_back(std::move(batch));
+    train_on(ctx, snap->slot, group, o.hyper, hb, acts, rew, off, term, boot);
+    if (model.apply(ctx.c)) {
+      rep.total_updates += 1;
+      rep.experiences_trained += static_cast<std::int64_t>(acts.size());
+      if (o.capture_trajectory) rep.theta_trajectory.push_back(model.read_theta());
+    } else {
+      rep.skipped_updates += 1;
+    }
+  }
+  rep.total_episodes = static_cast<std::int64_t>(rep.episode_scores.size());
+  rep.wall_time_s = seconds_between(t0, Clock::now());
+  rep.avg_tps = rep.total_updates / rep.wall_time_s;
+  rep.avg_pps = rep.total_predictions / rep.wall_time_s;
+  rep.avg_samples_per_s = rep.experiences_trained / rep.wall_time_s;
+  rep.final_knobs = o.knobs;
+  if (!rep.episode_scores.empty()) {
+    const std::size_t n = std::min<std::size_t>(30, rep.episode_scores.size());
+    double s = 0.0;
+    for (std::size_t i = rep.episode_scores.size() - n; i < rep.episode_scores.size(); ++i) s += rep.episode_scores[i];
+    rep.final_rolling_score = s / static_cast<double>(n);
+  }
+  rep.final_theta = model.read_theta();
+  rep.final_version = model.version();
+  return rep;
+}
+
+}  // namespace ga3c::host

@@ -10,6 +10,7 @@ parameters travel as fp32 (the device arithmetic type).
 """
 from __future__ import annotations
 
+import ctypes as C
 import math
 from dataclasses import dataclass, field
 from typing import List, Sequence
@@ -264,3 +265,172 @@ def compute_returns(rewards, terminal: bool, bootstrap: float, gamma: float) -> 
     _, ctx = _engine(NetworkSpec(1, [], 2), None, 1)
     out = ctx.compute_returns(r, [0, r.size], [int(bool(terminal))], [float(bootstrap)], gamma)
     return [float(x) for x in out]
+
+
+# ------------------------------------------------------------ host engine
+
+ENV_KINDS = {"bandit": 0, "catch": 1, "delay_lab": 2, "frame_catch": 3, "frames": 4}
+
+
+@dataclass
+class EnvSpec:
+    """envs.hpp EnvSpec + the two pixel environments of the B200 engine."""
+    kind: str = "bandit"
+    n_contexts: int = 4
+    n_actions: int = 4
+    grid_size: int = 5
+    step_delay_us: int = 500
+    episode_len: int = 64
+    action_repeat: int = 1
+
+    def input_hwc(self):
+        if self.kind in ("frame_catch", "frames"):
+            return (84, 84, 4)
+        dim = {"bandit": self.n_contexts, "catch": self.grid_size ** 2 + self.grid_size, "delay_lab": 4}[self.kind]
+        return (1, 1, dim)
+
+    def action_count(self):
+        return {"bandit": self.n_actions, "catch": 3, "delay_lab": 2}.get(self.kind, self.n_actions)
+
+
+def bandit(n_contexts=4, n_actions=4):
+    return EnvSpec("bandit", n_contexts=n_contexts, n_actions=n_actions)
+
+
+def catch_grid(grid_size=5):
+    return EnvSpec("catch", grid_size=grid_size)
+
+
+def delay_lab(step_delay_us=500, episode_len=64):
+    return EnvSpec("delay_lab", step_delay_us=step_delay_us, episode_len=episode_len)
+
+
+def frame_catch(grid_size=7, n_actions=6, step_delay_us=0):
+    return EnvSpec("frame_catch", grid_size=grid_size, n_actions=n_actions, step_delay_us=step_delay_us)
+
+
+def frames(step_delay_us=0, episode_len=64, n_actions=6):
+    return EnvSpec("frames", step_delay_us=step_delay_us, episode_len=episode_len, n_actions=n_actions)
+
+
+def net_for_env(env: EnvSpec, hidden_dims, convs=()):
+    """cli::net_for_env (cli.cpp:161-168): a net whose input/actions fit env."""
+    return NetworkSpec(0, hidden_dims, env.action_count(), in_hwc=env.input_hwc(), convs=convs)
+
+
+@dataclass
+class KnobConfig:
+    n_agents: int = 1
+    n_predictors: int = 2
+    n_trainers: int = 2
+    pred_batch_max: int = 32
+    min_train_batch: int = 1
+    train_queue_cap: int = 32
+    pred_queue_cap: int = 0
+
+
+@dataclass
+class StopCondition:
+    max_updates: int | None = None
+    max_seconds: float | None = None
+    target_score: float | None = None
+
+
+@dataclass
+class PipelineOptions:
+    net: NetworkSpec = None
+    hyper: Hyperparams = field(default_factory=Hyperparams)
+    env: EnvSpec = field(default_factory=EnvSpec)
+    knobs: KnobConfig = field(default_factory=KnobConfig)
+    stop: StopCondition = field(default_factory=StopCondition)
+    seed: int = 1
+    anneal: bool = False
+    anneal_batches: bool = False
+    epoch_s: float = 60.0
+    limits: tuple = (64, 16, 16)
+    metrics_interval_s: float = 1.0
+    greedy: bool = False
+    sync_after_submit: bool = False
+    capture_trajectory: bool = False
+    device: int = 0
+
+
+@dataclass
+class RunReport:
+    total_updates: int
+    skipped_updates: int
+    total_predictions: int
+    total_episodes: int
+    wall_time_s: float
+    avg_tps: float
+    avg_pps: float
+    avg_samples_per_s: float
+    mean_lag: float
+    final_rolling_score: float
+    experiences_produced: int
+    experiences_trained: int
+    experiences_dropped: int
+    experiences_left_queued: int
+    final_knobs: KnobConfig
+    final_version: int
+    final_theta: np.ndarray
+    theta_trajectory: list
+    episode_scores: list
+    anneal_history: list
+    pred_batch_mean: float
+
+
+def _run(opt: PipelineOptions, sync: bool) -> RunReport:
+    o = _abi.PipelineOpts()
+    _abi.lib.ga3c_default_pipeline_opts(o)
+    o.net = opt.net.to_c()
+    o.hyper = opt.hyper.to_c()
+    e = opt.env
+    o.env_kind = ENV_KINDS[e.kind]
+    o.n_contexts, o.env_actions, o.grid_size = e.n_contexts, e.n_actions, e.grid_size
+    o.step_delay_us, o.episode_len, o.action_repeat = e.step_delay_us, e.episode_len, e.action_repeat
+    k = opt.knobs
+    o.n_agents, o.n_predictors, o.n_trainers = k.n_agents, k.n_predictors, k.n_trainers
+    o.pred_batch_max, o.min_train_batch = k.pred_batch_max, k.min_train_batch
+    o.train_queue_cap, o.pred_queue_cap = k.train_queue_cap, k.pred_queue_cap
+    o.max_updates = opt.stop.max_updates or 0
+    o.max_seconds = opt.stop.max_seconds or 0.0
+    o.has_target_score = int(opt.stop.target_score is not None)
+    o.target_score = opt.stop.target_score or 0.0
+    o.seed = opt.seed
+    o.anneal, o.anneal_batches, o.epoch_s = int(opt.anneal), int(opt.anneal_batches), opt.epoch_s
+    o.max_agents, o.max_predictors, o.max_trainers = opt.limits
+    o.metrics_interval_s = opt.metrics_interval_s
+    o.greedy, o.sync_after_submit = int(opt.greedy), int(opt.sync_after_submit)
+    o.capture_trajectory, o.device = int(opt.capture_trajectory), opt.device
+    P = int(_abi.lib.ga3c_param_count(o.net))
+    cap_traj = (opt.stop.max_updates or 0) if opt.capture_trajectory else 0
+    theta = np.zeros(P, np.float32)
+    traj = np.zeros((max(cap_traj, 1), P), np.float32)
+    scores = np.zeros(1 << 16, np.float64)
+    ann = (_abi.AnnealEntry * 256)()
+    err = C.create_string_buffer(512)
+    r = _abi.RunReportC()
+    rc = _abi.lib.ga3c_pipeline_run(o, int(sync), r, _abi.ptr(theta), _abi.ptr(traj) if cap_traj else None,
+                                     cap_traj, _abi.ptr(scores), scores.size, ann, 256, err, 512)
+    _abi.check(rc, err.value.decode())
+    fk = KnobConfig(r.final_n_agents, r.final_n_predictors, r.final_n_trainers, r.final_pred_batch_max,
+                    r.final_min_train_batch, k.train_queue_cap, k.pred_queue_cap)
+    hist = [dict(knobs=KnobConfig(a.n_agents, a.n_predictors, a.n_trainers, a.pred_batch_max, a.min_train_batch),
+                 measured_tps=a.measured_tps, accepted=bool(a.accepted)) for a in ann[:min(r.n_anneal, 256)]]
+    return RunReport(r.total_updates, r.skipped_updates, r.total_predictions, r.total_episodes, r.wall_time_s,
+                     r.avg_tps, r.avg_pps, r.avg_samples_per_s, r.mean_lag, r.final_rolling_score,
+                     r.experiences_produced, r.experiences_trained, r.experiences_dropped,
+                     r.experiences_left_queued, fk, r.final_version, theta,
+                     [traj[i].copy() for i in range(min(r.n_trajectory, cap_traj))],
+                     list(scores[:min(r.total_episodes, scores.size)]), hist, r.last_frame_pred_batch_mean)
+
+
+def run(opt: PipelineOptions) -> RunReport:
+    """pipeline::run (pipeline.hpp:122) on the B200 engine."""
+    return _run(opt, False)
+
+
+def train_sync(opt: PipelineOptions) -> RunReport:
+    """reference::train_sync (reference.hpp:30): zero-lag single-thread trainer."""
+    return _run(opt, True)
