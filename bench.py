@@ -306,12 +306,8 @@ def main():
     torch.cuda.synchronize()
     stream = torch.cuda.ExternalStream(ctx.stream)
 
-    grad_view = None
-    if world > 1:
-        class _View:
-            __cuda_array_interface__ = {"shape": (P,), "typestr": "<f4", "data": (ctx.grad_ptr(), False),
-                                        "version": 3, "strides": None}
-        grad_view = torch.as_tensor(_View(), device=f"cuda:{local}")
+    from paper_1611_06256_b200 import dp
+    grad_view = dp.grad_view(ctx, P, f"cuda:{local}") if world > 1 else None
 
     fstride = T * FRAME_BYTES
     lv = ctx.last_values_ptr()
@@ -324,14 +320,9 @@ def main():
             ctx.sample_dev(uni[s, t].data_ptr(), NA, actions.data_ptr() + 4 * t, stride=T)
         ctx.compute_returns_dev(rewards[s].data_ptr(), offsets.data_ptr(), NA, terminal[s].data_ptr(), lv,
                                 hyper.gamma, rets.data_ptr())
-        for u in range(updates):
-            ctx.loss_grad_dev(fr + u * TB * FRAME_BYTES, True, actions.data_ptr() + 4 * u * TB,
-                              rets.data_ptr() + 8 * u * TB, TB, slot, apply_clip=world == 1)
-            if grad_view is not None:
-                with torch.cuda.stream(stream):
-                    dist.all_reduce(grad_view)
-                ctx.clip_grad()
-            ctx.apply_rmsprop_dev()
+        for u in range(updates):  # data parallel: summed local gradient -> all-reduce -> RMSProp
+            dp.dp_update(ctx, fr + u * TB * FRAME_BYTES, True, actions.data_ptr() + 4 * u * TB,
+                         rets.data_ptr() + 8 * u * TB, TB, slot, grad_view, stream, world)
 
     # ---- warmup + per-kernel breakdown (untimed) ----
     for i in range(args.warmup):
