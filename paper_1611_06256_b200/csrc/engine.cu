@@ -41,6 +41,11 @@ namespace {
 
 constexpr int kNumSMs = 148;
 constexpr std::size_t kPartFloats = std::size_t(32) << 20;  // split-K scratch per ctx (128 MB)
+// The scratch is cut into regions so branches of the backward DAG that run
+// concurrently never share one: 0 = FC forward partials, 1 + li = weight
+// gradient of trunk layer li, kRegions - 1 = heads.
+constexpr int kRegions = GA3C_MAX_CONV + GA3C_MAX_HIDDEN + 2;
+constexpr std::size_t kRegionFloats = kPartFloats / kRegions / 64 * 64;  // 256 B aligned
 constexpr int kMaxActions = 64;
 
 struct Slot {
@@ -72,10 +77,16 @@ struct ga3c_model {
 struct ga3c_ctx {
   ga3c_model* m = nullptr;
   cudaStream_t stream = nullptr;
+  // Kernels go to `cur`: the context stream, or a side stream while an
+  // independent branch of the backward DAG (a weight gradient) is issued.
+  cudaStream_t cur = nullptr;
+  cudaStream_t side[2] = {};
+  cudaEvent_t evs[16] = {};
+  int ev_next = 0;
   int max_batch = 0;
   void* d_in = nullptr;
   float* act[GA3C_MAX_CONV + GA3C_MAX_HIDDEN] = {};
-  float* dx[2] = {};
+  float* dout[GA3C_MAX_CONV + GA3C_MAX_HIDDEN] = {};  // per-layer output gradient (backward DAG)
   float* hin = nullptr;  // f32 copy of a raw input feeding the heads directly
   float* pi32 = nullptr;
   double* pi64 = nullptr;
@@ -90,6 +101,7 @@ struct ga3c_ctx {
   double* d_rets = nullptr;
   float* grad = nullptr;
   int* flag = nullptr;
+  unsigned* ticket = nullptr;  // last-CTA counter of heads_loss_kernel
   unsigned long long* dev_version = nullptr;
   float* part = nullptr;
   double* clip_part = nullptr;
@@ -158,7 +170,7 @@ SplitPlan plan_splits(int M, int N, int K, bool allow_split) {
   if (allow_split) {
     s = std::max(1, (2 * kNumSMs + tiles - 1) / tiles);
     s = std::min(s, std::max(1, K / 128));
-    while (s > 1 && static_cast<std::size_t>(s) * M * N > kPartFloats) --s;
+    while (s > 1 && static_cast<std::size_t>(s) * M * N > kRegionFloats) --s;
   }
   int kc = (K + s - 1) / s;
   kc = ((kc + kBK - 1) / kBK) * kBK;
@@ -166,6 +178,26 @@ SplitPlan plan_splits(int M, int N, int K, bool allow_split) {
   p.k_chunk = kc;
   p.splits = std::max(1, (K + kc - 1) / kc);
   return p;
+}
+
+float* region(ga3c_ctx* c, int r) { return c->part + static_cast<std::size_t>(r) * kRegionFloats; }
+
+// Branches of the backward DAG: fork() makes `s` wait for everything issued
+// on the context stream so far and directs launches to it; join() makes the
+// context stream wait for `s` and directs launches back.  Both are plain
+// event edges, so they are captured into CUDA graphs as graph dependencies.
+void fork_to(ga3c_ctx* c, cudaStream_t s) {
+  cudaEvent_t e = c->evs[c->ev_next++ & 15];
+  cudaEventRecord(e, c->stream);
+  cudaStreamWaitEvent(s, e, 0);
+  c->cur = s;
+}
+
+void join_from(ga3c_ctx* c, cudaStream_t s) {
+  cudaEvent_t e = c->evs[c->ev_next++ & 15];
+  cudaEventRecord(e, s);
+  cudaStreamWaitEvent(c->stream, e, 0);
+  c->cur = c->stream;
 }
 
 // Brackets one launch with CUDA events when (tag, layer) is the probed kernel
@@ -181,12 +213,12 @@ struct Launch {
         cudaEventCreate(&e);
         c->events.push_back(e);
       }
-      cudaEventRecord(c->events[c->ev_used], c->stream);
+      cudaEventRecord(c->events[c->ev_used], c->cur);
     }
   }
   ~Launch() {
     if (on) {
-      cudaEventRecord(c->events[c->ev_used + 1], c->stream);
+      cudaEventRecord(c->events[c->ev_used + 1], c->cur);
       c->ev_used += 2;
     }
     c->launches++;
@@ -198,7 +230,7 @@ void launch_gemm(ga3c_ctx* c, int tag, int layer, const LA& la, const LB& lb, co
                  int N, int K, const SplitPlan& p) {
   dim3 grid((N + kBN - 1) / kBN, (M + kBM - 1) / kBM, p.splits);
   Launch l(c, tag, layer);
-  pdl_launch(c->stream, gemm_simt_kernel<LA, LB, Epi>, dim3(grid), dim3(kThreads), 0, la, lb, epi, M, N, K, p.k_chunk);
+  pdl_launch(c->cur, gemm_simt_kernel<LA, LB, Epi>, dim3(grid), dim3(kThreads), 0, la, lb, epi, M, N, K, p.k_chunk);
 }
 
 // ------------------------------------------------------ tensor-core GEMMs
@@ -215,7 +247,7 @@ void tc_launch(ga3c_ctx* c, int tag, int layer, const Seg& A, const Seg& B, int 
   }
   dim3 grid((M + 127) / 128, splits, (N + BN - 1) / BN);
   Launch l(c, tag, layer);
-  pdl_launch(c->stream, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, A, B, M, N, K, kc, epi);
+  pdl_launch(c->cur, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, A, B, M, N, K, kc, epi);
 }
 
 template <typename TA, typename TB, int MODE>
@@ -327,16 +359,16 @@ int fc_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const vo
       const int tiles = ((L.out + 127) / 128) * ((B + bn - 1) / bn);
       const int chunks = L.in / 32;
       int splits = std::max(1, std::min(chunks, kNumSMs / std::max(1, tiles)));
-      while (splits > 1 && static_cast<std::size_t>(splits) * B * L.out > kPartFloats) --splits;
+      while (splits > 1 && static_cast<std::size_t>(splits) * B * L.out > kRegionFloats) --splits;
       const int kc = ((chunks + splits - 1) / splits) * 32;
       splits = (L.in + kc - 1) / kc;
-      TcEpiArgs e{nullptr, c->part, L.out};
+      TcEpiArgs e{nullptr, region(c, 0), L.out};
       tc_dispatch<float, T, TC_EPI_PART_T>(c, GA3C_K_FC_FWD, li, bn, W, X, L.out, B, L.in, splits, kc, e);
       if (!keep_partials) {
         const std::size_t n = static_cast<std::size_t>(B) * L.out;
         Launch l(c, GA3C_K_SPLITK, li);
-        pdl_launch(c->stream, splitk_bias_relu_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, 
-            c->part, splits, B, L.out, theta + L.b_off, out);
+        pdl_launch(c->cur, splitk_bias_relu_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, 
+            region(c, 0), splits, B, L.out, theta + L.b_off, out);
       }
       return splits;
     }
@@ -345,12 +377,12 @@ int fc_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const vo
   DenseK w{theta + L.w_off, L.in};
   const SplitPlan p = plan_splits(B, L.out, L.in, true);
   if (keep_partials || p.splits > 1) {
-    launch_gemm(c, GA3C_K_FC_FWD, li, a, w, EpiPartial{c->part, B, L.out}, B, L.out, L.in, p);
+    launch_gemm(c, GA3C_K_FC_FWD, li, a, w, EpiPartial{region(c, 0), B, L.out}, B, L.out, L.in, p);
     if (!keep_partials) {
       const std::size_t n = static_cast<std::size_t>(B) * L.out;
       Launch l(c, GA3C_K_SPLITK, li);
-      pdl_launch(c->stream, splitk_bias_relu_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, 
-          c->part, p.splits, B, L.out, theta + L.b_off, out);
+      pdl_launch(c->cur, splitk_bias_relu_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, 
+          region(c, 0), p.splits, B, L.out, theta + L.b_off, out);
     }
   } else {
     launch_gemm(c, GA3C_K_FC_FWD, li, a, w, EpiBiasRelu{out, theta + L.b_off, L.out}, B, L.out, L.in, p);
@@ -358,25 +390,25 @@ int fc_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const vo
   return p.splits;
 }
 
-void launch_splitk_grad(ga3c_ctx* c, int li, int splits, int M, int N, const GradMap& gm) {
+void launch_splitk_grad(ga3c_ctx* c, int li, int splits, int M, int N, const GradMap& gm, float* part) {
   const std::size_t n = static_cast<std::size_t>(M) * N;
   Launch l(c, GA3C_K_SPLITK, li);
   if (splits > 16)
-    pdl_launch(c->stream, splitk_grad8_kernel, dim3((unsigned)((n + 31) / 32)), dim3(256), 0, c->part, splits, M, N, gm);
+    pdl_launch(c->cur, splitk_grad8_kernel, dim3((unsigned)((n + 31) / 32)), dim3(256), 0, part, splits, M, N, gm);
   else
-    pdl_launch(c->stream, splitk_grad_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, c->part, splits, M, N, gm);
+    pdl_launch(c->cur, splitk_grad_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, part, splits, M, N, gm);
 }
 
 // Weight-gradient GEMM [M rows][N = Kw+1] (+ reduction) into dtheta.
 template <class LA, class LB>
 void wgrad_gemm(ga3c_ctx* c, int li, const LA& la, const LB& lb, const GradMap& gm, int M, int N,
-                int K) {
+                int K, float* part) {
   const SplitPlan p = plan_splits(M, N, K, true);
   if (p.splits == 1) {
     launch_gemm(c, GA3C_K_WGRAD, li, la, lb, EpiGrad{gm}, M, N, K, p);
   } else {
-    launch_gemm(c, GA3C_K_WGRAD, li, la, lb, EpiPartial{c->part, M, N}, M, N, K, p);
-    launch_splitk_grad(c, li, p.splits, M, N, gm);
+    launch_gemm(c, GA3C_K_WGRAD, li, la, lb, EpiPartial{part, M, N}, M, N, K, p);
+    launch_splitk_grad(c, li, p.splits, M, N, gm, part);
   }
 }
 
@@ -390,13 +422,13 @@ void wgrad_tc_launch(ga3c_ctx* c, int li, const WgradArgs& a, dim3 grid, int tag
     attr_set = true;
   }
   Launch l(c, tag, li);
-  pdl_launch(c->stream, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, a);
+  pdl_launch(c->cur, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, a);
 }
 
 // Tensor-core weight gradient; returns false when the shape needs the SIMT path.
 template <typename TX>
 bool layer_wgrad_tc(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const float* dout, int B,
-                    long long in_stride, const GradMap& gm) {
+                    long long in_stride, const GradMap& gm, float* part) {
   const int npix = B * L.pixels();
   Seg X = L.is_conv ? conv_seg<TX>(L, x_in, in_stride)
                     : dense_seg(x_in, B, in_stride > 0 ? in_stride : L.in, L.in, sizeof(TX) == 1);
@@ -409,10 +441,10 @@ bool layer_wgrad_tc(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const
   const int ntiles = (L.out + bn - 1) / bn;
   const int chunks = (npix + 31) / 32;
   int splits = std::max(1, std::min(chunks / 2, (kNumSMs + mtiles * ntiles - 1) / (mtiles * ntiles)));
-  while (splits > 1 && static_cast<std::size_t>(splits) * L.out * (L.in + 1) > kPartFloats) --splits;
+  while (splits > 1 && static_cast<std::size_t>(splits) * L.out * (L.in + 1) > kRegionFloats) --splits;
   const int kc = ((chunks + splits - 1) / splits) * 32;
   splits = (npix + kc - 1) / kc;
-  WgradArgs a{X, dout, L.out, L.out, L.in, npix, kc, c->part, gm, splits == 1, 0, nullptr, nullptr, 0};
+  WgradArgs a{X, dout, L.out, L.out, L.in, npix, kc, part, gm, splits == 1, 0, nullptr, nullptr, 0};
   dim3 grid(mtiles, splits, ntiles);
   switch (bn) {
     case 32: wgrad_tc_launch<TX, 32>(c, li, a, grid); break;
@@ -423,10 +455,10 @@ bool layer_wgrad_tc(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const
     const std::size_t n = static_cast<std::size_t>(L.out) * (L.in + 1);
     Launch l(c, GA3C_K_SPLITK, li);
     if (splits > 16)
-      pdl_launch(c->stream, splitk_wgrad8_kernel, dim3((unsigned)((n + 31) / 32)), dim3(256), 0, c->part,
+      pdl_launch(c->cur, splitk_wgrad8_kernel, dim3((unsigned)((n + 31) / 32)), dim3(256), 0, part,
                  splits, L.out, L.in, gm);
     else
-      pdl_launch(c->stream, splitk_wgrad_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, c->part,
+      pdl_launch(c->cur, splitk_wgrad_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, part,
                  splits, L.out, L.in, gm);
   }
   return true;
@@ -436,18 +468,19 @@ template <typename T>
 void layer_wgrad(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const float* dout, int B,
                  long long in_stride) {
   GradMap gm{c->grad, c->flag, L.w_off, L.b_off, 0, 0, L.out, L.in};
-  if (layer_wgrad_tc<T>(c, li, L, x_in, dout, B, in_stride, gm)) return;
+  float* part = region(c, 1 + li);
+  if (layer_wgrad_tc<T>(c, li, L, x_in, dout, B, in_stride, gm, part)) return;
   DenseT a{dout, L.out};  // (m = out channel, k = row) -> dout[row][m]
   if (L.is_conv) {
     WithOnes<Im2colB<T>> b;
     static_cast<Im2col<T>&>(b.l) = im2col_of<T>(L, x_in, in_stride);
     b.n_real = L.in;
-    wgrad_gemm(c, li, a, b, gm, L.out, L.in + 1, B * L.pixels());
+    wgrad_gemm(c, li, a, b, gm, L.out, L.in + 1, B * L.pixels(), part);
   } else {
     WithOnes<DenseTIn<T>> b{
         DenseTIn<T>{static_cast<const T*>(x_in), in_stride > 0 ? static_cast<int>(in_stride) : L.in},
         L.in};
-    wgrad_gemm(c, li, a, b, gm, L.out, L.in + 1, B);
+    wgrad_gemm(c, li, a, b, gm, L.out, L.in + 1, B, part);
   }
 }
 
@@ -475,7 +508,20 @@ bool fc_dgrad_tc(ga3c_ctx* c, int li, const Layer& L, const float* theta, const 
 void layer_dgrad(ga3c_ctx* c, int li, const Layer& L, const float* theta, const float* dout,
                  const float* gate, float* din, int B, const float* doutT = nullptr) {
   if (!L.is_conv && doutT && fc_dgrad_tc(c, li, L, theta, doutT, c->ldT, gate, din, B)) return;
-  if (L.is_conv && L.cin % 16 == 0 && L.cout % 4 == 0 && L.w_off % 4 == 0 &&
+  if (L.is_conv && L.cin % 16 == 0 && L.w_off % 4 == 0 && L.k == 4 && L.stride == 2 &&
+      (L.cout == 32 || L.cout == 64)) {
+    const int npix = B * L.ih * L.iw;
+    const std::size_t smem = static_cast<std::size_t>(L.cout) * L.k * L.k * 16 * sizeof(float);
+    auto kern = L.cout == 32 ? conv_dgrad_32x4s2_kernel : conv_dgrad_64x4s2_kernel;
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[L.cout == 64]) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr_set[L.cout == 64] = true;
+    }
+    Launch l(c, GA3C_K_DGRAD, li);
+    pdl_launch(c->cur, kern, dim3((npix + 63) / 64, L.cin / 16), dim3(256), smem, dout, theta + L.w_off,
+               gate, din, B, L.ih, L.iw, L.cin, L.oh, L.ow);
+  } else if (L.is_conv && L.cin % 16 == 0 && L.cout % 4 == 0 && L.w_off % 4 == 0 &&
       static_cast<std::size_t>(L.cout) * L.k * L.k * 16 * sizeof(float) <= 200 * 1024) {
     const int npix = B * L.ih * L.iw;
     const std::size_t smem = static_cast<std::size_t>(L.cout) * L.k * L.k * 16 * sizeof(float);
@@ -485,12 +531,12 @@ void layer_dgrad(ga3c_ctx* c, int li, const Layer& L, const float* theta, const 
       attr_set = true;
     }
     Launch l(c, GA3C_K_DGRAD, li);
-    pdl_launch(c->stream, conv_dgrad16_kernel, dim3(dim3((npix + 63) / 64, L.cin / 16)), dim3(256), smem, 
+    pdl_launch(c->cur, conv_dgrad16_kernel, dim3(dim3((npix + 63) / 64, L.cin / 16)), dim3(256), smem, 
         dout, theta + L.w_off, gate, din, B, L.ih, L.iw, L.cin, L.oh, L.ow, L.cout, L.k, L.stride);
   } else if (L.is_conv) {
     const std::size_t n = static_cast<std::size_t>(B) * L.ih * L.iw * L.cin;
     Launch l(c, GA3C_K_DGRAD, li);
-    pdl_launch(c->stream, conv_dgrad_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, 
+    pdl_launch(c->cur, conv_dgrad_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, 
         dout, theta + L.w_off, gate, din, B, L.ih, L.iw, L.cin, L.oh, L.ow, L.cout, L.k, L.stride);
   } else {
     DenseK a{dout, L.out};
@@ -508,8 +554,20 @@ __global__ void widen_u8_kernel(const uint8_t* __restrict__ x, float* __restrict
   if (i < n) y[i] = static_cast<float>(x[i]) * (1.0f / 256.0f);
 }
 
+// What the heads consume: the last FC layer's split-K partials (+ its bias),
+// or a finished h.
+struct HeadsIn {
+  const float* part = nullptr;
+  int n_split = 0;
+  const float* fc_bias = nullptr;
+  float* h = nullptr;
+};
+
+// Trunk forward; then the predictor heads (softmax) unless `hin` is given,
+// in which case the heads' inputs are returned for the trainer's fused
+// heads + loss kernel.
 int run_forward(ga3c_ctx* c, const float* theta, const void* d_in, bool u8, int B,
-                long long in_stride = 0) {
+                long long in_stride = 0, HeadsIn* hin = nullptr) {
   const Layout& lo = c->m->lo;
   const void* x = d_in;
   bool x_u8 = u8;
@@ -541,7 +599,7 @@ int run_forward(ga3c_ctx* c, const float* theta, const void* d_in, bool u8, int 
       // raw u8 input feeds the heads directly: widen once (k/256 is exact)
       const std::size_t n = static_cast<std::size_t>(B) * D;
       Launch l(c, GA3C_K_OTHER, -1);
-      pdl_launch(c->stream, widen_u8_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, 
+      pdl_launch(c->cur, widen_u8_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, 
           static_cast<const uint8_t*>(d_in), c->hin, n);
       h = c->hin;
     } else {
@@ -550,14 +608,21 @@ int run_forward(ga3c_ctx* c, const float* theta, const void* d_in, bool u8, int 
   } else {
     h = c->act[lo.n_trunk - 1];
     if (!lo.trunk[lo.n_trunk - 1].is_conv) {
-      part = c->part;
+      part = region(c, 0);
       fc_bias = theta + lo.trunk[lo.n_trunk - 1].b_off;
     }
+  }
+  if (hin) {
+    hin->part = part;
+    hin->n_split = n_split;
+    hin->fc_bias = fc_bias;
+    hin->h = h;
+    return GA3C_OK;
   }
   const std::size_t smem = (static_cast<std::size_t>(D) + 8 * (A + 1)) * sizeof(float);
   {
     Launch l(c, GA3C_K_HEADS, -1);
-    pdl_launch(c->stream, heads_forward_kernel, dim3(B), dim3(256), smem, part, n_split, fc_bias, h, B, D, theta,
+    pdl_launch(c->cur, heads_forward_kernel, dim3(B), dim3(256), smem, part, n_split, fc_bias, h, B, D, theta,
                                                       lo.policy.w_off, lo.policy.b_off, lo.value.w_off,
                                                       lo.value.b_off, A, c->pi32, c->pi64, c->v, c->v64);
   }
@@ -570,51 +635,63 @@ int run_loss_grad(ga3c_ctx* c, const float* theta, const void* d_in, bool u8, co
   const Layout& lo = m->lo;
   const int D = lo.head_in();
   const int A = lo.n_actions;
-  run_forward(c, theta, d_in, u8, B, in_stride);
-  const float* h = lo.n_trunk ? c->act[lo.n_trunk - 1]
-                              : (u8 ? c->hin : static_cast<const float*>(d_in));
-  float* dh = lo.n_trunk ? c->dx[0] : nullptr;
+  HeadsIn hi;
+  run_forward(c, theta, d_in, u8, B, in_stride, &hi);
+  const float* h = hi.h;
+  float* dh = lo.n_trunk ? c->dout[lo.n_trunk - 1] : nullptr;
   {
+    const std::size_t smem = (static_cast<std::size_t>(D) + 8 * (A + 1)) * sizeof(float);
     Launch l(c, GA3C_K_LOSS_BWD, -1);
-    pdl_launch(c->stream, loss_heads_bwd_kernel, dim3(B), dim3(lo.n_trunk ? 256 : 32), 0, 
-        c->pi64, c->v, d_act, d_rets, h, B, lo.n_trunk ? D : 0, A, theta, lo.policy.w_off,
-        lo.value.w_off, m->hp.beta, m->hp.eps_log, m->hp.value_loss_weight, c->dhead, dh,
-        lo.n_trunk ? c->dhT : nullptr, c->ldT, c->scal, c->flag);
+    pdl_launch(c->cur, heads_loss_kernel, dim3(B), dim3(256), smem, hi.part, hi.n_split, hi.fc_bias, hi.h, B, D,
+               theta, lo.policy.w_off, lo.policy.b_off, lo.value.w_off, lo.value.b_off, A, d_act, d_rets,
+               m->hp.beta, m->hp.eps_log, m->hp.value_loss_weight, c->pi64, c->v, c->dhead, dh,
+               lo.n_trunk ? c->dhT : nullptr, c->ldT, c->scal, c->scal_sum, c->ticket, c->flag);
   }
-  // heads weight gradient: [A+1][D+1] = dhead^T [h | 1]
+  // Backward DAG.  The critical path is the input-gradient chain
+  // (loss -> dgrad L-1 -> ... -> dgrad 1 -> wgrad 0); the heads' and the
+  // upper layers' weight gradients only need their layer's output gradient,
+  // so they run on side streams as soon as it exists.  Every branch writes
+  // disjoint dtheta ranges and its own split-K region, so the result is the
+  // same bit for bit as the serial order.
+  fork_to(c, c->side[0]);
   {
+    // heads weight gradient: [A+1][D+1] = dhead^T [h | 1]
     GradMap gm{c->grad, c->flag, lo.policy.w_off, lo.policy.b_off, lo.value.w_off, lo.value.b_off, A, D};
     DenseT a{c->dhead, A + 1};
     WithOnes<DenseT> b{DenseT{h, D}, D};
-    wgrad_gemm(c, -1, a, b, gm, A + 1, D + 1, B);
+    wgrad_gemm(c, -1, a, b, gm, A + 1, D + 1, B, region(c, kRegions - 1));
   }
-  int cur = 0;
+  c->cur = c->stream;
+  bool used[2] = {true, false};
   for (int li = lo.n_trunk - 1; li >= 0; --li) {
     const Layer& L = lo.trunk[li];
     const void* x_in = li == 0 ? d_in : c->act[li - 1];
     const bool in_u8 = li == 0 && u8;
     const long long st = li == 0 ? in_stride : 0;
+    if (li > 0) {
+      const int sd = li & 1;
+      fork_to(c, c->side[sd]);
+      used[sd] = true;
+    }
     if (in_u8)
-      layer_wgrad<uint8_t>(c, li, L, x_in, c->dx[cur], B, st);
+      layer_wgrad<uint8_t>(c, li, L, x_in, c->dout[li], B, st);
     else
-      layer_wgrad<float>(c, li, L, x_in, c->dx[cur], B, st);
+      layer_wgrad<float>(c, li, L, x_in, c->dout[li], B, st);
+    c->cur = c->stream;
     if (li > 0) {
       const float* doutT = li == lo.n_trunk - 1 ? c->dhT : nullptr;
-      layer_dgrad(c, li, L, theta, c->dx[cur], c->act[li - 1], c->dx[cur ^ 1], B, doutT);
-      cur ^= 1;
+      layer_dgrad(c, li, L, theta, c->dout[li], c->act[li - 1], c->dout[li - 1], B, doutT);
     }
   }
-  {
-    Launch l(c, GA3C_K_OTHER, -1);
-    pdl_launch(c->stream, scalars_kernel, dim3(1), dim3(32), 0, c->scal, B, c->scal_sum);
-  }
+  for (int sd = 0; sd < 2; ++sd)
+    if (used[sd]) join_from(c, c->side[sd]);
   if (apply_clip && m->hp.grad_clip_norm > 0.0) {
     {
       Launch l(c, GA3C_K_OTHER, -1);
-      pdl_launch(c->stream, sumsq_kernel, dim3(kNumSMs), dim3(256), 0, c->grad, lo.total, c->clip_part);
+      pdl_launch(c->cur, sumsq_kernel, dim3(kNumSMs), dim3(256), 0, c->grad, lo.total, c->clip_part);
     }
     Launch l(c, GA3C_K_OTHER, -1);
-    pdl_launch(c->stream, clip_scale_kernel, dim3(kNumSMs), dim3(256), 0, c->grad, lo.total, c->clip_part, kNumSMs,
+    pdl_launch(c->cur, clip_scale_kernel, dim3(kNumSMs), dim3(256), 0, c->grad, lo.total, c->clip_part, kNumSMs,
                                                       m->hp.grad_clip_norm);
   }
   return GA3C_OK;
@@ -629,7 +706,7 @@ void launch_rmsprop(ga3c_ctx* c, const Slot& src, const Slot& dst, unsigned long
   unsigned blocks = (unsigned)std::min<std::size_t>((n4 + 255) / 256, 8 * kNumSMs);
   if (blocks == 0) blocks = 1;
   Launch l(c, GA3C_K_RMSPROP, -1);
-  pdl_launch(c->stream, rmsprop_kernel, dim3(blocks), dim3(256), 0, src.theta, src.g, c->grad, dst.theta, dst.g, n,
+  pdl_launch(c->cur, rmsprop_kernel, dim3(blocks), dim3(256), 0, src.theta, src.g, c->grad, dst.theta, dst.g, n,
                                                 c->flag, ver, alpha, oma, static_cast<float>(hp.eta),
                                                 static_cast<float>(hp.eps_rms));
 }
@@ -861,14 +938,18 @@ ga3c_ctx* ga3c_ctx_create(ga3c_model* m, int max_batch, int* status) {
   const Layout& lo = m->lo;
   const std::size_t B = max_batch;
   bool ok = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) == cudaSuccess;
+  c->cur = c->stream;
+  for (auto& sd : c->side)
+    if (ok) ok = cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking) == cudaSuccess;
+  for (auto& e : c->evs)
+    if (ok) ok = cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
   auto alloc = [&](auto** p, std::size_t bytes) {
     if (!ok) return;
     ok = cudaMalloc(reinterpret_cast<void**>(p), std::max<std::size_t>(bytes, 16)) == cudaSuccess;
   };
   alloc(&c->d_in, B * lo.in_dim * sizeof(float));
   for (int i = 0; i < lo.n_trunk; ++i) alloc(&c->act[i], B * lo.trunk[i].out_dim() * sizeof(float));
-  alloc(&c->dx[0], B * lo.max_act_dim() * sizeof(float));
-  alloc(&c->dx[1], B * lo.max_act_dim() * sizeof(float));
+  for (int i = 0; i < lo.n_trunk; ++i) alloc(&c->dout[i], B * lo.trunk[i].out_dim() * sizeof(float));
   if (lo.n_trunk == 0) alloc(&c->hin, B * lo.in_dim * sizeof(float));
   alloc(&c->pi32, B * lo.n_actions * sizeof(float));
   alloc(&c->pi64, B * lo.n_actions * sizeof(double));
@@ -884,16 +965,20 @@ ga3c_ctx* ga3c_ctx_create(ga3c_model* m, int max_batch, int* status) {
   alloc(&c->d_rets, B * sizeof(double));
   alloc(&c->grad, lo.total * sizeof(float));
   alloc(&c->flag, sizeof(int));
+  alloc(&c->ticket, sizeof(unsigned));
   alloc(&c->dev_version, sizeof(unsigned long long));
   alloc(&c->part, kPartFloats * sizeof(float));
   alloc(&c->clip_part, kNumSMs * sizeof(double));
   if (ok) ok = cudaMallocHost(&c->h_flag, sizeof(int)) == cudaSuccess;
   if (ok) ok = cudaMemset(c->dev_version, 0, sizeof(unsigned long long)) == cudaSuccess;
   if (ok) ok = cudaMemset(c->flag, 0, sizeof(int)) == cudaSuccess;
+  if (ok) ok = cudaMemset(c->ticket, 0, sizeof(unsigned)) == cudaSuccess;
   if (ok) {
     const int max_smem = 200 * 1024;
     ok = cudaFuncSetAttribute(heads_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              max_smem) == cudaSuccess;
+                              max_smem) == cudaSuccess &&
+         cudaFuncSetAttribute(heads_loss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem) ==
+             cudaSuccess;
   }
   if (!ok) {
     g_tls_error = "ga3c_ctx_create: device allocation failed";
@@ -909,13 +994,22 @@ void ga3c_ctx_destroy(ga3c_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->m->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  void* ps[] = {c->d_in, c->dx[0], c->dx[1], c->hin, c->pi32, c->pi64, c->v, c->v64, c->dhead, c->dhT, c->scal,
-                c->scal_sum, c->d_actions, c->d_rets, c->grad, c->flag, c->dev_version, c->part,
+  void* ps[] = {c->d_in, c->hin, c->pi32, c->pi64, c->v, c->v64, c->dhead, c->dhT, c->scal,
+                c->scal_sum, c->d_actions, c->d_rets, c->grad, c->flag, c->ticket, c->dev_version, c->part,
                 c->clip_part, c->r_rew, c->r_off, c->r_term, c->r_boot, c->r_out};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (auto* a : c->act)
     if (a) cudaFree(a);
+  for (auto* a : c->dout)
+    if (a) cudaFree(a);
+  for (auto sd : c->side)
+    if (sd) {
+      cudaStreamSynchronize(sd);
+      cudaStreamDestroy(sd);
+    }
+  for (auto e : c->evs)
+    if (e) cudaEventDestroy(e);
   if (c->h_flag) cudaFreeHost(c->h_flag);
   for (auto e : c->events) cudaEventDestroy(e);
   for (auto g : c->graphs) cudaGraphExecDestroy(g);
@@ -1097,10 +1191,10 @@ int ga3c_clip_grad(ga3c_ctx* c) {
   if (m->hp.grad_clip_norm > 0.0) {
     {
       Launch l(c, GA3C_K_OTHER, -1);
-      pdl_launch(c->stream, sumsq_kernel, dim3(kNumSMs), dim3(256), 0, c->grad, m->lo.total, c->clip_part);
+      pdl_launch(c->cur, sumsq_kernel, dim3(kNumSMs), dim3(256), 0, c->grad, m->lo.total, c->clip_part);
     }
     Launch l(c, GA3C_K_OTHER, -1);
-    pdl_launch(c->stream, clip_scale_kernel, dim3(kNumSMs), dim3(256), 0, c->grad, m->lo.total, c->clip_part, kNumSMs,
+    pdl_launch(c->cur, clip_scale_kernel, dim3(kNumSMs), dim3(256), 0, c->grad, m->lo.total, c->clip_part, kNumSMs,
                                                       m->hp.grad_clip_norm);
   }
   GA3C_CUDA(cudaGetLastError());
@@ -1138,7 +1232,7 @@ int ga3c_apply_rmsprop(ga3c_ctx* c, const float* dtheta, int* applied, uint64_t*
       return GA3C_CUDA_ERROR;
     }
     Launch l(c, GA3C_K_OTHER, -1);
-    pdl_launch(c->stream, check_finite_kernel, dim3(kNumSMs), dim3(256), 0, c->grad, n, c->flag);
+    pdl_launch(c->cur, check_finite_kernel, dim3(kNumSMs), dim3(256), 0, c->grad, n, c->flag);
   }
   launch_rmsprop(c, m->slots[src], m->slots[dst], nullptr);
   cudaMemcpyAsync(c->h_flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
@@ -1195,7 +1289,7 @@ int ga3c_compute_returns_dev(ga3c_ctx* c, const double* d_rewards, const int32_t
   auto set_err = [&](const std::string& e) { m->set_error(e); };
   {
     Launch l(c, GA3C_K_RETURNS, -1);
-    pdl_launch(c->stream, returns_kernel, dim3((n_seg + 127) / 128), dim3(128), 0, d_rewards, d_off, n_seg, d_terminal,
+    pdl_launch(c->cur, returns_kernel, dim3((n_seg + 127) / 128), dim3(128), 0, d_rewards, d_off, n_seg, d_terminal,
                                                                d_bootstrap, gamma, d_out);
   }
   GA3C_CUDA(cudaGetLastError());
@@ -1257,7 +1351,7 @@ int ga3c_sample_actions_dev(ga3c_ctx* c, const float* d_pi, const double* d_u, i
   const double* pi64 = (d_pi == nullptr || d_pi == c->pi32) ? c->pi64 : nullptr;
   {
     Launch l(c, GA3C_K_SAMPLE, -1);
-    pdl_launch(c->stream, sample_kernel, dim3((B + 127) / 128), dim3(128), 0, d_pi, pi64, d_u, B, A, d_actions,
+    pdl_launch(c->cur, sample_kernel, dim3((B + 127) / 128), dim3(128), 0, d_pi, pi64, d_u, B, A, d_actions,
                                                           action_stride);
   }
   GA3C_CUDA(cudaGetLastError());
@@ -1380,7 +1474,7 @@ static int loss_grad_segments(ga3c_ctx* c, int slot, const void* states, bool u8
   if (!rc) {
     {
       Launch l(c, GA3C_K_RETURNS, -1);
-      pdl_launch(c->stream, returns_kernel, dim3((n_seg + 127) / 128), dim3(128), 0, c->r_rew,
+      pdl_launch(c->cur, returns_kernel, dim3((n_seg + 127) / 128), dim3(128), 0, c->r_rew,
                  (const int32_t*)c->r_off, n_seg, (const uint8_t*)c->r_term, (const double*)c->r_boot, gamma,
                  c->d_rets);
     }

@@ -26,6 +26,8 @@ namespace ga3c {
 
 namespace {
 
+constexpr int kMaxA = 64;  // n_actions limit (validated by the engine)
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -41,39 +43,35 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 }  // namespace
 
 // ------------------------------------------------------------------ heads
-// One CTA per sample.  h = ReLU(sum_s part[s][b][:] + bias) when the last
-// trunk layer is an FC whose split-K partials are handed over (part != null),
-// else h is read from h_in.  Then logits/value in fp32 (fixed-order block
-// reduction) and the softmax in fp64: pi64 (internal, for the loss and the
-// sampler) and pi32 (API output).
-__global__ void __launch_bounds__(256)
-heads_forward_kernel(const float* __restrict__ part, int n_split, const float* __restrict__ fc_bias,
-                     float* __restrict__ h_io, int B, int D, const float* __restrict__ theta,
-                     std::size_t wp_off, std::size_t bp_off, std::size_t wv_off, std::size_t bv_off,
-                     int A, float* __restrict__ pi32, double* __restrict__ pi64,
-                     float* __restrict__ v_out, double* __restrict__ v64_out) {
-  pdl_enter();
-  extern __shared__ float sm[];
-  float* h = sm;                // D
-  float* red = sm + D;          // [8 warps][A+1]
-  const int b = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// Shared pieces of the two heads kernels (one CTA per sample):
+//   heads_h       h = ReLU(sum_s part[s][b][:] + bias) when the last trunk
+//                 layer is an FC whose split-K partials are handed over
+//                 (part != null; eight interleaved chains combined in a fixed
+//                 order: independent loads in flight, reproducible result),
+//                 else h is read from h_in;
+//   heads_logits  logits / value in fp32 (fixed-order block reduction);
+//   softmax       max-subtracted softmax in fp64, one lane per action for
+//                 exp(), the normaliser summed in action order (nnet.cpp:110-117).
+__device__ __forceinline__ void heads_h(const float* __restrict__ part, int n_split,
+                                        const float* __restrict__ fc_bias, float* __restrict__ h_io, int B,
+                                        int D, int b, float* h) {
   float* hrow = h_io + static_cast<std::size_t>(b) * D;
-  for (int o = tid; o < D; o += blockDim.x) {
+  for (int o = threadIdx.x; o < D; o += blockDim.x) {
     float v;
     if (part) {
-      // 4 interleaved chains (splits k, k+4, ...) combined in a fixed order:
-      // independent loads in flight, reproducible result
-      float c[4] = {0.f, 0.f, 0.f, 0.f};
+      float c[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       const std::size_t stride = static_cast<std::size_t>(B) * D;
       const float* pp = part + static_cast<std::size_t>(b) * D + o;
       int k = 0;
-      for (; k + 4 <= n_split; k += 4) {
+      for (; k + 8 <= n_split; k += 8) {
+        float t[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) c[u] += pp[(k + u) * stride];
+        for (int u = 0; u < 8; ++u) t[u] = pp[(k + u) * stride];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c[u] += t[u];
       }
       for (int u = 0; k < n_split; ++k, ++u) c[u] += pp[k * stride];
-      const float s = (c[0] + c[1]) + (c[2] + c[3]);
+      const float s = ((c[0] + c[1]) + (c[2] + c[3])) + ((c[4] + c[5]) + (c[6] + c[7]));
       v = s + fc_bias[o];
       v = v < 0.0f ? 0.0f : v;
       hrow[o] = v;
@@ -82,7 +80,15 @@ heads_forward_kernel(const float* __restrict__ part, int n_split, const float* _
     }
     h[o] = v;
   }
-  __syncthreads();
+}
+
+// Returns (in warp 0, all lanes) nothing; writes logit_sh[0..A) (as double)
+// and *val_sh = value.  Must be called by the whole CTA.
+__device__ __forceinline__ void heads_logits(const float* __restrict__ theta, std::size_t wp_off,
+                                             std::size_t bp_off, std::size_t wv_off, std::size_t bv_off,
+                                             int A, int D, const float* h, float* red, double* logit_sh,
+                                             float* val_sh) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int j = 0; j <= A; ++j) {
     const float* w = theta + (j < A ? wp_off + static_cast<std::size_t>(j) * D : wv_off);
     float s = 0.0f;
@@ -92,9 +98,6 @@ heads_forward_kernel(const float* __restrict__ part, int n_split, const float* _
   }
   __syncthreads();
   if (warp == 0) {
-    // lanes j < A+1 finish the dot products in warp order, then lane 0 does
-    // the softmax in fp64 (A is small).
-    __shared__ double logit_sh[64];
     for (int j = lane; j <= A; j += 32) {
       float s = 0.0f;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w * (A + 1) + j];
@@ -102,85 +105,155 @@ heads_forward_kernel(const float* __restrict__ part, int n_split, const float* _
       const float z = s + bias;
       if (j < A)
         logit_sh[j] = z;
-      else {
-        v_out[b] = z;
-        v64_out[b] = z;
-      }
+      else
+        *val_sh = z;
     }
+  }
+  __syncthreads();
+}
+
+// p[0..A) = softmax(logit_sh) in fp64; whole CTA calls, warp 0 computes.
+__device__ __forceinline__ void softmax64(const double* logit_sh, int A, double* e_sh, double* p_sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    double m = logit_sh[0];
+    for (int j = 1; j < A; ++j)
+      if (m < logit_sh[j]) m = logit_sh[j];
+    for (int j = lane; j < A; j += 32) e_sh[j] = exp(logit_sh[j] - m);
     __syncwarp();
     if (lane == 0) {
-      double m = logit_sh[0];
-      for (int j = 1; j < A; ++j)
-        if (m < logit_sh[j]) m = logit_sh[j];
       double z = 0.0;
-      double e[64];
-      for (int j = 0; j < A; ++j) {
-        e[j] = exp(logit_sh[j] - m);
-        z += e[j];
-      }
-      for (int j = 0; j < A; ++j) {
-        const double p = e[j] / z;
-        pi64[static_cast<std::size_t>(b) * A + j] = p;
-        pi32[static_cast<std::size_t>(b) * A + j] = static_cast<float>(p);
-      }
+      for (int j = 0; j < A; ++j) z += e_sh[j];
+      e_sh[A] = z;
     }
+    __syncwarp();
+    const double z = e_sh[A];
+    for (int j = lane; j < A; j += 32) p_sh[j] = e_sh[j] / z;
+  }
+  __syncthreads();
+}
+
+// Predictor forward: FC finalize + heads + softmax.  pi64 (internal, for the
+// sampler) and pi32 (API output), V in fp32 and fp64.
+__global__ void __launch_bounds__(256)
+heads_forward_kernel(const float* __restrict__ part, int n_split, const float* __restrict__ fc_bias,
+                     float* __restrict__ h_io, int B, int D, const float* __restrict__ theta,
+                     std::size_t wp_off, std::size_t bp_off, std::size_t wv_off, std::size_t bv_off,
+                     int A, float* __restrict__ pi32, double* __restrict__ pi64,
+                     float* __restrict__ v_out, double* __restrict__ v64_out) {
+  pdl_enter();
+  extern __shared__ float sm[];
+  float* h = sm;        // D
+  float* red = sm + D;  // [8 warps][A+1]
+  __shared__ double logit_sh[kMaxA], e_sh[kMaxA + 1], p_sh[kMaxA];
+  __shared__ float val_sh;
+  const int b = blockIdx.x;
+  heads_h(part, n_split, fc_bias, h_io, B, D, b, h);
+  __syncthreads();
+  heads_logits(theta, wp_off, bp_off, wv_off, bv_off, A, D, h, red, logit_sh, &val_sh);
+  softmax64(logit_sh, A, e_sh, p_sh);
+  for (int j = threadIdx.x; j < A; j += blockDim.x) {
+    pi64[static_cast<std::size_t>(b) * A + j] = p_sh[j];
+    pi32[static_cast<std::size_t>(b) * A + j] = static_cast<float>(p_sh[j]);
+  }
+  if (threadIdx.x == 0) {
+    v_out[b] = val_sh;
+    v64_out[b] = val_sh;
   }
 }
 
-// -------------------------------------------------------- loss + heads bwd
-// One CTA per sample.  fp64 loss algebra (nnet.cpp:231-254) from pi64 and V,
-// then dh = W_p^T dlogits + W_v dV in fp32, gated by h <= 0.  Writes the
-// per-sample head gradients dhead[b][0..A] (= dlogits, dV) for the heads'
-// weight-gradient GEMM and the per-sample loss scalars.
+// Trainer: the forward's heads fused with the loss and the heads' backward,
+// one CTA per sample (nnet.cpp:229-270):
+//   fp64 loss algebra from pi and V (advantage constant in the policy term),
+//   dL/dlogits through the softmax Jacobian, dV, then
+//   dh = W_p^T dlogits + W_v dV in fp32 gated by h <= 0 (written row-major
+//   for the conv path and transposed for the FC input-gradient GEMM), the
+//   per-sample head gradients dhead[b] for the heads' weight gradient, and
+//   the per-sample loss diagnostics, whose fixed-order batch sum the last
+//   CTA to finish computes (ticket counter, no float atomics).
 __global__ void __launch_bounds__(256)
-loss_heads_bwd_kernel(const double* __restrict__ pi64, const float* __restrict__ v,
-                      const int32_t* __restrict__ actions, const double* __restrict__ rets,
-                      const float* __restrict__ h, int B, int D, int A,
-                      const float* __restrict__ theta, std::size_t wp_off, std::size_t wv_off,
-                      double beta, double eps, double c_v, float* __restrict__ dhead,
-                      float* __restrict__ dh, float* __restrict__ dhT, int ldT,
-                      double* __restrict__ scal, int* __restrict__ flag) {
+heads_loss_kernel(const float* __restrict__ part, int n_split, const float* __restrict__ fc_bias,
+                  float* __restrict__ h_io, int B, int D, const float* __restrict__ theta,
+                  std::size_t wp_off, std::size_t bp_off, std::size_t wv_off, std::size_t bv_off, int A,
+                  const int32_t* __restrict__ actions, const double* __restrict__ rets, double beta,
+                  double eps, double c_v, double* __restrict__ pi64, float* __restrict__ v_out,
+                  float* __restrict__ dhead, float* __restrict__ dh, float* __restrict__ dhT, int ldT,
+                  double* __restrict__ scal, double* __restrict__ scal_sum, unsigned* __restrict__ ticket,
+                  int* __restrict__ flag) {
   pdl_enter();
   // every dtheta writer of this step runs after this kernel: reset the
   // non-finite flag here (stream order) instead of a separate memset node
   if (blockIdx.x == 0 && threadIdx.x == 0) *flag = 0;
-  __shared__ float g_sh[65];
+  extern __shared__ float sm[];
+  float* h = sm;
+  float* red = sm + D;
+  __shared__ double logit_sh[kMaxA], e_sh[kMaxA + 1], p_sh[kMaxA], lg_sh[kMaxA], dp_sh[kMaxA];
+  __shared__ float val_sh, g_sh[kMaxA + 1];
+  __shared__ bool last_sh;
   const int b = blockIdx.x;
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    const double* p = pi64 + static_cast<std::size_t>(b) * A;
+  const int tid = threadIdx.x, lane = tid & 31;
+  heads_h(part, n_split, fc_bias, h_io, B, D, b, h);
+  __syncthreads();
+  heads_logits(theta, wp_off, bp_off, wv_off, bv_off, A, D, h, red, logit_sh, &val_sh);
+  softmax64(logit_sh, A, e_sh, p_sh);
+  if (tid < 32) {
     const int a = actions[b];
-    const double adv = rets[b] - static_cast<double>(v[b]);
-    const double pa = p[a];
-    double H = 0.0;
-    for (int k = 0; k < A; ++k) H -= p[k] * log(p[k] + eps);  // eps > 0 (validated)
-    scal[3 * b + 0] = -log(pa + eps) * adv - beta * H;
-    scal[3 * b + 1] = adv * adv;
-    scal[3 * b + 2] = H;
-    double dpol[64];
-    for (int k = 0; k < A; ++k) dpol[k] = beta * (log(p[k] + eps) + p[k] / (p[k] + eps));
-    dpol[a] += -adv / (pa + eps);
-    double dot = 0.0;
-    for (int k = 0; k < A; ++k) dot += dpol[k] * p[k];
-    for (int j = 0; j < A; ++j) {
-      const float g = static_cast<float>(p[j] * (dpol[j] - dot));
+    const double adv = rets[b] - static_cast<double>(val_sh);
+    for (int k = lane; k < A; k += 32) {
+      const double p = p_sh[k];
+      pi64[static_cast<std::size_t>(b) * A + k] = p;
+      lg_sh[k] = log(p + eps);  // eps > 0 (validated)
+      double d = beta * (lg_sh[k] + p / (p + eps));
+      if (k == a) d += -adv / (p + eps);
+      dp_sh[k] = d;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      v_out[b] = val_sh;
+      double H = 0.0, dot = 0.0;
+      for (int k = 0; k < A; ++k) H -= p_sh[k] * lg_sh[k];
+      for (int k = 0; k < A; ++k) dot += dp_sh[k] * p_sh[k];
+      scal[3 * b + 0] = -lg_sh[a] * adv - beta * H;
+      scal[3 * b + 1] = adv * adv;
+      scal[3 * b + 2] = H;
+      e_sh[0] = dot;
+      const float dvv = static_cast<float>(-2.0 * c_v * adv);
+      g_sh[A] = dvv;
+      dhead[static_cast<std::size_t>(b) * (A + 1) + A] = dvv;
+    }
+    __syncwarp();
+    const double dot = e_sh[0];
+    for (int j = lane; j < A; j += 32) {
+      const float g = static_cast<float>(p_sh[j] * (dp_sh[j] - dot));
       g_sh[j] = g;
       dhead[static_cast<std::size_t>(b) * (A + 1) + j] = g;
     }
-    const float dvv = static_cast<float>(-2.0 * c_v * adv);
-    g_sh[A] = dvv;
-    dhead[static_cast<std::size_t>(b) * (A + 1) + A] = dvv;
   }
   __syncthreads();
-  const float* hrow = h + static_cast<std::size_t>(b) * D;
-  float* drow = dh + static_cast<std::size_t>(b) * D;
-  for (int o = tid; o < D; o += blockDim.x) {
-    float s = 0.0f;
-    for (int j = 0; j < A; ++j) s = fmaf(g_sh[j], theta[wp_off + static_cast<std::size_t>(j) * D + o], s);
-    s = fmaf(g_sh[A], theta[wv_off + o], s);
-    const float g = hrow[o] <= 0.0f ? 0.0f : s;
-    drow[o] = g;
-    if (dhT) dhT[static_cast<std::size_t>(o) * ldT + b] = g;
+  if (dh) {
+    float* drow = dh + static_cast<std::size_t>(b) * D;
+    for (int o = tid; o < D; o += blockDim.x) {
+      float s = 0.0f;
+      for (int j = 0; j < A; ++j) s = fmaf(g_sh[j], theta[wp_off + static_cast<std::size_t>(j) * D + o], s);
+      s = fmaf(g_sh[A], theta[wv_off + o], s);
+      const float g = h[o] <= 0.0f ? 0.0f : s;
+      drow[o] = g;
+      if (dhT) dhT[static_cast<std::size_t>(o) * ldT + b] = g;
+    }
+  }
+  // last CTA: fixed-order batch sums of the diagnostics (nnet.cpp:233-235)
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last_sh = atomicAdd(ticket, 1u) == static_cast<unsigned>(B - 1);
+  __syncthreads();
+  if (last_sh) {
+    __threadfence();
+    if (tid < 3) {
+      double s = 0.0;
+      for (int i = 0; i < B; ++i) s += static_cast<volatile double*>(scal)[3 * i + tid];
+      scal_sum[tid] = s;
+    }
+    if (tid == 0) *ticket = 0u;
   }
 }
 
@@ -289,6 +362,97 @@ conv_dgrad16_kernel(const float* __restrict__ dout, const float* __restrict__ W,
   o.z = gt.z <= 0.f ? 0.f : acc.z;
   o.w = gt.w <= 0.f ? 0.f : acc.w;
   *reinterpret_cast<float4*>(din + base) = o;
+}
+
+// Same contraction with the shape known at compile time (the GA3C stacks:
+// k = 4, s = 2, COUT = 32 / 64): the weight slice arrives by cp.async, the
+// gate load overlaps it, and each tap's COUT/4 dout vectors are issued back
+// to back, so a thread waits for one round trip per tap instead of one per
+// vector.  Result identical to conv_dgrad16_kernel (same summation order).
+template <int COUT, int K, int S>
+__device__ __forceinline__ void conv_dgrad_t_body(const float* __restrict__ dout, const float* __restrict__ W,
+                                                  const float* __restrict__ gate, float* __restrict__ din, int B,
+                                                  int ih, int iw, int cin, int oh, int ow) {
+  constexpr int KK2 = K * K;
+  constexpr int NV = COUT * KK2 * 4;  // float4 slots of the [co][ky][kx][16 ci] slice
+  extern __shared__ float4 wsh4[];
+  pdl_enter();
+  const int ci0 = blockIdx.y * 16;
+  const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(wsh4));
+#pragma unroll
+  for (int j = 0; j < (NV + 255) / 256; ++j) {
+    const int i = threadIdx.x + 256 * j;
+    if (i < NV) {
+      const int q = i & 3, r = i >> 2;
+      const float* src = W + static_cast<std::size_t>(r) * cin + ci0 + 4 * q;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + 16u * i), "l"(src) : "memory");
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  const int grp = threadIdx.x & 3;
+  const int pix = blockIdx.x * 64 + (threadIdx.x >> 2);
+  const bool live = pix < B * ih * iw;
+  const int x = live ? pix % iw : 0;
+  const int y = live ? (pix / iw) % ih : 0;
+  const int b = live ? pix / (iw * ih) : 0;
+  const std::size_t base = static_cast<std::size_t>(live ? pix : 0) * cin + ci0 + 4 * grp;
+  const float4 gt = live ? *reinterpret_cast<const float4*>(gate + base) : make_float4(0.f, 0.f, 0.f, 0.f);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  if (!live) return;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (gt.x > 0.f || gt.y > 0.f || gt.z > 0.f || gt.w > 0.f) {
+#pragma unroll
+    for (int ty = 0; ty < K / S; ++ty) {
+      const int ky = y % S + S * ty;
+      const int oy = (y - ky) / S;
+      if (y < ky || oy >= oh) continue;
+#pragma unroll
+      for (int tx = 0; tx < K / S; ++tx) {
+        const int kx = x % S + S * tx;
+        const int ox = (x - kx) / S;
+        if (x < kx || ox >= ow) continue;
+        const float4* g4 =
+            reinterpret_cast<const float4*>(dout + ((static_cast<std::size_t>(b) * oh + oy) * ow + ox) * COUT);
+        float4 d[COUT / 4];
+#pragma unroll
+        for (int c4 = 0; c4 < COUT / 4; ++c4) d[c4] = __ldg(g4 + c4);
+        const float4* w4 = wsh4 + (ky * K + kx) * 4 + grp;
+#pragma unroll
+        for (int c4 = 0; c4 < COUT / 4; ++c4) {
+          const float dv[4] = {d[c4].x, d[c4].y, d[c4].z, d[c4].w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float4 w = w4[(4 * c4 + c) * KK2 * 4];
+            acc.x = fmaf(dv[c], w.x, acc.x);
+            acc.y = fmaf(dv[c], w.y, acc.y);
+            acc.z = fmaf(dv[c], w.z, acc.z);
+            acc.w = fmaf(dv[c], w.w, acc.w);
+          }
+        }
+      }
+    }
+  }
+  float4 o;
+  o.x = gt.x <= 0.f ? 0.f : acc.x;
+  o.y = gt.y <= 0.f ? 0.f : acc.y;
+  o.z = gt.z <= 0.f ? 0.f : acc.z;
+  o.w = gt.w <= 0.f ? 0.f : acc.w;
+  *reinterpret_cast<float4*>(din + base) = o;
+}
+
+__global__ void __launch_bounds__(256)
+conv_dgrad_32x4s2_kernel(const float* __restrict__ dout, const float* __restrict__ W,
+                         const float* __restrict__ gate, float* __restrict__ din, int B, int ih, int iw,
+                         int cin, int oh, int ow) {
+  conv_dgrad_t_body<32, 4, 2>(dout, W, gate, din, B, ih, iw, cin, oh, ow);
+}
+
+__global__ void __launch_bounds__(256)
+conv_dgrad_64x4s2_kernel(const float* __restrict__ dout, const float* __restrict__ W,
+                         const float* __restrict__ gate, float* __restrict__ din, int B, int ih, int iw,
+                         int cin, int oh, int ow) {
+  conv_dgrad_t_body<64, 4, 2>(dout, W, gate, din, B, ih, iw, cin, oh, ow);
 }
 
 // ------------------------------------------------------- split-K reductions

@@ -16,6 +16,13 @@ __global__ void heads_forward_kernel(const float* part, int n_split, const float
                                      int A, float* pi32, double* pi64, float* v_out,
                                      double* v64_out);
 
+__global__ void heads_loss_kernel(const float* part, int n_split, const float* fc_bias, float* h_io, int B,
+                                  int D, const float* theta, std::size_t wp_off, std::size_t bp_off,
+                                  std::size_t wv_off, std::size_t bv_off, int A, const int32_t* actions,
+                                  const double* rets, double beta, double eps, double c_v, double* pi64,
+                                  float* v_out, float* dhead, float* dh, float* dhT, int ldT, double* scal,
+                                  double* scal_sum, unsigned* ticket, int* flag);
+
 __global__ void loss_heads_bwd_kernel(const double* pi64, const float* v, const int32_t* actions,
                                       const double* rets, const float* h, int B, int D, int A,
                                       const float* theta, std::size_t wp_off, std::size_t wv_off,
@@ -28,6 +35,10 @@ __global__ void conv_dgrad_kernel(const float* dout, const float* W, const float
                                   int B, int ih, int iw, int cin, int oh, int ow, int cout, int k,
                                   int s);
 
+__global__ void conv_dgrad_32x4s2_kernel(const float* dout, const float* W, const float* gate, float* din, int B,
+                                         int ih, int iw, int cin, int oh, int ow);
+__global__ void conv_dgrad_64x4s2_kernel(const float* dout, const float* W, const float* gate, float* din, int B,
+                                         int ih, int iw, int cin, int oh, int ow);
 __global__ void conv_dgrad16_kernel(const float* dout, const float* W, const float* gate, float* din,
                                     int B, int ih, int iw, int cin, int oh, int ow, int cout, int k,
                                     int s);

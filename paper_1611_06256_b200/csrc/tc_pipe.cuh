@@ -42,7 +42,7 @@ __device__ unsigned long long g_trace[256];
 namespace ga3c {
 namespace pipe {
 
-constexpr int kMaxStages = 4;
+constexpr int kMaxStages = 8;
 constexpr int stages_for(int stage_bytes) {
   return (220 * 1024) / stage_bytes < kMaxStages ? (220 * 1024) / stage_bytes : kMaxStages;
 }

@@ -72,6 +72,7 @@ tc_kk_ws_kernel(Seg A, Seg B, int M, int N, int K, int kc, TcEpiArgs epi) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t ready[pipe::kMaxStages], done[pipe::kMaxStages], acc_bar;
   __shared__ uint32_t tmem_base_sh;
+  __shared__ float bias_sh[BN];
   uint8_t* smem = detail::align1024(smem_raw);
   const uint32_t sbase = tc::smem_u32(smem);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -178,6 +179,11 @@ tc_kk_ws_kernel(Seg A, Seg B, int M, int N, int K, int kc, TcEpiArgs epi) {
     // staged through the (now idle) pipeline smem so global stores are
     // 16-byte, fully coalesced rows.
     TRACE(5);
+    if constexpr (MODE == TC_EPI_BIAS_RELU) {
+      // bias for this N tile, fetched while the last MMAs drain
+      if (tid < BN) bias_sh[tid] = n0 + tid < N ? __ldg(epi.bias + n0 + tid) : 0.f;
+      asm volatile("bar.sync 1, %0;" ::"n"(kProducers) : "memory");
+    }
     if (nchunks > 0) tc::mbar_wait(&acc_bar, 0);
     tc::tc_fence_after();
     TRACE(2);
@@ -207,12 +213,11 @@ tc_kk_ws_kernel(Seg A, Seg B, int M, int N, int K, int kc, TcEpiArgs epi) {
         if constexpr (MODE == TC_EPI_BIAS_RELU) {
 #pragma unroll
           for (int j = 0; j < 16; j += 4) {
-            const int n = n0 + c0 + j;
             float4 q;
-            q.x = v[j] + (n < N ? __ldg(epi.bias + n) : 0.f);
-            q.y = v[j + 1] + (n + 1 < N ? __ldg(epi.bias + n + 1) : 0.f);
-            q.z = v[j + 2] + (n + 2 < N ? __ldg(epi.bias + n + 2) : 0.f);
-            q.w = v[j + 3] + (n + 3 < N ? __ldg(epi.bias + n + 3) : 0.f);
+            q.x = v[j] + bias_sh[c0 + j];
+            q.y = v[j + 1] + bias_sh[c0 + j + 1];
+            q.z = v[j + 2] + bias_sh[c0 + j + 2];
+            q.w = v[j + 3] + bias_sh[c0 + j + 3];
             q.x = q.x < 0.f ? 0.f : q.x;
             q.y = q.y < 0.f ? 0.f : q.y;
             q.z = q.z < 0.f ? 0.f : q.z;
@@ -440,6 +445,23 @@ __global__ void __launch_bounds__(kThreads, 1) tc_mn_ws_kernel(WgradArgs a) {
     // ---- epilogue: C'[kk][co] staged transposed in smem as [co][kk], then
     // each warp writes whole 128-kk rows (512 B) with float4 stores
     TRACE(5);
+    // mode 1: the ReLU gates of this warp's output rows, loaded while the
+    // last MMAs drain (one round trip instead of one per row)
+    constexpr int RPW = BN / (kProducers / 32);
+    const int kvalid = min(128, a.Kw - kk0);  // multiple of 32 (Kw % 32 == 0)
+    const int nco = min(BN, a.cout - n0);
+    const bool lane_ok = 4 * lane < kvalid;
+    float4 gts[RPW];
+    if (a.mode == 1) {
+#pragma unroll
+      for (int j = 0; j < RPW; ++j) {
+        const int row = warp + (kProducers / 32) * j;
+        gts[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row < nco && lane_ok)
+          gts[j] = __ldg(reinterpret_cast<const float4*>(
+              a.gate + static_cast<std::size_t>(n0 + row) * a.ldo + kk0 + 4 * lane));
+      }
+    }
     if (nchunks > 0) tc::mbar_wait(&acc_bar, 0);
     tc::tc_fence_after();
     TRACE(2);
@@ -469,16 +491,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_mn_ws_kernel(WgradArgs a) {
       for (int j = 0; j < 16; ++j) stg[(c0 + j) * PT + r] = v[j];
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kProducers) : "memory");
-    const int kvalid = min(128, a.Kw - kk0);  // multiple of 32 (Kw % 32 == 0)
-    const int nco = min(BN, a.cout - n0);
-    const bool lane_ok = 4 * lane < kvalid;
-    for (int row = warp; row < nco; row += kProducers / 32) {
+#pragma unroll
+    for (int j = 0; j < RPW; ++j) {
+      const int row = warp + (kProducers / 32) * j;
+      if (row >= nco) break;
       const int co = n0 + row;
       const float4 x = *reinterpret_cast<const float4*>(stg + row * PT + 4 * lane);
       if (a.mode == 1) {
         if (lane_ok) {
           const std::size_t o = static_cast<std::size_t>(co) * a.ldo + kk0 + 4 * lane;
-          const float4 gt = __ldg(reinterpret_cast<const float4*>(a.gate + o));
+          const float4 gt = gts[j];
           float4 y;
           y.x = gt.x <= 0.f ? 0.f : x.x;
           y.y = gt.y <= 0.f ? 0.f : x.y;

@@ -2,29 +2,43 @@
 // (globaltimer at phase points).  Debug tool, not product.
 #define GA3C_TRACE 1
 #include <cstdio>
+#include <string>
 #include <vector>
 #include <cuda_runtime.h>
 #include "tc_ws.cuh"
 using namespace ga3c;
 
+template <typename TA, int BN>
+int run(int argc, char** argv);
+
 int main(int argc, char** argv) {
+  if (argc > 2 && std::string(argv[2]) == "conv1") return run<uint8_t, 16>(argc, argv);
+  return run<float, 32>(argc, argv);
+}
+
+template <typename TA, int BN>
+int run(int argc, char** argv) {
+  const bool c1 = sizeof(TA) == 1;
   const int B = argc > 1 ? atoi(argv[1]) : 40;
   // conv2 of DNN A: in [B][20][20][16] f32, W [32][4][4][16], out [B][9][9][32]
-  const int ih = 20, iw = 20, cin = 16, k = 4, s = 2, oh = 9, ow = 9, cout = 32, K = k * k * cin;
-  std::vector<float> x(B * ih * iw * cin), w(cout * K), b(cout, 0.01f);
-  for (size_t i = 0; i < x.size(); ++i) x[i] = (float)((i * 7919) % 1000) / 1000.f;
+  const int ih = c1 ? 84 : 20, iw = ih, cin = c1 ? 4 : 16, k = c1 ? 8 : 4, s = c1 ? 4 : 2;
+  const int oh = (ih - k) / s + 1, ow = oh, cout = c1 ? 16 : 32, K = k * k * cin;
+  std::vector<TA> x(B * ih * iw * cin);
+  std::vector<float> w(cout * K), b(cout, 0.01f);
+  for (size_t i = 0; i < x.size(); ++i) x[i] = c1 ? (TA)((i * 7919) % 256) : (TA)((float)((i * 7919) % 1000) / 1000.f);
   for (size_t i = 0; i < w.size(); ++i) w[i] = (float)((i * 104729) % 1000) / 1000.f - 0.5f;
-  float *dx, *dw, *db, *dout;
-  cudaMalloc(&dx, x.size() * 4); cudaMalloc(&dw, w.size() * 4); cudaMalloc(&db, 128);
+  TA* dx;
+  float *dw, *db, *dout;
+  cudaMalloc(&dx, x.size() * sizeof(TA)); cudaMalloc(&dw, w.size() * 4); cudaMalloc(&db, 128);
   cudaMalloc(&dout, (size_t)B * oh * ow * cout * 4);
-  cudaMemcpy(dx, x.data(), x.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dx, x.data(), x.size() * sizeof(TA), cudaMemcpyHostToDevice);
   cudaMemcpy(dw, w.data(), w.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(db, b.data(), 128, cudaMemcpyHostToDevice);
   Seg A{dx, (long long)ih * iw * cin, oh * ow, ow, s * iw * cin, s * cin, k * cin, iw * cin, B * oh * ow};
   Seg W{dw, K, 1, 1, 0, 0, K, 0, cout};
   TcEpiArgs e{db, dout, cout};
-  using S = ws::KKShape<float, float, 32>;
-  auto kern = ws::tc_kk_ws_kernel<float, float, 32, TC_EPI_BIAS_RELU>;
+  using S = ws::KKShape<TA, float, BN>;
+  auto kern = ws::tc_kk_ws_kernel<TA, float, BN, TC_EPI_BIAS_RELU>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
   const int M = B * oh * ow;
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
