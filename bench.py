@@ -65,8 +65,10 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=0)
     p.add_argument("--cpu-seconds", type=float, default=6.0)
-    p.add_argument("--probe", default="auto", help="kernel class for the roofline probe")
+    p.add_argument("--probe", default="conv_fwd:0",
+                   help="kernel class[:layer] for the roofline probe (auto = largest eager share)")
     p.add_argument("--no-graph", action="store_true", help="launch eagerly instead of CUDA graphs")
+    p.add_argument("--timeline", default="", help="write a per-launch timeline of one eager step here")
     return p.parse_args()
 
 
@@ -324,6 +326,14 @@ def main():
             dp.dp_update(ctx, fr + u * TB * FRAME_BYTES, True, actions.data_ptr() + 4 * u * TB,
                          rets.data_ptr() + 8 * u * TB, TB, slot, grad_view, stream, world)
 
+    def busy():
+        # Park the stream behind a ~4 ms spin so the host can enqueue a whole
+        # eager step before the GPU reaches it: the probed kernels then run
+        # back to back, and their event brackets time the kernels rather than
+        # the host's launch rate.
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(int(8e6))
+
     # ---- warmup + per-kernel breakdown (untimed) ----
     for i in range(args.warmup):
         step(i)
@@ -333,16 +343,29 @@ def main():
     for tag in ("conv_fwd", "fc_fwd", "heads", "loss_bwd", "wgrad", "dgrad", "splitk", "rmsprop",
                 "returns", "sample", "other"):
         ctx.time_kernel(tag, -1)
+        busy()
         step(0)
         ms, cnt = ctx.kernel_time()
         breakdown[tag] = round(ms, 4)
     for (tag, li) in probe_keys:
         if li >= 0:
             ctx.time_kernel(tag, li)
+            busy()
             step(0)
             ms, cnt = ctx.kernel_time()
             breakdown[f"{tag}[{li}]"] = round(ms, 4)
     ctx.time_kernel("none")
+    if args.timeline:
+        ctx.time_kernel("all")
+        busy()
+        step(0)
+        tl = ctx.timeline()
+        ctx.time_kernel("none")
+        with open(args.timeline, "w") as f:
+            f.write("# one eager step, launches queued behind a spin; ms from the first launch\n")
+            f.write("# start_ms end_ms dur_us stream kernel[layer]\n")
+            for tag, li, sid, a, b in tl:
+                f.write(f"{a:9.4f} {b:9.4f} {1e3 * (b - a):8.2f}  s{sid}  {tag}[{li}]\n")
     work = work_per_step(args.net, NA, T, TB)
     if args.probe == "auto":
         cand = [(breakdown.get(f"{t}[{l}]" if l >= 0 else t, 0.0), (t, l)) for (t, l) in work]
@@ -399,8 +422,9 @@ def main():
         ctx.time_kernel(probe[0], probe[1])
         probe_steps = max(3, min(args.steps, 50))
         for i in range(probe_steps):
+            busy()
             step(args.warmup + i)
-        ctx.sync()
+            ctx.sync()
     probe_ms, probe_n = ctx.kernel_time()
     ctx.time_kernel("none")
     if world > 1:
@@ -424,7 +448,8 @@ def main():
                  "kernel": f"{probe[0]}[layer {probe[1]}]", "launches": probe_n,
                  "avg_launch_us": 1e3 * probe_ms / max(1, probe_n),
                  "share_of_step": probe_ms / (ms_step * probed_steps),
-                 "probe_pass": ("eager steps after the graph-timed region" if graphs is not None
+                 "probe_pass": ("eager steps after the graph-timed region, each queued behind a spin so "
+                                "launches run back to back" if graphs is not None
                                 else "inside the timed region"),
                  "peak_source": f"{peak_src} ({'HBM copy' if probe[0] == 'rmsprop' else 'cuBLAS bf16 burst'})"})
 

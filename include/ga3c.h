@@ -229,6 +229,14 @@ int ga3c_compute_returns_dev(ga3c_ctx* c, const double* d_rewards, const int32_t
 int ga3c_ctx_time_kernel(ga3c_ctx* c, int tag, int layer);
 /* Sum of the bracketed device durations since the last call (blocking). */
 int ga3c_ctx_kernel_time(ga3c_ctx* c, double* total_ms, uint64_t* launches);
+/* Bracket every launch (profiling): with ga3c_ctx_time_kernel(c, GA3C_K_ALL,
+ * -1), ga3c_ctx_timeline returns up to `cap` launches since the last read:
+ * start / end in ms relative to the first bracketed launch, kernel class,
+ * trunk layer (-1 = none) and stream (0 = context stream, 1/2 = the side
+ * streams of the backward DAG).  Blocking; resets the record. */
+#define GA3C_K_ALL 12
+int ga3c_ctx_timeline(ga3c_ctx* c, int cap, double* start_ms, double* end_ms, int* tags, int* layers,
+                      int* streams, int* n);
 
 /* ------------------------------------------------------- CUDA graphs */
 /* Capture the device-resident calls issued on this context's stream between

@@ -149,10 +149,11 @@ _SIGS = {
     "ga3c_ctx_graph_end": (C.c_int, [_P, C.POINTER(C.c_int)]),
     "ga3c_ctx_graph_launch": (C.c_int, [_P, C.c_int]),
     "ga3c_ctx_kernel_time": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
+    "ga3c_ctx_timeline": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _P, C.POINTER(C.c_int)]),
 }
 
 K_TAGS = {"none": 0, "conv_fwd": 1, "fc_fwd": 2, "heads": 3, "loss_bwd": 4, "wgrad": 5, "dgrad": 6,
-          "splitk": 7, "rmsprop": 8, "returns": 9, "sample": 10, "other": 11}
+          "splitk": 7, "rmsprop": 8, "returns": 9, "sample": 10, "other": 11, "all": 12}
 
 EXPORTED = tuple(_SIGS)
 
@@ -404,6 +405,19 @@ class Context:
         ms, n = C.c_double(0), C.c_uint64(0)
         check(lib.ga3c_ctx_kernel_time(self.h, C.byref(ms), C.byref(n)), self.model.error())
         return ms.value, n.value
+
+    def timeline(self, cap=4096):
+        """Per-launch (tag, layer, stream, start_ms, end_ms) since the last read
+        (after time_kernel("all"))."""
+        import numpy as np
+        st, en = np.zeros(cap), np.zeros(cap)
+        tg, ly, sm = (np.zeros(cap, np.int32) for _ in range(3))
+        n = C.c_int(0)
+        check(lib.ga3c_ctx_timeline(self.h, cap, st.ctypes.data, en.ctypes.data, tg.ctypes.data, ly.ctypes.data,
+                                    sm.ctypes.data, C.byref(n)), self.model.error())
+        names = {v: k for k, v in K_TAGS.items()}
+        return [(names.get(int(tg[i]), str(tg[i])), int(ly[i]), int(sm[i]), float(st[i]), float(en[i]))
+                for i in range(n.value)]
 
     def graph_begin(self):
         check(lib.ga3c_ctx_graph_begin(self.h), self.model.error())

@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -101,7 +102,6 @@ struct ga3c_ctx {
   double* d_rets = nullptr;
   float* grad = nullptr;
   int* flag = nullptr;
-  unsigned* ticket = nullptr;  // last-CTA counter of heads_loss_kernel
   unsigned long long* dev_version = nullptr;
   float* part = nullptr;
   double* clip_part = nullptr;
@@ -119,6 +119,7 @@ struct ga3c_ctx {
   int timed_tag = 0, timed_layer = -1;
   std::vector<cudaEvent_t> events;
   std::size_t ev_used = 0;
+  std::vector<int> ev_meta;  // per bracketed launch: tag | layer << 8 | stream << 16
   // captured CUDA graphs of device-resident step sequences
   std::vector<cudaGraphExec_t> graphs;
   bool capturing = false;
@@ -156,6 +157,27 @@ void pdl_launch(cudaStream_t st, void (*kern)(KArgs...), dim3 grid, dim3 block, 
   cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// The same with a (cx, cy, cz) thread-block cluster.
+template <typename... KArgs, typename... Args>
+void pdl_launch_cluster(cudaStream_t st, void (*kern)(KArgs...), dim3 grid, dim3 block, std::size_t smem,
+                        dim3 cluster, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = cluster.x;
+  at[1].val.clusterDim.y = cluster.y;
+  at[1].val.clusterDim.z = cluster.z;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // --------------------------------------------------------------- GEMMs
 
 struct SplitPlan {
@@ -186,7 +208,25 @@ float* region(ga3c_ctx* c, int r) { return c->part + static_cast<std::size_t>(r)
 // on the context stream so far and directs launches to it; join() makes the
 // context stream wait for `s` and directs launches back.  Both are plain
 // event edges, so they are captured into CUDA graphs as graph dependencies.
+// A/B knobs for measurement (read once):
+//   GA3C_SERIAL_BWD=1   the whole backward on the context stream
+//   GA3C_NO_PRIO=1      side streams at the same priority as the context stream
+//   GA3C_NO_CLUSTER=1   no cluster split-K (conv forward, FC input gradient)
+bool env_flag(const char* name) {
+  const char* e = std::getenv(name);
+  return e && e[0] == '1';
+}
+bool serial_bwd() {
+  static const bool v = env_flag("GA3C_SERIAL_BWD");
+  return v;
+}
+bool no_cluster() {
+  static const bool v = env_flag("GA3C_NO_CLUSTER");
+  return v;
+}
+
 void fork_to(ga3c_ctx* c, cudaStream_t s) {
+  if (serial_bwd()) return;
   cudaEvent_t e = c->evs[c->ev_next++ & 15];
   cudaEventRecord(e, c->stream);
   cudaStreamWaitEvent(s, e, 0);
@@ -194,6 +234,7 @@ void fork_to(ga3c_ctx* c, cudaStream_t s) {
 }
 
 void join_from(ga3c_ctx* c, cudaStream_t s) {
+  if (serial_bwd()) return;
   cudaEvent_t e = c->evs[c->ev_next++ & 15];
   cudaEventRecord(e, s);
   cudaStreamWaitEvent(c->stream, e, 0);
@@ -206,13 +247,17 @@ struct Launch {
   ga3c_ctx* c;
   bool on;
   Launch(ga3c_ctx* c_, int tag, int layer) : c(c_) {
-    on = c->timed_tag == tag && (c->timed_layer < 0 || c->timed_layer == layer);
+    on = c->timed_tag == GA3C_K_ALL ||
+         (c->timed_tag == tag && (c->timed_layer < 0 || c->timed_layer == layer));
     if (on) {
       while (c->events.size() < c->ev_used + 2) {
         cudaEvent_t e;
         cudaEventCreate(&e);
         c->events.push_back(e);
       }
+      const int sid = c->cur == c->stream ? 0 : (c->cur == c->side[0] ? 1 : 2);
+      c->ev_meta.resize(c->ev_used / 2 + 1);
+      c->ev_meta[c->ev_used / 2] = tag | ((layer + 1) << 8) | (sid << 16);
       cudaEventRecord(c->events[c->ev_used], c->cur);
     }
   }
@@ -247,7 +292,11 @@ void tc_launch(ga3c_ctx* c, int tag, int layer, const Seg& A, const Seg& B, int 
   }
   dim3 grid((M + 127) / 128, splits, (N + BN - 1) / BN);
   Launch l(c, tag, layer);
-  pdl_launch(c->cur, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, A, B, M, N, K, kc, epi);
+  if (MODE == TC_EPI_BIAS_RELU && splits > 1)  // split-K reduced inside a cluster
+    pdl_launch_cluster(c->cur, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, dim3(1, splits, 1), A, B, M, N, K,
+                       kc, epi);
+  else
+    pdl_launch(c->cur, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, A, B, M, N, K, kc, epi);
 }
 
 template <typename TA, typename TB, int MODE>
@@ -331,8 +380,15 @@ void conv_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const
     if (seg_ok(A, A.rows) && L.in % 32 == 0 && L.cout <= 128 && L.cout % 4 == 0 && (L.w_off % 4) == 0) {
       TcEpiArgs e{theta + L.b_off, out, L.cout};
       const int M = B * L.pixels();
-      tc_dispatch<T, float, TC_EPI_BIAS_RELU>(c, GA3C_K_CONV_FWD, li, tc_bn(L.cout), A, W, M, L.cout,
-                                              L.in, 1, L.in, e);
+      const int bn = tc_bn(L.cout);
+      // Fewer tiles than SMs: split K over a cluster of up to 8 CTAs whose
+      // partial tiles are summed through DSMEM in the epilogue.
+      const int tiles = ((M + 127) / 128) * ((L.cout + bn - 1) / bn);
+      const int chunks = L.in / 32;
+      int ks = no_cluster() ? 1 : std::max(1, std::min({8, chunks, kNumSMs / std::max(1, tiles)}));
+      const int kc = ((chunks + ks - 1) / ks) * 32;
+      ks = (L.in + kc - 1) / kc;
+      tc_dispatch<T, float, TC_EPI_BIAS_RELU>(c, GA3C_K_CONV_FWD, li, bn, A, W, M, L.cout, L.in, ks, kc, e);
       return;
     }
   }
@@ -422,7 +478,10 @@ void wgrad_tc_launch(ga3c_ctx* c, int li, const WgradArgs& a, dim3 grid, int tag
     attr_set = true;
   }
   Launch l(c, tag, li);
-  pdl_launch(c->cur, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, a);
+  if (a.mode == 1 && grid.y > 1)  // split-K reduced inside a cluster
+    pdl_launch_cluster(c->cur, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, dim3(1, grid.y, 1), a);
+  else
+    pdl_launch(c->cur, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, a);
 }
 
 // Tensor-core weight gradient; returns false when the shape needs the SIMT path.
@@ -494,9 +553,16 @@ bool fc_dgrad_tc(ga3c_ctx* c, int li, const Layer& L, const float* theta, const 
   W.rows = L.out;
   if (!seg_ok(W, L.out) || L.in % 32 != 0 || ldT % 4 != 0 || B > 128) return false;
   const int bn = B <= 32 ? 32 : (B <= 64 ? 64 : 128);
-  WgradArgs a{W, doutT, ldT, B, L.in, L.out, ((L.out + 31) / 32) * 32, nullptr, GradMap{}, 0,
-              1, din, gate, L.in};
-  dim3 grid((L.in + 127) / 128, 1, 1);
+  // split the reduction over the layer's outputs across a cluster when the
+  // row tiles alone cannot fill the SMs
+  const int mtiles = (L.in + 127) / 128;
+  const int chunks = (L.out + 31) / 32;
+  static const bool no_mn = env_flag("GA3C_NO_CLUSTER_MN");
+  int ks = no_cluster() || no_mn ? 1 : std::max(1, std::min({8, chunks, kNumSMs / mtiles}));
+  const int kc = ((chunks + ks - 1) / ks) * 32;
+  ks = (L.out + kc - 1) / kc;
+  WgradArgs a{W, doutT, ldT, B, L.in, L.out, kc, nullptr, GradMap{}, 0, 1, din, gate, L.in};
+  dim3 grid(mtiles, ks, 1);
   switch (bn) {
     case 32: wgrad_tc_launch<float, 32>(c, li, a, grid, GA3C_K_DGRAD); break;
     case 64: wgrad_tc_launch<float, 64>(c, li, a, grid, GA3C_K_DGRAD); break;
@@ -619,7 +685,7 @@ int run_forward(ga3c_ctx* c, const float* theta, const void* d_in, bool u8, int 
     hin->h = h;
     return GA3C_OK;
   }
-  const std::size_t smem = (static_cast<std::size_t>(D) + 8 * (A + 1)) * sizeof(float);
+  const std::size_t smem = (static_cast<std::size_t>(D) * (A + 2) + 8 * (A + 1)) * sizeof(float);
   {
     Launch l(c, GA3C_K_HEADS, -1);
     pdl_launch(c->cur, heads_forward_kernel, dim3(B), dim3(256), smem, part, n_split, fc_bias, h, B, D, theta,
@@ -640,12 +706,12 @@ int run_loss_grad(ga3c_ctx* c, const float* theta, const void* d_in, bool u8, co
   const float* h = hi.h;
   float* dh = lo.n_trunk ? c->dout[lo.n_trunk - 1] : nullptr;
   {
-    const std::size_t smem = (static_cast<std::size_t>(D) + 8 * (A + 1)) * sizeof(float);
+    const std::size_t smem = (static_cast<std::size_t>(D) * (A + 2) + 8 * (A + 1)) * sizeof(float);
     Launch l(c, GA3C_K_LOSS_BWD, -1);
     pdl_launch(c->cur, heads_loss_kernel, dim3(B), dim3(256), smem, hi.part, hi.n_split, hi.fc_bias, hi.h, B, D,
                theta, lo.policy.w_off, lo.policy.b_off, lo.value.w_off, lo.value.b_off, A, d_act, d_rets,
                m->hp.beta, m->hp.eps_log, m->hp.value_loss_weight, c->pi64, c->v, c->dhead, dh,
-               lo.n_trunk ? c->dhT : nullptr, c->ldT, c->scal, c->scal_sum, c->ticket, c->flag);
+               lo.n_trunk ? c->dhT : nullptr, c->ldT, c->scal, c->flag);
   }
   // Backward DAG.  The critical path is the input-gradient chain
   // (loss -> dgrad L-1 -> ... -> dgrad 1 -> wgrad 0); the heads' and the
@@ -660,6 +726,10 @@ int run_loss_grad(ga3c_ctx* c, const float* theta, const void* d_in, bool u8, co
     DenseT a{c->dhead, A + 1};
     WithOnes<DenseT> b{DenseT{h, D}, D};
     wgrad_gemm(c, -1, a, b, gm, A + 1, D + 1, B, region(c, kRegions - 1));
+  }
+  {
+    Launch l(c, GA3C_K_OTHER, -1);
+    pdl_launch(c->cur, scalars_kernel, dim3(1), dim3(32), 0, c->scal, B, c->scal_sum);
   }
   c->cur = c->stream;
   bool used[2] = {true, false};
@@ -825,6 +895,11 @@ ga3c_model* ga3c_model_create(const ga3c_net_spec* spec, const ga3c_hyper* hp, i
   m->hp = *hp;
   m->lo = layout_of(*spec);
   m->device = device;
+  if ((static_cast<std::size_t>(m->lo.head_in()) * (spec->n_actions + 2) + 8 * (spec->n_actions + 1)) *
+          sizeof(float) > 200 * 1024) {
+    delete m;
+    return fail(GA3C_INVALID_ARGUMENT, "head input too wide: the heads' weights must fit shared memory");
+  }
   Slot s;
   const std::size_t bytes = m->lo.total * sizeof(float);
   if (cudaMalloc(&s.theta, bytes) != cudaSuccess || cudaMalloc(&s.g, bytes) != cudaSuccess ||
@@ -937,10 +1012,16 @@ ga3c_ctx* ga3c_ctx_create(ga3c_model* m, int max_batch, int* status) {
   c->max_batch = max_batch;
   const Layout& lo = m->lo;
   const std::size_t B = max_batch;
-  bool ok = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) == cudaSuccess;
+  // The context stream carries the critical path (forward, loss, the
+  // input-gradient chain, RMSProp) at the highest priority; the side
+  // streams of the backward DAG (weight gradients) fill the SMs it leaves.
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (env_flag("GA3C_NO_PRIO")) prio_hi = prio_lo;
+  bool ok = cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi) == cudaSuccess;
   c->cur = c->stream;
   for (auto& sd : c->side)
-    if (ok) ok = cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking) == cudaSuccess;
+    if (ok) ok = cudaStreamCreateWithPriority(&sd, cudaStreamNonBlocking, prio_lo) == cudaSuccess;
   for (auto& e : c->evs)
     if (ok) ok = cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
   auto alloc = [&](auto** p, std::size_t bytes) {
@@ -965,14 +1046,12 @@ ga3c_ctx* ga3c_ctx_create(ga3c_model* m, int max_batch, int* status) {
   alloc(&c->d_rets, B * sizeof(double));
   alloc(&c->grad, lo.total * sizeof(float));
   alloc(&c->flag, sizeof(int));
-  alloc(&c->ticket, sizeof(unsigned));
   alloc(&c->dev_version, sizeof(unsigned long long));
   alloc(&c->part, kPartFloats * sizeof(float));
   alloc(&c->clip_part, kNumSMs * sizeof(double));
   if (ok) ok = cudaMallocHost(&c->h_flag, sizeof(int)) == cudaSuccess;
   if (ok) ok = cudaMemset(c->dev_version, 0, sizeof(unsigned long long)) == cudaSuccess;
   if (ok) ok = cudaMemset(c->flag, 0, sizeof(int)) == cudaSuccess;
-  if (ok) ok = cudaMemset(c->ticket, 0, sizeof(unsigned)) == cudaSuccess;
   if (ok) {
     const int max_smem = 200 * 1024;
     ok = cudaFuncSetAttribute(heads_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -995,7 +1074,7 @@ void ga3c_ctx_destroy(ga3c_ctx* c) {
   cudaSetDevice(c->m->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   void* ps[] = {c->d_in, c->hin, c->pi32, c->pi64, c->v, c->v64, c->dhead, c->dhT, c->scal,
-                c->scal_sum, c->d_actions, c->d_rets, c->grad, c->flag, c->ticket, c->dev_version, c->part,
+                c->scal_sum, c->d_actions, c->d_rets, c->grad, c->flag, c->dev_version, c->part,
                 c->clip_part, c->r_rew, c->r_off, c->r_term, c->r_boot, c->r_out};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -1359,7 +1438,7 @@ int ga3c_sample_actions_dev(ga3c_ctx* c, const float* d_pi, const double* d_u, i
 }
 
 int ga3c_ctx_time_kernel(ga3c_ctx* c, int tag, int layer) {
-  if (!c || tag < 0 || tag > GA3C_K_OTHER) return GA3C_INVALID_ARGUMENT;
+  if (!c || tag < 0 || tag > GA3C_K_ALL) return GA3C_INVALID_ARGUMENT;
   c->timed_tag = tag;
   c->timed_layer = layer;
   c->ev_used = 0;
@@ -1379,6 +1458,30 @@ int ga3c_ctx_kernel_time(ga3c_ctx* c, double* total_ms, uint64_t* launches) {
   }
   if (total_ms) *total_ms = tot;
   if (launches) *launches = c->ev_used / 2;
+  c->ev_used = 0;
+  return GA3C_OK;
+}
+
+int ga3c_ctx_timeline(ga3c_ctx* c, int cap, double* start_ms, double* end_ms, int* tags, int* layers,
+                      int* streams, int* n) {
+  if (!c || cap < 0) return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  GA3C_CUDA(cudaDeviceSynchronize());
+  const int cnt = static_cast<int>(c->ev_used / 2);
+  int k = 0;
+  for (int i = 0; i < cnt && k < cap; ++i, ++k) {
+    float a = 0.f, b = 0.f;
+    GA3C_CUDA(cudaEventElapsedTime(&a, c->events[0], c->events[2 * i]));
+    GA3C_CUDA(cudaEventElapsedTime(&b, c->events[0], c->events[2 * i + 1]));
+    if (start_ms) start_ms[k] = a;
+    if (end_ms) end_ms[k] = b;
+    const int meta = c->ev_meta[i];
+    if (tags) tags[k] = meta & 0xff;
+    if (layers) layers[k] = ((meta >> 8) & 0xff) - 1;
+    if (streams) streams[k] = meta >> 16;
+  }
+  if (n) *n = k;
   c->ev_used = 0;
   return GA3C_OK;
 }

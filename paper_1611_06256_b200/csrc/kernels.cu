@@ -24,6 +24,22 @@
 
 namespace ga3c {
 
+#ifdef GA3C_HTRACE
+__device__ unsigned long long g_htrace[32];
+#define HTRACE(i)                                                       \
+  do {                                                                  \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                          \
+      unsigned long long t_;                                            \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));             \
+      g_htrace[i] = t_;                                                 \
+    }                                                                   \
+  } while (0)
+#else
+#define HTRACE(i) \
+  do {            \
+  } while (0)
+#endif
+
 namespace {
 
 constexpr int kMaxA = 64;  // n_actions limit (validated by the engine)
@@ -59,18 +75,17 @@ __device__ __forceinline__ void heads_h(const float* __restrict__ part, int n_sp
   for (int o = threadIdx.x; o < D; o += blockDim.x) {
     float v;
     if (part) {
+      // 16 loads in flight per round; split k accumulates into chain k % 8
       float c[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       const std::size_t stride = static_cast<std::size_t>(B) * D;
       const float* pp = part + static_cast<std::size_t>(b) * D + o;
-      int k = 0;
-      for (; k + 8 <= n_split; k += 8) {
-        float t[8];
+      for (int k = 0; k < n_split; k += 16) {
+        float t[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) t[u] = pp[(k + u) * stride];
+        for (int u = 0; u < 16; ++u) t[u] = k + u < n_split ? pp[(k + u) * stride] : 0.f;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) c[u] += t[u];
+        for (int u = 0; u < 16; ++u) c[u & 7] += t[u];
       }
-      for (int u = 0; k < n_split; ++k, ++u) c[u] += pp[k * stride];
       const float s = ((c[0] + c[1]) + (c[2] + c[3])) + ((c[4] + c[5]) + (c[6] + c[7]));
       v = s + fc_bias[o];
       v = v < 0.0f ? 0.0f : v;
@@ -82,27 +97,66 @@ __device__ __forceinline__ void heads_h(const float* __restrict__ part, int n_sp
   }
 }
 
+// Head weights [A][D] policy rows then the value row -> smem (4-byte
+// cp.async: the offsets carry no alignment guarantee); completes with
+// heads_w_wait().  Issued first so it overlaps the partial reduction.
+__device__ __forceinline__ void heads_w_issue(const float* __restrict__ theta, std::size_t wp_off,
+                                              std::size_t wv_off, int A, int D, float* w) {
+  const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(w));
+  const int n = (A + 1) * D;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const float* src = i < A * D ? theta + wp_off + i : theta + wv_off + (i - A * D);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sb + 4u * i), "l"(src) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void heads_w_wait() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+}
+
 // Returns (in warp 0, all lanes) nothing; writes logit_sh[0..A) (as double)
 // and *val_sh = value.  Must be called by the whole CTA.
-__device__ __forceinline__ void heads_logits(const float* __restrict__ theta, std::size_t wp_off,
-                                             std::size_t bp_off, std::size_t wv_off, std::size_t bv_off,
-                                             int A, int D, const float* h, float* red, double* logit_sh,
-                                             float* val_sh) {
+// bias_j: lane j of warp 0 holds the bias of output j (j <= A), prefetched
+// at kernel start.  All (A+1) dot products run in one pass over h with
+// independent accumulators and interleaved warp reductions.
+__device__ __forceinline__ void heads_logits(int A, int D, const float* wsm, const float* h, float bias_j,
+                                             float* red, double* logit_sh, float* val_sh) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int j = 0; j <= A; ++j) {
-    const float* w = theta + (j < A ? wp_off + static_cast<std::size_t>(j) * D : wv_off);
-    float s = 0.0f;
-    for (int o = tid; o < D; o += blockDim.x) s = fmaf(w[o], h[o], s);
-    s = warp_sum(s);
-    if (lane == 0) red[warp * (A + 1) + j] = s;
+  if (A + 1 <= 8) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int o = tid; o < D; o += blockDim.x) {
+      const float x = h[o];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j <= A) acc[j] = fmaf(wsm[static_cast<std::size_t>(j) * D + o], x, acc[j]);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j <= A) red[warp * (A + 1) + j] = acc[j];
+    }
+  } else {
+    for (int j = 0; j <= A; ++j) {
+      const float* w = wsm + static_cast<std::size_t>(j) * D;
+      float sacc = 0.0f;
+      for (int o = tid; o < D; o += blockDim.x) sacc = fmaf(w[o], h[o], sacc);
+      sacc = warp_sum(sacc);
+      if (lane == 0) red[warp * (A + 1) + j] = sacc;
+    }
   }
   __syncthreads();
   if (warp == 0) {
     for (int j = lane; j <= A; j += 32) {
-      float s = 0.0f;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w * (A + 1) + j];
-      const float bias = j < A ? theta[bp_off + j] : theta[bv_off];
-      const float z = s + bias;
+      float sacc = 0.0f;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) sacc += red[w * (A + 1) + j];
+      const float z = sacc + bias_j;
       if (j < A)
         logit_sh[j] = z;
       else
@@ -143,14 +197,18 @@ heads_forward_kernel(const float* __restrict__ part, int n_split, const float* _
                      float* __restrict__ v_out, double* __restrict__ v64_out) {
   pdl_enter();
   extern __shared__ float sm[];
-  float* h = sm;        // D
-  float* red = sm + D;  // [8 warps][A+1]
+  float* h = sm;                 // D
+  float* red = sm + D;           // [8 warps][A+1]
+  float* wsm = red + 8 * (A + 1);  // [A+1][D] head weights
   __shared__ double logit_sh[kMaxA], e_sh[kMaxA + 1], p_sh[kMaxA];
   __shared__ float val_sh;
   const int b = blockIdx.x;
+  heads_w_issue(theta, wp_off, wv_off, A, D, wsm);
+  const int lane = threadIdx.x & 31;
+  const float bias_j = threadIdx.x < 32 && lane <= A ? theta[lane < A ? bp_off + lane : bv_off] : 0.f;
   heads_h(part, n_split, fc_bias, h_io, B, D, b, h);
-  __syncthreads();
-  heads_logits(theta, wp_off, bp_off, wv_off, bv_off, A, D, h, red, logit_sh, &val_sh);
+  heads_w_wait();
+  heads_logits(A, D, wsm, h, bias_j, red, logit_sh, &val_sh);
   softmax64(logit_sh, A, e_sh, p_sh);
   for (int j = threadIdx.x; j < A; j += blockDim.x) {
     pi64[static_cast<std::size_t>(b) * A + j] = p_sh[j];
@@ -178,27 +236,37 @@ heads_loss_kernel(const float* __restrict__ part, int n_split, const float* __re
                   const int32_t* __restrict__ actions, const double* __restrict__ rets, double beta,
                   double eps, double c_v, double* __restrict__ pi64, float* __restrict__ v_out,
                   float* __restrict__ dhead, float* __restrict__ dh, float* __restrict__ dhT, int ldT,
-                  double* __restrict__ scal, double* __restrict__ scal_sum, unsigned* __restrict__ ticket,
-                  int* __restrict__ flag) {
+                  double* __restrict__ scal, int* __restrict__ flag) {
   pdl_enter();
   // every dtheta writer of this step runs after this kernel: reset the
   // non-finite flag here (stream order) instead of a separate memset node
   if (blockIdx.x == 0 && threadIdx.x == 0) *flag = 0;
+  HTRACE(0);
   extern __shared__ float sm[];
   float* h = sm;
   float* red = sm + D;
+  float* wsm = red + 8 * (A + 1);  // [A+1][D] head weights
   __shared__ double logit_sh[kMaxA], e_sh[kMaxA + 1], p_sh[kMaxA], lg_sh[kMaxA], dp_sh[kMaxA];
   __shared__ float val_sh, g_sh[kMaxA + 1];
-  __shared__ bool last_sh;
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31;
+  heads_w_issue(theta, wp_off, wv_off, A, D, wsm);
+  HTRACE(1);
+  // small per-sample inputs, fetched now so their latency hides under the
+  // partial reduction
+  const float bias_j = tid < 32 && lane <= A ? theta[lane < A ? bp_off + lane : bv_off] : 0.f;
+  const int a = tid < 32 ? actions[b] : 0;
+  const double ret_b = tid < 32 ? rets[b] : 0.0;
   heads_h(part, n_split, fc_bias, h_io, B, D, b, h);
-  __syncthreads();
-  heads_logits(theta, wp_off, bp_off, wv_off, bv_off, A, D, h, red, logit_sh, &val_sh);
+  HTRACE(2);
+  heads_w_wait();
+  HTRACE(3);
+  heads_logits(A, D, wsm, h, bias_j, red, logit_sh, &val_sh);
+  HTRACE(4);
   softmax64(logit_sh, A, e_sh, p_sh);
+  HTRACE(5);
   if (tid < 32) {
-    const int a = actions[b];
-    const double adv = rets[b] - static_cast<double>(val_sh);
+    const double adv = ret_b - static_cast<double>(val_sh);
     for (int k = lane; k < A; k += 32) {
       const double p = p_sh[k];
       pi64[static_cast<std::size_t>(b) * A + k] = p;
@@ -230,31 +298,20 @@ heads_loss_kernel(const float* __restrict__ part, int n_split, const float* __re
     }
   }
   __syncthreads();
+  HTRACE(6);
   if (dh) {
     float* drow = dh + static_cast<std::size_t>(b) * D;
     for (int o = tid; o < D; o += blockDim.x) {
       float s = 0.0f;
-      for (int j = 0; j < A; ++j) s = fmaf(g_sh[j], theta[wp_off + static_cast<std::size_t>(j) * D + o], s);
-      s = fmaf(g_sh[A], theta[wv_off + o], s);
+      for (int j = 0; j < A; ++j) s = fmaf(g_sh[j], wsm[static_cast<std::size_t>(j) * D + o], s);
+      s = fmaf(g_sh[A], wsm[static_cast<std::size_t>(A) * D + o], s);
       const float g = h[o] <= 0.0f ? 0.0f : s;
       drow[o] = g;
       if (dhT) dhT[static_cast<std::size_t>(o) * ldT + b] = g;
     }
   }
-  // last CTA: fixed-order batch sums of the diagnostics (nnet.cpp:233-235)
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) last_sh = atomicAdd(ticket, 1u) == static_cast<unsigned>(B - 1);
-  __syncthreads();
-  if (last_sh) {
-    __threadfence();
-    if (tid < 3) {
-      double s = 0.0;
-      for (int i = 0; i < B; ++i) s += static_cast<volatile double*>(scal)[3 * i + tid];
-      scal_sum[tid] = s;
-    }
-    if (tid == 0) *ticket = 0u;
-  }
+  HTRACE(7);
+  HTRACE(9);
 }
 
 // Fixed-order batch sums of the per-sample diagnostics (nnet.cpp:233-235).

@@ -21,7 +21,7 @@ __global__ void heads_loss_kernel(const float* part, int n_split, const float* f
                                   std::size_t wv_off, std::size_t bv_off, int A, const int32_t* actions,
                                   const double* rets, double beta, double eps, double c_v, double* pi64,
                                   float* v_out, float* dhead, float* dh, float* dhT, int ldT, double* scal,
-                                  double* scal_sum, unsigned* ticket, int* flag);
+                                  int* flag);
 
 __global__ void loss_heads_bwd_kernel(const double* pi64, const float* v, const int32_t* actions,
                                       const double* rets, const float* h, int B, int D, int A,

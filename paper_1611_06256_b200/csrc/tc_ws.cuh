@@ -82,6 +82,8 @@ tc_kk_ws_kernel(Seg A, Seg B, int M, int N, int K, int kc, TcEpiArgs epi) {
   const int kb = split * kc;
   const int ke = min(K, kb + kc);
   const int nchunks = (ke - kb + 31) / 32;
+  // BIAS_RELU with grid.y > 1: split-K over a (1, grid.y, 1) cluster
+  const bool csplit = MODE == TC_EPI_BIAS_RELU && gridDim.y > 1;
 
   TRACE(0);
   typename S::TileA ta;
@@ -210,7 +212,12 @@ tc_kk_ws_kernel(Seg A, Seg B, int M, int N, int K, int kc, TcEpiArgs epi) {
         } else {
           tc::tmem_ld_wait();
         }
-        if constexpr (MODE == TC_EPI_BIAS_RELU) {
+        if (MODE == TC_EPI_BIAS_RELU && csplit) {
+          // split-K partial: raw sums, reduced across the cluster below
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<float4*>(stg + r * PR + c0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        } else if constexpr (MODE == TC_EPI_BIAS_RELU) {
 #pragma unroll
           for (int j = 0; j < 16; j += 4) {
             float4 q;
@@ -236,7 +243,7 @@ tc_kk_ws_kernel(Seg A, Seg B, int M, int N, int K, int kc, TcEpiArgs epi) {
     if constexpr (MODE == TC_EPI_BIAS_RELU) {
       // rows m0.. of out (row stride ldo): nvalid floats each
       const int v4 = nvalid / 4;  // N % 4 == 0 (checked by the dispatcher)
-      for (int e = tid; e < mvalid * v4; e += kProducers) {
+      for (int e = tid; e < (csplit ? 0 : mvalid * v4); e += kProducers) {
         const int rr = e / v4, q = e - rr * v4;
         *reinterpret_cast<float4*>(epi.out + static_cast<std::size_t>(m0 + rr) * epi.ldo + n0 + 4 * q) =
             *reinterpret_cast<const float4*>(stg + rr * PR + 4 * q);
@@ -250,6 +257,48 @@ tc_kk_ws_kernel(Seg A, Seg B, int M, int N, int K, int kc, TcEpiArgs epi) {
           *reinterpret_cast<float4*>(epi.out + (static_cast<std::size_t>(split) * N + n0 + n) * epi.ldo + m0 +
                                      4 * q) = *reinterpret_cast<const float4*>(stg + n * PT + 4 * q);
       }
+    }
+  }
+  if constexpr (MODE == TC_EPI_BIAS_RELU) {
+    if (csplit) {
+      // Split-K across the cluster (grid.y = cluster.y = KS): every CTA
+      // staged its partial tile; CTA rank q finishes rows [q*RB, (q+1)*RB)
+      // by summing the KS partials in rank order through DSMEM (fixed order:
+      // deterministic), then bias + ReLU and coalesced stores.
+      tc::cluster_sync();
+      if (warp < kMmaWarp) {
+        const int KS = gridDim.y;
+        const int rank = static_cast<int>(tc::cluster_rank());
+        constexpr int PR = BN + 4;
+        const int mvalid = min(128, M - m0);
+        const int v4 = min(BN, N - n0) / 4;
+        const int RB = (128 + KS - 1) / KS;
+        const int r0 = rank * RB, r1 = min(mvalid, r0 + RB);
+        const uint32_t base = tc::smem_u32(smem);
+        for (int e = tid; e < (r1 - r0) * v4; e += kProducers) {
+          const int rr = r0 + e / v4, q = e % v4;
+          const uint32_t off = base + static_cast<uint32_t>((rr * PR + 4 * q) * 4);
+          float4 a = tc::ld_dsmem4(tc::mapa(off, 0));
+          for (int k = 1; k < KS; ++k) {
+            const float4 b = tc::ld_dsmem4(tc::mapa(off, k));
+            a.x += b.x;
+            a.y += b.y;
+            a.z += b.z;
+            a.w += b.w;
+          }
+          const int c = 4 * q;
+          a.x += bias_sh[c];
+          a.y += bias_sh[c + 1];
+          a.z += bias_sh[c + 2];
+          a.w += bias_sh[c + 3];
+          a.x = a.x < 0.f ? 0.f : a.x;
+          a.y = a.y < 0.f ? 0.f : a.y;
+          a.z = a.z < 0.f ? 0.f : a.z;
+          a.w = a.w < 0.f ? 0.f : a.w;
+          *reinterpret_cast<float4*>(epi.out + static_cast<std::size_t>(m0 + rr) * epi.ldo + n0 + c) = a;
+        }
+      }
+      tc::cluster_sync();  // partial tiles stay readable until every rank is done
     }
   }
   TRACE(3);
@@ -300,6 +349,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_mn_ws_kernel(WgradArgs a) {
   const int pe = min(a.npix, pb + a.kc);
   const int nchunks = (pe - pb + 31) / 32;
   const bool do_bias = blockIdx.x == 0 && a.mode == 0;
+  // mode 1 with grid.y > 1: split-K over a (1, grid.y, 1) cluster
+  const bool csplit = a.mode == 1 && gridDim.y > 1;
 
   const int xp = tid >> 3, xv = tid & 7;
   int xcoff[4];
@@ -449,13 +500,20 @@ __global__ void __launch_bounds__(kThreads, 1) tc_mn_ws_kernel(WgradArgs a) {
     // last MMAs drain (one round trip instead of one per row)
     constexpr int RPW = BN / (kProducers / 32);
     const int kvalid = min(128, a.Kw - kk0);  // multiple of 32 (Kw % 32 == 0)
-    const int nco = min(BN, a.cout - n0);
     const bool lane_ok = 4 * lane < kvalid;
+    // output rows this CTA finishes: all of them, or (cluster split-K) the
+    // rank's block of BN / KS rows
+    int rbase = 0, nco = min(BN, a.cout - n0);
+    if (csplit) {
+      const int RB = (BN + gridDim.y - 1) / gridDim.y;
+      rbase = static_cast<int>(tc::cluster_rank()) * RB;
+      nco = min(nco, rbase + RB);
+    }
     float4 gts[RPW];
     if (a.mode == 1) {
 #pragma unroll
       for (int j = 0; j < RPW; ++j) {
-        const int row = warp + (kProducers / 32) * j;
+        const int row = rbase + warp + (kProducers / 32) * j;
         gts[j] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (row < nco && lane_ok)
           gts[j] = __ldg(reinterpret_cast<const float4*>(
@@ -491,12 +549,30 @@ __global__ void __launch_bounds__(kThreads, 1) tc_mn_ws_kernel(WgradArgs a) {
       for (int j = 0; j < 16; ++j) stg[(c0 + j) * PT + r] = v[j];
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kProducers) : "memory");
+    if (csplit) tc::cluster_sync();  // every rank's partial tile is staged
 #pragma unroll
     for (int j = 0; j < RPW; ++j) {
-      const int row = warp + (kProducers / 32) * j;
+      const int row = rbase + warp + (kProducers / 32) * j;
       if (row >= nco) break;
       const int co = n0 + row;
-      const float4 x = *reinterpret_cast<const float4*>(stg + row * PT + 4 * lane);
+      float4 x;
+      if (csplit) {
+        // fixed rank order through DSMEM: deterministic
+        x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (lane_ok) {
+          const uint32_t off = tc::smem_u32(stg + row * PT + 4 * lane);
+          x = tc::ld_dsmem4(tc::mapa(off, 0));
+          for (int k = 1; k < static_cast<int>(gridDim.y); ++k) {
+            const float4 y = tc::ld_dsmem4(tc::mapa(off, k));
+            x.x += y.x;
+            x.y += y.y;
+            x.z += y.z;
+            x.w += y.w;
+          }
+        }
+      } else {
+        x = *reinterpret_cast<const float4*>(stg + row * PT + 4 * lane);
+      }
       if (a.mode == 1) {
         if (lane_ok) {
           const std::size_t o = static_cast<std::size_t>(co) * a.ldo + kk0 + 4 * lane;
@@ -550,6 +626,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_mn_ws_kernel(WgradArgs a) {
         }
       }
     }
+  }
+  if (csplit) {
+    // MMA warp: matches the producers' "staged" barrier; everyone: partial
+    // tiles stay readable until every rank is done
+    if (warp == kMmaWarp) tc::cluster_sync();
+    tc::cluster_sync();
   }
   TRACE(3);
   tc::tc_fence_before();
