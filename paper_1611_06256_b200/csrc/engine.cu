@@ -34,6 +34,7 @@
 #include "tc_wgrad.cuh"
 #include "tc_pipe.cuh"
 #include "tc_ws.cuh"
+#include "tc_bf16.cuh"
 #include "pdl.cuh"
 
 using namespace ga3c;
@@ -280,11 +281,11 @@ void launch_gemm(ga3c_ctx* c, int tag, int layer, const LA& la, const LB& lb, co
 
 // ------------------------------------------------------ tensor-core GEMMs
 
-template <typename TA, typename TB, int BN, int MODE>
-void tc_launch(ga3c_ctx* c, int tag, int layer, const Seg& A, const Seg& B, int M, int N, int K,
-               int splits, int kc, const TcEpiArgs& epi) {
-  using S = ws::KKShape<TA, TB, BN>;
-  auto kern = ws::tc_kk_ws_kernel<TA, TB, BN, MODE>;
+template <typename TA, typename TB, int BN, int MODE, bool SHALLOW>
+void tc_launch_v(ga3c_ctx* c, int tag, int layer, const Seg& A, const Seg& B, int M, int N, int K, int splits,
+                 int kc, const TcEpiArgs& epi) {
+  using S = ws::KKShape<TA, TB, BN, SHALLOW>;
+  auto kern = ws::tc_kk_ws_kernel<TA, TB, BN, MODE, SHALLOW>;
   static bool attr_set = false;  // idempotent; racing setters write the same value
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
@@ -297,6 +298,18 @@ void tc_launch(ga3c_ctx* c, int tag, int layer, const Seg& A, const Seg& B, int 
                        kc, epi);
   else
     pdl_launch(c->cur, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, A, B, M, N, K, kc, epi);
+}
+
+// Grids of more than one wave get the shallow ring (two CTAs per SM).
+template <typename TA, typename TB, int BN, int MODE>
+void tc_launch(ga3c_ctx* c, int tag, int layer, const Seg& A, const Seg& B, int M, int N, int K, int splits,
+               int kc, const TcEpiArgs& epi) {
+  static const bool deep_only = env_flag("GA3C_DEEP_ONLY");
+  const long long ctas = static_cast<long long>((M + 127) / 128) * splits * ((N + BN - 1) / BN);
+  if (ctas > kNumSMs && splits == 1 && !deep_only)
+    tc_launch_v<TA, TB, BN, MODE, true>(c, tag, layer, A, B, M, N, K, splits, kc, epi);
+  else
+    tc_launch_v<TA, TB, BN, MODE, false>(c, tag, layer, A, B, M, N, K, splits, kc, epi);
 }
 
 template <typename TA, typename TB, int MODE>
@@ -370,9 +383,67 @@ Im2col<T> im2col_of(const Layer& L, const void* x, long long bstride) {
   return g;
 }
 
+template <int BN, bool SHALLOW>
+void u8_conv_launch(ga3c_ctx* c, int li, const Seg& A, const Seg& W, int M, int N, int K, int ks, int kc,
+                    const TcEpiArgs& e) {
+  using S = bf::U8Shape<BN>;
+  constexpr int NS = SHALLOW ? (S::NS_2 < S::NS_DEEP ? S::NS_2 : S::NS_DEEP) : S::NS_DEEP;
+  constexpr int SMEM = NS * S::STAGE + 1024;
+  auto kern = bf::tc_u8_fwd_kernel<BN, SHALLOW>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr_set = true;
+  }
+  dim3 grid((M + 127) / 128, ks, (N + BN - 1) / BN);
+  Launch l(c, GA3C_K_CONV_FWD, li);
+  if (ks > 1)
+    pdl_launch_cluster(c->cur, kern, grid, dim3(bf::kThreads), SMEM, dim3(1, ks, 1), A, W, M, N, K, kc, e);
+  else
+    pdl_launch(c->cur, kern, grid, dim3(bf::kThreads), SMEM, A, W, M, N, K, kc, e);
+}
+
+// Conv on raw u8 frames through the exact bf16 split (tc_bf16.cuh).
+bool u8_conv_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const Seg& A, float* out, int B) {
+  static const bool off = env_flag("GA3C_NO_BF16");
+  const int bn = tc_bn(L.cout);
+  if (off || L.in % 64 != 0 || (L.k * L.cin) % 32 != 0 || bn > 64 || L.cout % 4 != 0 || L.w_off % 4 != 0 ||
+      A.rowlen % 32 != 0)
+    return false;
+  Seg W = dense_seg(theta + L.w_off, L.cout, L.in, L.in, false);
+  TcEpiArgs e{theta + L.b_off, out, L.cout};
+  const int M = B * L.pixels();
+  const int tiles = ((M + 127) / 128) * ((L.cout + bn - 1) / bn);
+  const int chunks = L.in / 64;
+  int ks = no_cluster() ? 1 : std::max(1, std::min({8, chunks, kNumSMs / std::max(1, tiles)}));
+  const int kc = ((chunks + ks - 1) / ks) * 64;
+  ks = (L.in + kc - 1) / kc;
+  const bool shallow = tiles * ks > kNumSMs && ks == 1 && !env_flag("GA3C_DEEP_ONLY");
+  switch (bn) {
+    case 16:
+      shallow ? u8_conv_launch<16, true>(c, li, A, W, M, L.cout, L.in, ks, kc, e)
+              : u8_conv_launch<16, false>(c, li, A, W, M, L.cout, L.in, ks, kc, e);
+      break;
+    case 32:
+      shallow ? u8_conv_launch<32, true>(c, li, A, W, M, L.cout, L.in, ks, kc, e)
+              : u8_conv_launch<32, false>(c, li, A, W, M, L.cout, L.in, ks, kc, e);
+      break;
+    default:
+      shallow ? u8_conv_launch<64, true>(c, li, A, W, M, L.cout, L.in, ks, kc, e)
+              : u8_conv_launch<64, false>(c, li, A, W, M, L.cout, L.in, ks, kc, e);
+      break;
+  }
+  return true;
+}
+
 template <typename T>
 void conv_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const void* x, float* out,
                   int B, long long in_stride) {
+  if constexpr (sizeof(T) == 1) {
+    Seg A = conv_seg<T>(L, x, in_stride);
+    A.rows = B * L.pixels();
+    if (seg_ok(A, A.rows) && u8_conv_forward(c, li, L, theta, A, out, B)) return;
+  }
   {
     Seg A = conv_seg<T>(L, x, in_stride);
     A.rows = B * L.pixels();

@@ -42,7 +42,11 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 }
 // All threads of every CTA in the cluster; release/acquire orders the smem
 // writes before the barrier with the remote reads after it.
+// .aligned: the warp must be converged, so reconverge first (a role branch
+// such as the single MMA-issuing lane may still be diverged here; a diverged
+// arrival would be counted against the next barrier phase).
 __device__ __forceinline__ void cluster_sync() {
+  __syncwarp();
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {

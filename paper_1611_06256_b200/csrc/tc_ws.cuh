@@ -50,24 +50,28 @@ struct TmemCols {
 };
 
 // =========================================================== K-major GEMM
-template <typename TA, typename TB, int BN>
+// SHALLOW: at most ~112 KB of ring so two CTAs share an SM (multi-wave
+// grids: the second CTA's loads and MMAs cover the first one's epilogue).
+template <typename TA, typename TB, int BN, bool SHALLOW = false>
 struct KKShape {
   using TileA = pipe::KTile<TA, 128>;
   using TileB = pipe::KTile<TB, BN>;  // f32: hi rows [0,BN) then lo rows [BN,2BN) -- one 2BN-row tile
   static constexpr bool A_LO = sizeof(TA) == 4;
   static constexpr bool B_LO = sizeof(TB) == 4;
   static constexpr int STAGE = TileA::BYTES + TileB::BYTES;
-  static constexpr int NS = pipe::stages_for(STAGE);
+  static constexpr int NS_DEEP = pipe::stages_for(STAGE);
+  static constexpr int NS_2 = (112 * 1024) / STAGE < 2 ? 2 : (112 * 1024) / STAGE;
+  static constexpr int NS = SHALLOW ? (NS_2 < NS_DEEP ? NS_2 : NS_DEEP) : NS_DEEP;
   static_assert(NS >= 2, "tile too large for a 2-stage pipeline");
   static constexpr int SMEM = NS * STAGE + 1024;
   static constexpr int ACC_COLS = B_LO ? 2 * BN : BN;
   static constexpr int TMEM_COLS = TmemCols<ACC_COLS>::V;
 };
 
-template <typename TA, typename TB, int BN, int MODE>
+template <typename TA, typename TB, int BN, int MODE, bool SHALLOW = false>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_kk_ws_kernel(Seg A, Seg B, int M, int N, int K, int kc, TcEpiArgs epi) {
-  using S = KKShape<TA, TB, BN>;
+  using S = KKShape<TA, TB, BN, SHALLOW>;
   static_assert(!S::B_LO || 2 * BN <= 256, "N-concatenated tile exceeds the MMA N limit");
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t ready[pipe::kMaxStages], done[pipe::kMaxStages], acc_bar;
