@@ -210,6 +210,37 @@ int ga3c_compute_returns_dev(ga3c_ctx* c, const double* d_rewards, const int32_t
                              int n_seg, const uint8_t* d_terminal, const double* d_bootstrap,
                              double gamma, double* d_out);
 
+/* -------------------------------------------------------- frame store */
+/* Device-resident 4-frame stacks.  The reference's
+ * PredictionRequest carries the whole stacked state (pipeline.hpp:23-27);
+ * here an agent sends only its NEWEST frame (in_h x in_w bytes) and the
+ * store shifts it into that agent's stack on the device (channel 0 = oldest
+ * frame, 3 = newest; an episode start -- reset or the agent's first push --
+ * repeats the frame four times).  Each agent's last `history` stacked states
+ * stay on the device, so training gathers its experiences from there instead
+ * of copying them to the GPU a second time (the TrainingQueue's
+ * Experience.state, returns.hpp:13-19).  Needs in_c == 4. */
+typedef struct ga3c_frames ga3c_frames;
+ga3c_frames* ga3c_frames_create(ga3c_model* m, int n_agents, int history, int* status);
+void ga3c_frames_destroy(ga3c_frames* f);
+/* Predictor call (predictor_loop pipeline.cpp:65-93 with the frame push):
+ * push new_frames[n][in_h*in_w] for agents[n] (resets nullable), forward the
+ * n new stacked states on snapshot `slot` (-1 = latest) and return pi / v as
+ * in ga3c_forward_u8.  state_slots (nullable, n) receives where each new
+ * state is stored -- the handle training uses. */
+int ga3c_predict_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* new_frames,
+                        const int32_t* agents, const uint8_t* resets, int n, int32_t* state_slots,
+                        float* pi, float* v, uint64_t* version_used);
+/* Trainer call: as ga3c_loss_grad_segments_u8, with sample b's state read
+ * from the store at (agents[b], state_slots[b]) on the device. */
+int ga3c_train_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const int32_t* agents,
+                      const int32_t* state_slots, int B, const int32_t* actions, const double* rewards,
+                      const int32_t* seg_offsets, int n_seg, const uint8_t* terminal,
+                      const double* bootstrap, double gamma, int apply_clip, double* scalars,
+                      double* returns_out);
+/* Copy one stored stacked state to the host (tests, debugging). */
+int ga3c_frames_read(ga3c_frames* f, int agent, int state_slot, uint8_t* state);
+
 /* ------------------------------------------------------ timing probe */
 /* Kernel classes for the roofline probe. */
 #define GA3C_K_NONE 0

@@ -150,6 +150,13 @@ _SIGS = {
     "ga3c_ctx_graph_launch": (C.c_int, [_P, C.c_int]),
     "ga3c_ctx_kernel_time": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
     "ga3c_ctx_timeline": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _P, C.POINTER(C.c_int)]),
+    "ga3c_frames_create": (_P, [_P, C.c_int, C.c_int, C.POINTER(C.c_int)]),
+    "ga3c_frames_destroy": (None, [_P]),
+    "ga3c_predict_frames": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_int, _P, _P, _P,
+                                      C.POINTER(C.c_uint64)]),
+    "ga3c_train_frames": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, _P, _P, _P, C.c_int, _P, _P, C.c_double,
+                                    C.c_int, _P, _P]),
+    "ga3c_frames_read": (C.c_int, [_P, C.c_int, C.c_int, _P]),
 }
 
 K_TAGS = {"none": 0, "conv_fwd": 1, "fc_fwd": 2, "heads": 3, "loss_bwd": 4, "wgrad": 5, "dgrad": 6,
@@ -218,6 +225,8 @@ class Model:
             check(st.value, lib.ga3c_model_last_error(None).decode())
         self.P = int(lib.ga3c_model_param_count(self.h))
         self.device = device
+        self.n_actions = spec.n_actions
+        self.input_dim = int(spec.in_h) * int(spec.in_w) * int(spec.in_c)
 
     def close(self):
         if getattr(self, "h", None):
@@ -434,3 +443,67 @@ class Context:
         v = C.c_uint64(0)
         check(lib.ga3c_ctx_read_dev_version(self.h, C.byref(v)), self.model.error())
         return v.value
+
+
+class Frames:
+    """Device frame-stack store (ga3c_frames_*): agents push their newest
+    frame; stacked states stay on the device for prediction and training."""
+
+    def __init__(self, model: Model, n_agents: int, history: int):
+        st = C.c_int(0)
+        self.h = lib.ga3c_frames_create(model.h, n_agents, history, C.byref(st))
+        if not self.h:
+            check(st.value or 3, model.error())
+        self.model = model
+        self.n_agents, self.history = n_agents, history
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.ga3c_frames_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def read(self, agent: int, slot: int):
+        import numpy as np
+        out = np.empty(self.model.input_dim, np.uint8)
+        check(lib.ga3c_frames_read(self.h, agent, slot, out.ctypes.data))
+        return out
+
+
+def predict_frames(ctx: "Context", frames: Frames, new_frames, agents, resets=None, slot=-1):
+    """-> (pi [n][A], v [n], state_slots [n], version)."""
+    import numpy as np
+    nf = np.ascontiguousarray(new_frames, np.uint8)
+    ag = np.ascontiguousarray(agents, np.int32)
+    n = len(ag)
+    rs = None if resets is None else np.ascontiguousarray(resets, np.uint8)
+    pi = np.empty((n, ctx.model.n_actions), np.float32)
+    v = np.empty(n, np.float32)
+    slots = np.empty(n, np.int32)
+    ver = C.c_uint64(0)
+    check(lib.ga3c_predict_frames(ctx.h, slot, frames.h, nf.ctypes.data, ag.ctypes.data,
+                                  None if rs is None else rs.ctypes.data, n, slots.ctypes.data, pi.ctypes.data,
+                                  v.ctypes.data, C.byref(ver)), ctx.model.error())
+    return pi, v, slots, ver.value
+
+
+def train_frames(ctx: "Context", frames: Frames, agents, state_slots, actions, rewards, seg_offsets, terminal,
+                 bootstrap, gamma, apply_clip=True, slot=-1):
+    """-> (scalars [3], returns [B])."""
+    import numpy as np
+    ag = np.ascontiguousarray(agents, np.int32)
+    sl = np.ascontiguousarray(state_slots, np.int32)
+    ac = np.ascontiguousarray(actions, np.int32)
+    rw = np.ascontiguousarray(rewards, np.float64)
+    off = np.ascontiguousarray(seg_offsets, np.int32)
+    te = np.ascontiguousarray(terminal, np.uint8)
+    bo = np.ascontiguousarray(bootstrap, np.float64)
+    B = len(ag)
+    sc = np.empty(3)
+    rets = np.empty(B)
+    check(lib.ga3c_train_frames(ctx.h, slot, frames.h, ag.ctypes.data, sl.ctypes.data, B, ac.ctypes.data,
+                                rw.ctypes.data, off.ctypes.data, len(off) - 1, te.ctypes.data, bo.ctypes.data,
+                                gamma, 1 if apply_clip else 0, sc.ctypes.data, rets.ctypes.data), ctx.model.error())
+    return sc, rets

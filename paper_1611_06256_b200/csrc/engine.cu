@@ -114,6 +114,8 @@ struct ga3c_ctx {
   double* r_out = nullptr;
   std::size_t r_cap = 0, r_seg_cap = 0;
   int* h_flag = nullptr;  // pinned
+  int32_t* f_idx = nullptr;  // frame-store index staging
+  std::size_t f_idx_cap = 0;
   std::uint64_t launches = 0;
   std::string last_error;
   // kernel timing probe (ga3c_ctx_time_kernel)
@@ -124,6 +126,15 @@ struct ga3c_ctx {
   // captured CUDA graphs of device-resident step sequences
   std::vector<cudaGraphExec_t> graphs;
   bool capturing = false;
+};
+
+struct ga3c_frames {
+  ga3c_model* m = nullptr;
+  int n_agents = 0, history = 0;
+  std::size_t frame_px = 0;   // bytes of one frame (in_h * in_w)
+  uint8_t* ring = nullptr;    // [agent][history][in_h][in_w][4] u8 stacked states
+  std::mutex mu;              // guards count (pushes per agent)
+  std::vector<long long> count;
 };
 
 namespace {
@@ -838,6 +849,60 @@ int run_loss_grad(ga3c_ctx* c, const float* theta, const void* d_in, bool u8, co
   return GA3C_OK;
 }
 
+// Frame store kernels.  A stacked pixel is one u32 (4 frames, oldest in the
+// low byte); pushing shifts the oldest out and the new frame in, or fills
+// all four with the new frame at an episode start.
+//   idx = [agent | source slot | destination slot | reset] x n
+__global__ void frames_push_kernel(uint32_t* __restrict__ ring, std::size_t px, int H,
+                                   const uint32_t* __restrict__ newf, const int32_t* __restrict__ idx, int n,
+                                   uint32_t* __restrict__ dense) {
+  pdl_enter();
+  const int i = blockIdx.y;
+  const std::size_t q = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // 4 pixels
+  if (q * 4 >= px) return;
+  const int a = idx[i], src = idx[n + i], dst = idx[2 * n + i];
+  const bool rst = idx[3 * n + i] != 0;
+  const uint32_t f4 = newf[(static_cast<std::size_t>(i) * px) / 4 + q];
+  const std::size_t so = ((static_cast<std::size_t>(a) * H + src) * px) + 4 * q;
+  const std::size_t d0 = ((static_cast<std::size_t>(a) * H + dst) * px) + 4 * q;
+  const uint4 old = *reinterpret_cast<const uint4*>(ring + so);
+  const uint32_t o[4] = {old.x, old.y, old.z, old.w};
+  uint32_t r[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t fb = (f4 >> (8 * j)) & 0xFFu;
+    r[j] = rst ? fb * 0x01010101u : (o[j] >> 8) | (fb << 24);
+  }
+  const uint4 w = make_uint4(r[0], r[1], r[2], r[3]);
+  *reinterpret_cast<uint4*>(ring + d0) = w;
+  if (dense) *reinterpret_cast<uint4*>(dense + static_cast<std::size_t>(i) * px + 4 * q) = w;
+}
+
+//   idx = [agent | slot] x B  ->  dense [B][state]
+__global__ void frames_gather_kernel(const uint32_t* __restrict__ ring, std::size_t px, int H,
+                                     const int32_t* __restrict__ idx, int B, uint32_t* __restrict__ out) {
+  pdl_enter();
+  const int b = blockIdx.y;
+  const std::size_t q = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q * 4 >= px) return;
+  const std::size_t so = ((static_cast<std::size_t>(idx[b]) * H + idx[B + b]) * px) + 4 * q;
+  *reinterpret_cast<uint4*>(out + static_cast<std::size_t>(b) * px + 4 * q) =
+      *reinterpret_cast<const uint4*>(ring + so);
+}
+
+int frames_idx_reserve(ga3c_ctx* c, std::size_t n) {
+  if (n <= c->f_idx_cap) return 0;
+  cudaStreamSynchronize(c->stream);
+  cudaFree(c->f_idx);
+  c->f_idx = nullptr;
+  c->f_idx_cap = std::max<std::size_t>(n, 1024);
+  if (cudaMalloc(&c->f_idx, c->f_idx_cap * sizeof(int32_t)) != cudaSuccess) {
+    c->f_idx_cap = 0;
+    return 1;
+  }
+  return 0;
+}
+
 void launch_rmsprop(ga3c_ctx* c, const Slot& src, const Slot& dst, unsigned long long* ver) {
   const ga3c_hyper& hp = c->m->hp;
   const std::size_t n = c->m->lo.total;
@@ -1146,7 +1211,7 @@ void ga3c_ctx_destroy(ga3c_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   void* ps[] = {c->d_in, c->hin, c->pi32, c->pi64, c->v, c->v64, c->dhead, c->dhT, c->scal,
                 c->scal_sum, c->d_actions, c->d_rets, c->grad, c->flag, c->dev_version, c->part,
-                c->clip_part, c->r_rew, c->r_off, c->r_term, c->r_boot, c->r_out};
+                c->clip_part, c->r_rew, c->r_off, c->r_term, c->r_boot, c->r_out, c->f_idx};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (auto* a : c->act)
@@ -1596,11 +1661,14 @@ int ga3c_ctx_graph_launch(ga3c_ctx* c, int graph_id) {
 // Trainer step on host buffers with the n-step returns computed on the device
 // (returns.cpp:8-26 for every segment, then nnet.cpp:201-291): one upload,
 // returns_kernel -> loss/backward kernels on the context stream, scalars back.
+// `states` are host states copied to the context buffer, unless `dev_ready`
+// is set: then the u8 states already sit in c->d_in in stream order (the
+// frame store's gather).
 static int loss_grad_segments(ga3c_ctx* c, int slot, const void* states, bool u8, int B,
                               const int32_t* actions, const double* rewards, const int32_t* off,
                               int n_seg, const uint8_t* terminal, const double* bootstrap, double gamma,
-                              int apply_clip, double* scalars, double* returns_out) {
-  if (!c || B < 1 || B > c->max_batch || !states || !actions || !rewards || !off || n_seg < 1 ||
+                              int apply_clip, double* scalars, double* returns_out, bool dev_ready = false) {
+  if (!c || B < 1 || B > c->max_batch || (!states && !dev_ready) || !actions || !rewards || !off || n_seg < 1 ||
       !terminal || !bootstrap)
     return GA3C_INVALID_ARGUMENT;
   ga3c_model* m = c->m;
@@ -1615,7 +1683,7 @@ static int loss_grad_segments(ga3c_ctx* c, int slot, const void* states, bool u8
     if (actions[b] < 0 || actions[b] >= m->lo.n_actions) return GA3C_INVALID_ARGUMENT;
   }
   const std::size_t dim = m->lo.in_dim;
-  if (!u8 && !all_finite(static_cast<const float*>(states), dim * B)) return GA3C_NONFINITE_INPUT;
+  if (!dev_ready && !u8 && !all_finite(static_cast<const float*>(states), dim * B)) return GA3C_NONFINITE_INPUT;
   if (set_device(m)) return GA3C_CUDA_ERROR;
   if ((std::size_t)B > c->r_cap) {
     cudaFree(c->r_rew);
@@ -1638,7 +1706,7 @@ static int loss_grad_segments(ga3c_ctx* c, int slot, const void* states, bool u8
   if (pinned_here) ga3c_snapshot_acquire(m, &s, nullptr);
   int rc = GA3C_OK;
   const std::size_t bytes = dim * B * (u8 ? 1 : sizeof(float));
-  if (cudaMemcpyAsync(c->d_in, states, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+  if ((!dev_ready && cudaMemcpyAsync(c->d_in, states, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess) ||
       cudaMemcpyAsync(c->d_actions, actions, sizeof(int32_t) * B, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
       cudaMemcpyAsync(c->r_rew, rewards, sizeof(double) * B, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
       cudaMemcpyAsync(c->r_off, off, sizeof(int32_t) * (n_seg + 1), cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
@@ -1676,6 +1744,151 @@ int ga3c_loss_grad_segments_u8(ga3c_ctx* c, int slot, const uint8_t* frames, int
                                double* scalars, double* returns_out) {
   return loss_grad_segments(c, slot, frames, true, B, actions, rewards, seg_offsets, n_seg, terminal,
                             bootstrap, gamma, apply_clip, scalars, returns_out);
+}
+
+// ------------------------------------------------------ frame store
+// Device-resident frame stacks: the host sends each
+// agent's NEWEST frame (in_h x in_w bytes, 7 KB for 84x84) instead of the
+// whole stacked state; the store keeps every agent's last `history` stacked
+// states on the device, so the predictor reads its batch and the trainer
+// gathers its experiences without another host->device copy.
+
+int ga3c_predict_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* new_frames,
+                        const int32_t* agents, const uint8_t* resets, int n, int32_t* state_slots, float* pi,
+                        float* v, uint64_t* version_used) {
+  if (!c || !f || f->m != c->m || n < 0 || n > c->max_batch || (n > 0 && (!new_frames || !agents || !pi || !v)))
+    return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  std::vector<int32_t> idx(4 * static_cast<std::size_t>(n));
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    for (int i = 0; i < n; ++i) {
+      const int a = agents[i];
+      if (a < 0 || a >= f->n_agents) return GA3C_INVALID_ARGUMENT;
+    }
+    for (int i = 0; i < n; ++i) {
+      const int a = agents[i];
+      const bool rst = (resets && resets[i]) || f->count[a] == 0;
+      idx[i] = a;
+      idx[n + i] = static_cast<int32_t>((f->count[a] + f->history - 1) % f->history);  // source (latest) slot
+      idx[2 * n + i] = static_cast<int32_t>(f->count[a] % f->history);                 // destination slot
+      idx[3 * n + i] = rst ? 1 : 0;
+      f->count[a] += 1;
+      if (state_slots) state_slots[i] = idx[2 * n + i];
+    }
+  }
+  if (set_device(m)) return GA3C_CUDA_ERROR;
+  int s = slot;
+  uint64_t ver = 0;
+  const bool pinned_here = slot < 0;
+  if (pinned_here) {
+    ga3c_snapshot_acquire(m, &s, &ver);
+  } else {
+    if (slot >= (int)m->slots.size()) return GA3C_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(m->read_m);
+    ver = m->slots[slot].version;
+  }
+  int rc = GA3C_OK;
+  if (n > 0) {
+    if (frames_idx_reserve(c, 4 * n)) rc = GA3C_CUDA_ERROR;
+    // dense stacked states at d_in, the new frames right after them
+    uint8_t* dense = static_cast<uint8_t*>(c->d_in);
+    uint8_t* newf = dense + static_cast<std::size_t>(c->max_batch) * m->lo.in_dim;
+    if (!rc && (cudaMemcpyAsync(newf, new_frames, f->frame_px * n, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+                cudaMemcpyAsync(c->f_idx, idx.data(), sizeof(int32_t) * 4 * n, cudaMemcpyHostToDevice,
+                                c->stream) != cudaSuccess))
+      rc = GA3C_CUDA_ERROR;
+    if (!rc) {
+      {
+        Launch l(c, GA3C_K_OTHER, -1);
+        pdl_launch(c->cur, frames_push_kernel, dim3((unsigned)((f->frame_px / 4 + 255) / 256), n), dim3(256), 0,
+                   reinterpret_cast<uint32_t*>(f->ring), f->frame_px, f->history,
+                   reinterpret_cast<const uint32_t*>(newf), (const int32_t*)c->f_idx, n,
+                   reinterpret_cast<uint32_t*>(dense));
+      }
+      run_forward(c, m->slots[s].theta, dense, true, n);
+      const int A = m->lo.n_actions;
+      if (cudaMemcpyAsync(pi, c->pi32, sizeof(float) * n * A, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+          cudaMemcpyAsync(v, c->v, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+        rc = GA3C_CUDA_ERROR;
+    }
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+      rc = GA3C_CUDA_ERROR;
+      set_err(std::string("predict_frames: ") + cudaGetErrorString(e));
+    }
+  }
+  if (pinned_here) ga3c_snapshot_release(m, s);
+  if (version_used) *version_used = ver;
+  return rc;
+}
+
+int ga3c_train_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const int32_t* agents, const int32_t* state_slots,
+                      int B, const int32_t* actions, const double* rewards, const int32_t* seg_offsets, int n_seg,
+                      const uint8_t* terminal, const double* bootstrap, double gamma, int apply_clip,
+                      double* scalars, double* returns_out) {
+  if (!c || !f || f->m != c->m || B < 1 || B > c->max_batch || !agents || !state_slots) return GA3C_INVALID_ARGUMENT;
+  for (int b = 0; b < B; ++b)
+    if (agents[b] < 0 || agents[b] >= f->n_agents || state_slots[b] < 0 || state_slots[b] >= f->history)
+      return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  if (set_device(m)) return GA3C_CUDA_ERROR;
+  if (frames_idx_reserve(c, 2 * B)) return GA3C_CUDA_ERROR;
+  std::vector<int32_t> idx(2 * static_cast<std::size_t>(B));
+  std::copy(agents, agents + B, idx.begin());
+  std::copy(state_slots, state_slots + B, idx.begin() + B);
+  GA3C_CUDA(cudaMemcpyAsync(c->f_idx, idx.data(), sizeof(int32_t) * 2 * B, cudaMemcpyHostToDevice, c->stream));
+  {
+    Launch l(c, GA3C_K_OTHER, -1);
+    pdl_launch(c->cur, frames_gather_kernel, dim3((unsigned)((f->frame_px / 4 + 255) / 256), B), dim3(256), 0,
+               reinterpret_cast<const uint32_t*>(f->ring), f->frame_px, f->history, (const int32_t*)c->f_idx, B,
+               reinterpret_cast<uint32_t*>(c->d_in));
+  }
+  return loss_grad_segments(c, slot, nullptr, true, B, actions, rewards, seg_offsets, n_seg, terminal, bootstrap,
+                            gamma, apply_clip, scalars, returns_out, true);
+}
+
+ga3c_frames* ga3c_frames_create(ga3c_model* m, int n_agents, int history, int* status) {
+  auto fail = [&](int st) -> ga3c_frames* {
+    if (status) *status = st;
+    return nullptr;
+  };
+  if (!m || n_agents < 1 || history < 2) return fail(GA3C_INVALID_ARGUMENT);
+  if (m->spec.in_c != 4 || m->lo.in_dim % 16 != 0) return fail(GA3C_INVALID_ARGUMENT);  // 4-frame u8 stacks
+  if (set_device(m)) return fail(GA3C_CUDA_ERROR);
+  auto* f = new ga3c_frames();
+  f->m = m;
+  f->n_agents = n_agents;
+  f->history = history;
+  f->frame_px = static_cast<std::size_t>(m->spec.in_h) * m->spec.in_w;
+  f->count.assign(n_agents, 0);
+  const std::size_t bytes = static_cast<std::size_t>(n_agents) * history * m->lo.in_dim;
+  if (cudaMalloc(&f->ring, bytes) != cudaSuccess || cudaMemset(f->ring, 0, bytes) != cudaSuccess) {
+    cudaFree(f->ring);
+    delete f;
+    return fail(GA3C_OUT_OF_MEMORY);
+  }
+  if (status) *status = GA3C_OK;
+  return f;
+}
+
+void ga3c_frames_destroy(ga3c_frames* f) {
+  if (!f) return;
+  cudaSetDevice(f->m->device);
+  cudaFree(f->ring);
+  delete f;
+}
+
+int ga3c_frames_read(ga3c_frames* f, int agent, int state_slot, uint8_t* state) {
+  if (!f || agent < 0 || agent >= f->n_agents || state_slot < 0 || state_slot >= f->history || !state)
+    return GA3C_INVALID_ARGUMENT;
+  if (set_device(f->m)) return GA3C_CUDA_ERROR;
+  const std::size_t dim = f->m->lo.in_dim;
+  const cudaError_t e = cudaMemcpy(state, f->ring + (static_cast<std::size_t>(agent) * f->history + state_slot) * dim,
+                                   dim, cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? GA3C_OK : GA3C_CUDA_ERROR;
 }
 
 int ga3c_loss_grad_segments_f32(ga3c_ctx* c, int slot, const float* states, int B,

@@ -1,0 +1,86 @@
+"""Device frame-stack store (include/ga3c.h ga3c_frames_*, SURVEY.md §8f row
+1): agents push only their newest frame; the stacked state must equal the
+one the host would build (4 frames, oldest first, an episode start repeats
+the frame), and predicting / training from the store must give exactly what
+ga3c_forward_u8 / ga3c_loss_grad_segments_u8 give on those host states."""
+import numpy as np
+import pytest
+
+import pyoracle as O
+
+pytestmark = pytest.mark.gpu
+
+H, W = 84, 84
+
+
+def setup(n_agents=6, history=7, max_batch=64):
+    import ctypes as C
+    from paper_1611_06256_b200 import _abi
+    spec = _abi.NetSpec()
+    C.memmove(C.byref(spec), C.byref(O.dnn_a()), C.sizeof(spec))
+    m = _abi.Model(spec, _abi.default_hyper())
+    th = np.zeros(m.P, np.float32)
+    _abi.check(_abi.lib.ga3c_init_params(spec, 3, None, th.ctypes.data))
+    m.load(th)
+    ctx = _abi.Context(m, max_batch)
+    fr = _abi.Frames(m, n_agents, history)
+    return _abi, m, ctx, fr
+
+
+def host_stack(prev, f, reset):
+    if prev is None or reset:
+        return np.repeat(f[:, :, None], 4, axis=2)
+    return np.concatenate([prev[:, :, 1:], f[:, :, None]], axis=2)
+
+
+def test_push_builds_stacks_and_predicts_like_forward_u8():
+    _abi, m, ctx, fr = setup()
+    rng = np.random.default_rng(0)
+    stacks = {}
+    for step in range(9):
+        agents = rng.permutation(6)[: rng.integers(1, 7)].astype(np.int32)
+        new = rng.integers(0, 256, (len(agents), H, W), dtype=np.uint8)
+        resets = (rng.random(len(agents)) < 0.2).astype(np.uint8)
+        pi, v, slots, _ = _abi.predict_frames(ctx, fr, new.reshape(len(agents), -1), agents, resets)
+        states = []
+        for i, a in enumerate(agents):
+            stacks[a] = host_stack(stacks.get(a), new[i], resets[i])
+            states.append(stacks[a].reshape(-1))
+            assert np.array_equal(fr.read(int(a), int(slots[i])), stacks[a].reshape(-1))
+        pi2, v2 = ctx.forward(np.stack(states))[:2]
+        assert np.array_equal(pi, pi2) and np.array_equal(v, v2)
+
+
+def test_train_from_store_matches_host_states_bitwise():
+    _abi, m, ctx, fr = setup(n_agents=4, history=7)
+    rng = np.random.default_rng(1)
+    T = 5
+    slots = np.zeros((4, T), np.int32)
+    states = np.zeros((4, T, H * W * 4), np.uint8)
+    stacks = {}
+    for t in range(T):
+        new = rng.integers(0, 256, (4, H, W), dtype=np.uint8)
+        _, _, sl, _ = _abi.predict_frames(ctx, fr, new.reshape(4, -1), np.arange(4, dtype=np.int32))
+        slots[:, t] = sl
+        for a in range(4):
+            stacks[a] = host_stack(stacks.get(a), new[a], False)
+            states[a, t] = stacks[a].reshape(-1)
+    agents = np.repeat(np.arange(4, dtype=np.int32), T)
+    acts = rng.integers(0, 6, 4 * T).astype(np.int32)
+    rew = rng.standard_normal(4 * T)
+    off = np.arange(0, 4 * T + 1, T, dtype=np.int32)
+    term = np.array([0, 1, 0, 0], np.uint8)
+    boot = rng.standard_normal(4)
+    sc1, r1 = _abi.train_frames(ctx, fr, agents, slots.reshape(-1), acts, rew, off, term, boot, 0.99)
+    g1 = ctx.read_grad()[0].copy()
+    sc2, r2 = ctx.loss_grad_segments(states.reshape(4 * T, -1), acts, rew, off, term, boot, 0.99)[:2]
+    g2 = ctx.read_grad()[0]
+    assert np.array_equal(r1, r2) and np.array_equal(sc1, sc2) and np.array_equal(g1, g2)
+
+
+def test_frames_validation():
+    _abi, m, ctx, fr = setup(n_agents=2, history=3)
+    with pytest.raises(ValueError):
+        _abi.predict_frames(ctx, fr, np.zeros((1, H * W), np.uint8), np.array([5], np.int32))
+    with pytest.raises(ValueError):
+        _abi.train_frames(ctx, fr, [0], [9], [0], [0.0], [0, 1], [1], [0.0], 0.99)
