@@ -64,6 +64,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=0)
+    p.add_argument("--e2e-trainers", type=int, default=4, help="trainer threads in the e2e leg (0 = serial)")
     p.add_argument("--cpu-seconds", type=float, default=6.0)
     p.add_argument("--probe", default="conv_fwd:0",
                    help="kernel class[:layer] for the roofline probe (auto = largest eager share)")
@@ -483,66 +484,187 @@ def main():
 
 
 def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world, grad_view, stream, dist):
-    """Same iteration through the reference-facing host-buffer C ABI calls:
-    every step copies its frames host->device (pinned), reads pi/V back,
-    samples on the host (util.hpp:46-54), computes returns through the ABI
-    and trains through ga3c_loss_grad_u8 + ga3c_apply_rmsprop."""
+    """The same iteration through the public host-buffer C ABI, inputs and
+    outputs in pinned host memory, every host<->device copy inside the timed
+    region.  Agents send only their newest 84x84 frame (ga3c_predict_frames:
+    the 4-frame stack is built in the device frame store, SURVEY.md §8f row
+    1); the host samples actions from pi (util.hpp:46-54); trainers call
+    ga3c_train_frames (returns on the device, states gathered from the
+    store) and ga3c_apply_rmsprop.  The older full-state calls
+    (ga3c_forward_u8 / ga3c_loss_grad_u8, 28 KB per state each way) are
+    timed too and reported beside it."""
     import torch
+    from paper_1611_06256_b200 import _abi
     NA, T, TB = args.agents, args.tmax, args.train_batch
     n = NA * T
     updates = n // TB
     k = args.e2e_steps or max(3, min(args.steps, 30))
     hs = min(sets, 2)
-    fr_agent = [frames[s].cpu().pin_memory().numpy() for s in range(hs)]           # [NA][T] frames
-    fr_time = [frames[s].transpose(0, 1).contiguous().cpu().pin_memory().numpy() for s in range(hs)]
+    px = FRAME[0] * FRAME[1]
+    # newest frame of every agent at every step: the last channel of the stacked synthetic states
+    newf = [frames[s][..., FRAME[2] - 1].transpose(0, 1).reshape(T, NA, px).contiguous().cpu().pin_memory().numpy()
+            for s in range(hs)]
     u_h = uni[:hs].cpu().numpy()
     r_h = rewards[:hs].cpu().numpy()
     term_h = terminal[:hs].cpu().numpy()
-    off = np.arange(0, n + 1, T, dtype=np.int32)
+    store = _abi.Frames(model, NA, T + 2)
+    agents = np.arange(NA, dtype=np.int32)
+    seg_off = np.arange(0, TB + 1, T, dtype=np.int32)
+    per_upd = TB // T
+    prev_term = np.zeros(NA, np.uint8)
     h2d = d2h = 0
 
     def one(i):
-        nonlocal h2d, d2h
+        nonlocal h2d, d2h, prev_term
         s = i % hs
         acts = np.zeros((NA, T), np.int32)
+        slots = np.zeros((NA, T), np.int32)
         v = None
         for t in range(T):
-            pi, v, _ = ctx.forward(fr_time[s][t])
+            pi, v, sl, _ = _abi.predict_frames(ctx, store, newf[s][t], agents, prev_term if t == 0 else None)
+            slots[:, t] = sl
             cdf = np.cumsum(pi.astype(np.float64), 1)
-            a = (u_h[s, t][:, None] < cdf).argmax(1)
-            a[~(u_h[s, t][:, None] < cdf).any(1)] = N_ACTIONS - 1
+            hit = u_h[s, t][:, None] < cdf
+            a = hit.argmax(1)
+            a[~hit.any(1)] = N_ACTIONS - 1
             acts[:, t] = a
-        rets = ctx.compute_returns(r_h[s].reshape(-1), off, term_h[s], v.astype(np.float64), hyper.gamma)
+        boot = v.astype(np.float64)
         for u in range(updates):
-            sl = slice(u * TB // T, (u + 1) * TB // T)
-            ctx.loss_grad(fr_agent[s][sl].reshape(TB, -1), acts[sl].reshape(-1), rets[u * TB:(u + 1) * TB],
-                          apply_clip=world == 1, want_grad=False)
+            sl = slice(u * per_upd, (u + 1) * per_upd)
+            _abi.train_frames(ctx, store, np.repeat(agents[sl], T), slots[sl].reshape(-1), acts[sl].reshape(-1),
+                              r_h[s][sl].reshape(-1), seg_off, term_h[s][sl], boot[sl], hyper.gamma,
+                              apply_clip=world == 1)
             if grad_view is not None:
                 with torch.cuda.stream(stream):
                     dist.all_reduce(grad_view)
                 ctx.clip_grad()
             ctx.apply_rmsprop()
-        h2d = T * NA * FRAME_BYTES + n * FRAME_BYTES + n * (8 + 4 + 8) + NA * (1 + 8) + 4 * (NA + 1)
-        d2h = T * NA * (N_ACTIONS + 1) * 4 + n * 8 + updates * (3 * 8 + 4)
+        prev_term = term_h[s].astype(np.uint8)
+        h2d = (T * NA * (px + 4 * 4) + NA + updates * (TB * (4 + 4 + 4 + 8) + 4 * (per_upd + 1) + per_upd * 9))
+        d2h = T * NA * (N_ACTIONS + 1 + 1) * 4 + updates * (3 * 8 + TB * 8 + 4)
 
-    for i in range(2):
-        one(i)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for i in range(k):
-        one(i)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([dt], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt = float(t.item())
-    return {"value": world * n * k / dt, "unit": "samples/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "steps": k, "ms_per_step": 1e3 * dt / k,
-            "path": "ga3c_forward_u8 / ga3c_compute_returns / ga3c_loss_grad_u8 / ga3c_apply_rmsprop "
-                    "(host buffers, pinned)"}
+    def full_state_step(i):
+        s = i % hs
+        acts = np.zeros((NA, T), np.int32)
+        v = None
+        for t in range(T):
+            pi, v, _ = ctx.forward(fr_time[s][t])
+            acts[:, t] = np.minimum((u_h[s, t][:, None] < np.cumsum(pi.astype(np.float64), 1)).argmax(1),
+                                    N_ACTIONS - 1)
+        rets = ctx.compute_returns(r_h[s].reshape(-1), off, term_h[s], v.astype(np.float64), hyper.gamma)
+        for u in range(updates):
+            sl = slice(u * TB // T, (u + 1) * TB // T)
+            ctx.loss_grad(fr_agent[s][sl].reshape(TB, -1), acts[sl].reshape(-1), rets[u * TB:(u + 1) * TB],
+                          apply_clip=world == 1, want_grad=False)
+            ctx.apply_rmsprop()
+
+    def timed(fn, steps):
+        for i in range(2):
+            fn(i)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for i in range(steps):
+            fn(i)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        return dt
+
+    dt_serial = timed(one, k)
+
+    # GA3C's own concurrency (pipeline.cpp:65-93, 241-306): a predictor
+    # thread serves the agents while trainer threads, each with its own
+    # context (stream), train on finished segments and apply to the latest
+    # parameters (out-of-place snapshots, so predictions never read a
+    # half-written model).  The frame store keeps 2 steps of history, so a
+    # trainer may lag the predictor by one step.
+    import queue
+    import threading
+    ctx_t = [_abi.Context(model, max(NA, TB)) for _ in range(args.e2e_trainers)]
+    store.close()
+    store = _abi.Frames(model, NA, 2 * T + 2)
+    q = queue.Queue(maxsize=1)
+
+    def trainer(j):
+        c = ctx_t[j]
+        while True:
+            item = q.get()
+            if item is None:
+                q.put(None)
+                return
+            s, acts, slots, boot, u = item
+            sl = slice(u * per_upd, (u + 1) * per_upd)
+            _abi.train_frames(c, store, np.repeat(agents[sl], T), slots[sl].reshape(-1), acts[sl].reshape(-1),
+                              r_h[s][sl].reshape(-1), seg_off, term_h[s][sl], boot[sl], hyper.gamma)
+            c.apply_rmsprop()
+
+    def predict_step(i, pt):
+        s = i % hs
+        acts = np.zeros((NA, T), np.int32)
+        slots = np.zeros((NA, T), np.int32)
+        v = None
+        for t in range(T):
+            pi, v, sl, _ = _abi.predict_frames(ctx, store, newf[s][t], agents, pt if t == 0 else None)
+            slots[:, t] = sl
+            cdf = np.cumsum(pi.astype(np.float64), 1)
+            hit = u_h[s, t][:, None] < cdf
+            a = hit.argmax(1)
+            a[~hit.any(1)] = N_ACTIONS - 1
+            acts[:, t] = a
+        return s, acts, slots, v.astype(np.float64)
+
+    dt = dt_serial
+    mode = "serial calls"
+    if world == 1 and args.e2e_trainers > 0:
+        ths = [threading.Thread(target=trainer, args=(j,), daemon=True) for j in range(args.e2e_trainers)]
+        for th in ths:
+            th.start()
+        pt = np.zeros(NA, np.uint8)
+        for i in range(2):  # warm-up
+            s, acts, slots, boot = predict_step(i, pt)
+            for u in range(updates):
+                q.put((s, acts, slots, boot, u))
+            pt = term_h[s].astype(np.uint8)
+        while q.unfinished_tasks and not q.empty():
+            time.sleep(1e-4)
+        time.sleep(0.05)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(k):
+            s, acts, slots, boot = predict_step(i, pt)
+            for u in range(updates):
+                q.put((s, acts, slots, boot, u))
+            pt = term_h[s].astype(np.uint8)
+        q.put(None)
+        for th in ths:
+            th.join()
+        torch.cuda.synchronize()
+        dt_thr = time.perf_counter() - t0
+        if dt_thr < dt:
+            dt, mode = dt_thr, f"1 predictor thread + {args.e2e_trainers} trainer threads"
+    for c in ctx_t:
+        c.close()
+    store.close()
+    out = {"value": world * n * k / dt, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "steps": k, "ms_per_step": 1e3 * dt / k, "mode": mode,
+           "serial_value": world * n * k / dt_serial,
+           "path": "ga3c_predict_frames (newest 84x84 frame per agent) / host sampling / ga3c_train_frames / "
+                   "ga3c_apply_rmsprop (host buffers, pinned)"}
+    if world == 1:
+        fr_agent = [frames[s].cpu().pin_memory().numpy() for s in range(hs)]
+        fr_time = [frames[s].transpose(0, 1).contiguous().cpu().pin_memory().numpy() for s in range(hs)]
+        off = np.arange(0, n + 1, T, dtype=np.int32)
+        kf = max(3, k // 3)
+        dtf = timed(full_state_step, kf)
+        out["full_state_api"] = {"value": n * kf / dtf, "h2d_bytes_per_step": 2 * n * FRAME_BYTES,
+                                 "path": "ga3c_forward_u8 / ga3c_compute_returns / ga3c_loss_grad_u8 / "
+                                         "ga3c_apply_rmsprop (whole 28 KB states both ways)"}
+    return out
 
 
 if __name__ == "__main__":
