@@ -65,6 +65,8 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=0)
     p.add_argument("--e2e-trainers", type=int, default=4, help="trainer threads in the e2e leg (0 = serial)")
+    p.add_argument("--trainers", type=int, default=3,
+                   help="trainer contexts in flight in the device step (N_T; N_T + 1 must divide the updates)")
     p.add_argument("--cpu-seconds", type=float, default=6.0)
     p.add_argument("--probe", default="conv_fwd:0",
                    help="kernel class[:layer] for the roofline probe (auto = largest eager share)")
@@ -246,6 +248,7 @@ def config_of(args, world, sets=None):
             "predictor_batch": args.agents, "min_train_batch": args.train_batch,
             "global_train_batch": args.train_batch * world, "updates_per_step": n // args.train_batch,
             "params": param_count(args.net), "parallelism": f"dp{world}",
+            "trainers_in_flight": args.trainers, "policy_lag_updates": args.trainers - 1,
             "l2": (f"inputs cycled over {sets} sets = {sets * n * FRAME_BYTES / 1e6:.0f} MB > 126 MB L2"
                    if sets else "n/a")}
 
@@ -315,17 +318,51 @@ def main():
     fstride = T * FRAME_BYTES
     lv = ctx.last_values_ptr()
 
+    # N_T trainers in flight (GA3C's trainer threads, pipeline.cpp:241-306):
+    # update u's gradient runs on trainer context u % N_T (its own stream and
+    # workspace) against parameter version u - (N_T - 1), the policy lag GA3C
+    # accepts; the RMSProp steps stay serialized in update order on the main
+    # stream and write out of place into a ring of N_T + 1 device slots, so a
+    # trainer never reads a version that is being overwritten.
+    NT = args.trainers
+    assert hyper.grad_clip_norm == 0.0 or NT == 1, "clipping with several trainers in flight is not wired here"
+    assert NT >= 1 and updates % (NT + 1) == 0 if NT > 1 else True, "N_T + 1 must divide the updates per step"
+    if NT > 1:
+        R = NT + 1
+        ring = model.ring(R)
+        tctx = [_abi.Context(model, TB) for _ in range(NT)]
+        tstream = [torch.cuda.ExternalStream(c.stream) for c in tctx]
+        tgrad = [dp.grad_view(c, P, f"cuda:{local}") for c in tctx] if world > 1 else None
+        ev_g = [torch.cuda.Event() for _ in range(updates)]
+        ev_a = [torch.cuda.Event() for _ in range(updates)]
+        ev_r = torch.cuda.Event()
+
     def step(i):
         s = i % sets
         fr = frames[s].data_ptr()
+        pslot = ring[0] if NT > 1 else slot
         for t in range(T):
-            ctx.forward_dev(fr + t * FRAME_BYTES, NA, True, slot=slot, stride=fstride)
+            ctx.forward_dev(fr + t * FRAME_BYTES, NA, True, slot=pslot, stride=fstride)
             ctx.sample_dev(uni[s, t].data_ptr(), NA, actions.data_ptr() + 4 * t, stride=T)
         ctx.compute_returns_dev(rewards[s].data_ptr(), offsets.data_ptr(), NA, terminal[s].data_ptr(), lv,
                                 hyper.gamma, rets.data_ptr())
-        for u in range(updates):  # data parallel: summed local gradient -> all-reduce -> RMSProp
-            dp.dp_update(ctx, fr + u * TB * FRAME_BYTES, True, actions.data_ptr() + 4 * u * TB,
-                         rets.data_ptr() + 8 * u * TB, TB, slot, grad_view, stream, world)
+        if NT == 1:
+            for u in range(updates):  # data parallel: summed local gradient -> all-reduce -> RMSProp
+                dp.dp_update(ctx, fr + u * TB * FRAME_BYTES, True, actions.data_ptr() + 4 * u * TB,
+                             rets.data_ptr() + 8 * u * TB, TB, slot, grad_view, stream, world)
+            return
+        ev_r.record(stream)
+        for u in range(updates):
+            j = u % NT
+            (ev_a[u - NT] if u >= NT else ev_r).wait(tstream[j])
+            tctx[j].loss_grad_dev(fr + u * TB * FRAME_BYTES, True, actions.data_ptr() + 4 * u * TB,
+                                  rets.data_ptr() + 8 * u * TB, TB, ring[(u - NT + 1) % R], apply_clip=world == 1)
+            ev_g[u].record(tstream[j])
+            ev_g[u].wait(stream)
+            if world > 1:  # default hyper: no clip, so nothing to do after the sum
+                dp.allreduce_sum_(tgrad[j], stream)
+            ctx.apply_slots_dev(tctx[j], ring[u % R], ring[(u + 1) % R])
+            ev_a[u].record(stream)
 
     def busy():
         # Park the stream behind a ~4 ms spin so the host can enqueue a whole

@@ -195,6 +195,17 @@ int ga3c_apply_rmsprop(ga3c_ctx* c, const float* dtheta, int* applied, uint64_t*
  * the context gradient, gated by the on-device non-finite flag; no host
  * synchronisation.  Only valid while no other thread reads the model. */
 int ga3c_apply_rmsprop_dev(ga3c_ctx* c);
+/* Device loop with several trainers in flight (GA3C's N_T trainer threads,
+ * pipeline.cpp:241-306, each on its own context and stream): n extra
+ * parameter slots, initialised from the latest snapshot and owned by the
+ * caller (never recycled), into which the loop applies out of place --
+ * update u reads slot ring[u % n] and writes ring[(u + 1) % n], so a
+ * trainer still reading an older version is never overwritten. */
+int ga3c_model_ring(ga3c_model* m, int n, int* slots_out);
+/* One RMSProp step from src_slot into dst_slot with the gradient and
+ * non-finite flag of context grad_from (NULL = c), stream-ordered on c's
+ * stream; the caller orders grad_from's stream before it.  Capturable. */
+int ga3c_apply_rmsprop_slots_dev(ga3c_ctx* c, const ga3c_ctx* grad_from, int src_slot, int dst_slot);
 /* On-device update counter of ga3c_apply_rmsprop_dev (blocking read). */
 int ga3c_ctx_read_dev_version(ga3c_ctx* c, uint64_t* version);
 

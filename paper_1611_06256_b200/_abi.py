@@ -150,6 +150,8 @@ _SIGS = {
     "ga3c_ctx_graph_launch": (C.c_int, [_P, C.c_int]),
     "ga3c_ctx_kernel_time": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
     "ga3c_ctx_timeline": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _P, C.POINTER(C.c_int)]),
+    "ga3c_model_ring": (C.c_int, [_P, C.c_int, _P]),
+    "ga3c_apply_rmsprop_slots_dev": (C.c_int, [_P, _P, C.c_int, C.c_int]),
     "ga3c_frames_create": (_P, [_P, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "ga3c_frames_destroy": (None, [_P]),
     "ga3c_predict_frames": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_int, _P, _P, _P,
@@ -254,6 +256,13 @@ class Model:
 
     def version(self):
         return int(lib.ga3c_model_version(self.h))
+
+    def ring(self, n):
+        """n caller-owned device slots for a multi-trainer device loop."""
+        import numpy as np
+        out = np.zeros(n, np.int32)
+        check(lib.ga3c_model_ring(self.h, n, out.ctypes.data), self.error())
+        return [int(x) for x in out]
 
     def acquire(self):
         s, v = C.c_int(0), C.c_uint64(0)
@@ -385,6 +394,10 @@ class Context:
     def loss_grad_dev(self, d_states, u8, d_actions, d_returns, B, slot, apply_clip=True, stride=0):
         check(lib.ga3c_loss_grad_dev(self.h, slot, d_states, int(u8), stride, d_actions, d_returns, B,
                                      int(apply_clip)), self.model.error())
+
+    def apply_slots_dev(self, grad_from, src_slot, dst_slot):
+        check(lib.ga3c_apply_rmsprop_slots_dev(self.h, grad_from.h if grad_from is not None else None, src_slot,
+                                               dst_slot), self.model.error())
 
     def apply_rmsprop_dev(self):
         check(lib.ga3c_apply_rmsprop_dev(self.h), self.model.error())

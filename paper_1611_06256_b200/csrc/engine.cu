@@ -903,7 +903,11 @@ int frames_idx_reserve(ga3c_ctx* c, std::size_t n) {
   return 0;
 }
 
-void launch_rmsprop(ga3c_ctx* c, const Slot& src, const Slot& dst, unsigned long long* ver) {
+// RMSProp from slot `src` into slot `dst` with the gradient (and its
+// non-finite flag) of context `g` (default: c itself), on c's stream.
+void launch_rmsprop(ga3c_ctx* c, const Slot& src, const Slot& dst, unsigned long long* ver,
+                    const ga3c_ctx* g = nullptr) {
+  if (!g) g = c;
   const ga3c_hyper& hp = c->m->hp;
   const std::size_t n = c->m->lo.total;
   const float alpha = static_cast<float>(hp.alpha);
@@ -912,8 +916,8 @@ void launch_rmsprop(ga3c_ctx* c, const Slot& src, const Slot& dst, unsigned long
   unsigned blocks = (unsigned)std::min<std::size_t>((n4 + 255) / 256, 8 * kNumSMs);
   if (blocks == 0) blocks = 1;
   Launch l(c, GA3C_K_RMSPROP, -1);
-  pdl_launch(c->cur, rmsprop_kernel, dim3(blocks), dim3(256), 0, src.theta, src.g, c->grad, dst.theta, dst.g, n,
-                                                c->flag, ver, alpha, oma, static_cast<float>(hp.eta),
+  pdl_launch(c->cur, rmsprop_kernel, dim3(blocks), dim3(256), 0, src.theta, src.g, (const float*)g->grad, dst.theta,
+             dst.g, n, (const int*)g->flag, ver, alpha, oma, static_cast<float>(hp.eta),
                                                 static_cast<float>(hp.eps_rms));
 }
 
@@ -1479,6 +1483,39 @@ int ga3c_apply_rmsprop_dev(ga3c_ctx* c) {
   auto set_err = [&](const std::string& e) { m->set_error(e); };
   Slot& s = m->slots[m->cur];
   launch_rmsprop(c, s, s, c->dev_version);
+  GA3C_CUDA(cudaGetLastError());
+  return GA3C_OK;
+}
+
+int ga3c_model_ring(ga3c_model* m, int n, int* slots_out) {
+  if (!m || n < 1 || !slots_out) return GA3C_INVALID_ARGUMENT;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  if (set_device(m)) return GA3C_CUDA_ERROR;
+  std::lock_guard<std::mutex> uk(m->update_m);
+  std::lock_guard<std::mutex> lk(m->read_m);
+  const Slot latest = m->slots[m->cur];
+  const std::size_t bytes = m->lo.total * sizeof(float);
+  for (int i = 0; i < n; ++i) {
+    Slot s;
+    GA3C_CUDA(cudaMalloc(&s.theta, bytes));
+    GA3C_CUDA(cudaMalloc(&s.g, bytes));
+    GA3C_CUDA(cudaMemcpy(s.theta, latest.theta, bytes, cudaMemcpyDeviceToDevice));
+    GA3C_CUDA(cudaMemcpy(s.g, latest.g, bytes, cudaMemcpyDeviceToDevice));
+    s.version = latest.version;
+    s.refs = 1;  // owned by the caller's device loop: never recycled
+    m->slots.push_back(s);
+    slots_out[i] = static_cast<int>(m->slots.size()) - 1;
+  }
+  return GA3C_OK;
+}
+
+int ga3c_apply_rmsprop_slots_dev(ga3c_ctx* c, const ga3c_ctx* grad_from, int src_slot, int dst_slot) {
+  if (!c || (grad_from && grad_from->m != c->m) || src_slot < 0 || dst_slot < 0 ||
+      src_slot >= (int)c->m->slots.size() || dst_slot >= (int)c->m->slots.size() || src_slot == dst_slot)
+    return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  launch_rmsprop(c, m->slots[src_slot], m->slots[dst_slot], c->dev_version, grad_from);
   GA3C_CUDA(cudaGetLastError());
   return GA3C_OK;
 }
