@@ -364,6 +364,22 @@ def main():
             ctx.apply_slots_dev(tctx[j], ring[u % R], ring[(u + 1) % R])
             ev_a[u].record(stream)
 
+    contexts = [ctx] + (tctx if NT > 1 else [])
+
+    def time_kernel(tag, li=-1):
+        for c in contexts:
+            c.time_kernel(tag, li)
+
+    def kernel_time():
+        ms = cnt = 0
+        for c in contexts:
+            a, b = c.kernel_time()
+            ms, cnt = ms + a, cnt + b
+        return ms, cnt
+
+    def launches_all():
+        return sum(c.launches() for c in contexts)
+
     def busy():
         # Park the stream behind a ~4 ms spin so the host can enqueue a whole
         # eager step before the GPU reaches it: the probed kernels then run
@@ -380,25 +396,25 @@ def main():
     probe_keys = sorted(work_per_step(args.net, NA, T, TB))
     for tag in ("conv_fwd", "fc_fwd", "heads", "loss_bwd", "wgrad", "dgrad", "splitk", "rmsprop",
                 "returns", "sample", "other"):
-        ctx.time_kernel(tag, -1)
+        time_kernel(tag, -1)
         busy()
         step(0)
-        ms, cnt = ctx.kernel_time()
+        ms, cnt = kernel_time()
         breakdown[tag] = round(ms, 4)
     for (tag, li) in probe_keys:
         if li >= 0:
-            ctx.time_kernel(tag, li)
+            time_kernel(tag, li)
             busy()
             step(0)
-            ms, cnt = ctx.kernel_time()
+            ms, cnt = kernel_time()
             breakdown[f"{tag}[{li}]"] = round(ms, 4)
-    ctx.time_kernel("none")
+    time_kernel("none")
     if args.timeline:
         ctx.time_kernel("all")
         busy()
         step(0)
         tl = ctx.timeline()
-        ctx.time_kernel("none")
+        time_kernel("none")
         with open(args.timeline, "w") as f:
             f.write("# one eager step, launches queued behind a spin; ms from the first launch\n")
             f.write("# start_ms end_ms dur_us stream kernel[layer]\n")
@@ -417,17 +433,17 @@ def main():
         # one CUDA graph per input set: the whole GA3C iteration replays as a
         # single launch (kernel timing probes are captured as event nodes)
         graphs = []
-        l_cap = ctx.launches()
+        l_cap = launches_all()
         for s in range(sets):
             ctx.graph_begin()
             step(s)
             graphs.append(ctx.graph_end())
-        launches_per_step = (ctx.launches() - l_cap) // sets
+        launches_per_step = (launches_all() - l_cap) // sets
         for s in range(sets):  # warm the instantiated graphs
             ctx.graph_launch(graphs[s])
         ctx.sync()
     else:
-        ctx.time_kernel(probe[0], probe[1])  # eager: probe inside the timed region
+        time_kernel(probe[0], probe[1])  # eager: probe inside the timed region
 
     # ---- timed region ----
     clocks = ClockSampler(local)
@@ -437,7 +453,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ctx.sync()
-    l0 = ctx.launches()
+    l0 = launches_all()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for i in range(args.steps):
@@ -448,7 +464,7 @@ def main():
     ev1.record(stream)
     ev1.synchronize()
     ctx.sync()
-    launches = ctx.launches() - l0
+    launches = launches_all() - l0
     if graphs is not None:
         launches = launches_per_step * args.steps
     ms_total = ev0.elapsed_time(ev1)
@@ -457,14 +473,14 @@ def main():
     if graphs is not None:
         # CUDA events cannot time kernels inside a graph replay: time the probed
         # kernel with events on its stream over K eager steps right after
-        ctx.time_kernel(probe[0], probe[1])
+        time_kernel(probe[0], probe[1])
         probe_steps = max(3, min(args.steps, 50))
         for i in range(probe_steps):
             busy()
             step(args.warmup + i)
             ctx.sync()
-    probe_ms, probe_n = ctx.kernel_time()
-    ctx.time_kernel("none")
+    probe_ms, probe_n = kernel_time()
+    time_kernel("none")
     if world > 1:
         t = torch.tensor([ms_total], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -482,7 +498,15 @@ def main():
     else:
         achieved = w / (probe_ms / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s"}
-    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": None,
+    traffic, traffic_src = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get(f"{probe[0]}[{probe[1]}]" if probe[1] >= 0 else probe[0])
+        if tr and args.net == "dnn_a":
+            traffic, traffic_src = tr["bytes_per_launch"], f"{tr['launch']}; {tr['capture']}"
+    except (OSError, ValueError, KeyError):
+        pass
+    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": traffic, "traffic_source": traffic_src,
                  "kernel": f"{probe[0]}[layer {probe[1]}]", "launches": probe_n,
                  "avg_launch_us": 1e3 * probe_ms / max(1, probe_n),
                  "share_of_step": probe_ms / (ms_step * probed_steps),

@@ -84,3 +84,22 @@ def test_frames_validation():
         _abi.predict_frames(ctx, fr, np.zeros((1, H * W), np.uint8), np.array([5], np.int32))
     with pytest.raises(ValueError):
         _abi.train_frames(ctx, fr, [0], [9], [0], [0.0], [0, 1], [1], [0.0], 0.99)
+
+
+def test_ring_apply_matches_published_apply():
+    """ga3c_model_ring + ga3c_apply_rmsprop_slots_dev (the multi-trainer
+    device loop) apply the same RMSProp step as ga3c_apply_rmsprop."""
+    _abi, m1, ctx1, _ = setup()
+    _, m2, ctx2, _ = setup()
+    rng = np.random.default_rng(3)
+    states = rng.integers(0, 256, (8, H * W * 4), dtype=np.uint8)
+    acts = rng.integers(0, 6, 8).astype(np.int32)
+    rets = rng.standard_normal(8)
+    d, _ = ctx1.loss_grad(states, acts, rets)
+    ring = m1.ring(2)
+    ctx1.apply_slots_dev(ctx1, ring[0], ring[1])
+    ctx1.sync()
+    pi1, v1, _ = ctx1.forward(states, slot=ring[1])
+    ctx2.apply_rmsprop(d)
+    pi2, v2, _ = ctx2.forward(states)
+    assert np.array_equal(pi1, pi2) and np.array_equal(v1, v2)
