@@ -35,6 +35,7 @@
 #include "tc_pipe.cuh"
 #include "tc_ws.cuh"
 #include "tc_bf16.cuh"
+#include "tc_dgrad.cuh"
 #include "pdl.cuh"
 
 using namespace ga3c;
@@ -653,9 +654,47 @@ bool fc_dgrad_tc(ga3c_ctx* c, int li, const Layer& L, const float* theta, const 
   return true;
 }
 
+// Conv input gradient on the tensor cores (tc_dgrad.cuh): s*s stride-phase
+// implicit GEMMs; false when the geometry needs the SIMT kernels.
+template <int BN, bool SHALLOW>
+void dgrad_tc_launch(ga3c_ctx* c, int li, const dg::DgradArgs& a, dim3 grid) {
+  using S = dg::DgShape<BN, SHALLOW>;
+  auto kern = dg::tc_dgrad_kernel<BN, SHALLOW>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
+    attr_set = true;
+  }
+  Launch l(c, GA3C_K_DGRAD, li);
+  pdl_launch(c->cur, kern, grid, dim3(ws::kThreads), S::SMEM, a);
+}
+
+bool conv_dgrad_tc(ga3c_ctx* c, int li, const Layer& L, const float* theta, const float* dout,
+                   const float* gate, float* din, int B) {
+  static const bool off = env_flag("GA3C_SIMT_DGRAD");
+  if (off || L.k % L.stride != 0 || L.cout % 32 != 0 || L.cin % 16 != 0 || L.cin > 128) return false;
+  const int T = L.k / L.stride;
+  if (T * T * L.cout / 32 < 1) return false;
+  dg::DgradArgs a{dout, theta + L.w_off, gate, din, B, L.ih, L.iw, L.cin, L.oh, L.ow, L.cout, L.k, L.stride, T};
+  const int bn = L.cin <= 16 ? 16 : (L.cin <= 32 ? 32 : (L.cin <= 64 ? 64 : 128));
+  const int a0 = (L.ih + L.stride - 1) / L.stride, b0 = (L.iw + L.stride - 1) / L.stride;
+  const long long m0 = static_cast<long long>(B) * a0 * b0;
+  const int ntiles = (L.cin + bn - 1) / bn;
+  dim3 grid(static_cast<unsigned>((m0 + 127) / 128), L.stride * L.stride, ntiles);
+  const bool shallow = static_cast<long long>(grid.x) * grid.y * grid.z > kNumSMs;
+  switch (bn) {
+    case 16: shallow ? dgrad_tc_launch<16, true>(c, li, a, grid) : dgrad_tc_launch<16, false>(c, li, a, grid); break;
+    case 32: shallow ? dgrad_tc_launch<32, true>(c, li, a, grid) : dgrad_tc_launch<32, false>(c, li, a, grid); break;
+    case 64: shallow ? dgrad_tc_launch<64, true>(c, li, a, grid) : dgrad_tc_launch<64, false>(c, li, a, grid); break;
+    default: shallow ? dgrad_tc_launch<128, true>(c, li, a, grid) : dgrad_tc_launch<128, false>(c, li, a, grid); break;
+  }
+  return true;
+}
+
 void layer_dgrad(ga3c_ctx* c, int li, const Layer& L, const float* theta, const float* dout,
                  const float* gate, float* din, int B, const float* doutT = nullptr) {
   if (!L.is_conv && doutT && fc_dgrad_tc(c, li, L, theta, doutT, c->ldT, gate, din, B)) return;
+  if (L.is_conv && conv_dgrad_tc(c, li, L, theta, dout, gate, din, B)) return;
   if (L.is_conv && L.cin % 16 == 0 && L.w_off % 4 == 0 && L.k == 4 && L.stride == 2 &&
       (L.cout == 32 || L.cout == 64)) {
     const int npix = B * L.ih * L.iw;
