@@ -70,6 +70,12 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=6.0)
     p.add_argument("--probe", default="conv_fwd:0",
                    help="kernel class[:layer] for the roofline probe (auto = largest eager share)")
+    p.add_argument("--trainer-sms", type=int, default=0,
+                   help="N_T > 1: SMs each trainer context's split-K plans fill (ga3c_ctx_set_sm_budget); "
+                        "0 = auto: a 1/N_T share when an update is latency-bound (< 50 MFLOP/sample), else all")
+    p.add_argument("--pred-sms", type=int, default=0, help="same for the predictor context (0 = all)")
+    p.add_argument("--no-overlap", action="store_true",
+                   help="N_T > 1: run the predictor phase before the trainers instead of beside them")
     p.add_argument("--no-graph", action="store_true", help="launch eagerly instead of CUDA graphs")
     p.add_argument("--timeline", default="", help="write a per-launch timeline of one eager step here")
     return p.parse_args()
@@ -249,6 +255,8 @@ def config_of(args, world, sets=None):
             "global_train_batch": args.train_batch * world, "updates_per_step": n // args.train_batch,
             "params": param_count(args.net), "parallelism": f"dp{world}",
             "trainers_in_flight": args.trainers, "policy_lag_updates": args.trainers - 1,
+            "predictor_trainer_overlap": args.trainers > 1 and not args.no_overlap,
+            "trainer_sm_budget": args.trainer_sms if args.trainers > 1 else 148,
             "l2": (f"inputs cycled over {sets} sets = {sets * n * FRAME_BYTES / 1e6:.0f} MB > 126 MB L2"
                    if sets else "n/a")}
 
@@ -307,8 +315,13 @@ def main():
     rewards = (torch.rand((sets, NA, T), dtype=torch.float64, device="cuda", generator=g) - 0.5) * 2
     terminal = (torch.rand((sets, NA), device="cuda", generator=g) < T / 64.0).to(torch.uint8)
     offsets = torch.arange(0, n + 1, T, dtype=torch.int32, device="cuda")
-    actions = torch.zeros((NA, T), dtype=torch.int32, device="cuda")
-    rets = torch.zeros((NA, T), dtype=torch.float64, device="cuda")
+    # double-buffered experience (actions, n-step returns): with several
+    # trainers in flight the predictor phase of step i overlaps the trainer
+    # phase, which consumes step i-1's experiences (GA3C's concurrent
+    # predictor and trainer threads decoupled by the training queue)
+    actions2 = torch.zeros((2, NA, T), dtype=torch.int32, device="cuda")
+    rets2 = torch.zeros((2, NA, T), dtype=torch.float64, device="cuda")
+    actions, rets = actions2[0], rets2[0]
     torch.cuda.synchronize()
     stream = torch.cuda.ExternalStream(ctx.stream)
 
@@ -316,7 +329,6 @@ def main():
     grad_view = dp.grad_view(ctx, P, f"cuda:{local}") if world > 1 else None
 
     fstride = T * FRAME_BYTES
-    lv = ctx.last_values_ptr()
 
     # N_T trainers in flight (GA3C's trainer threads, pipeline.cpp:241-306):
     # update u's gradient runs on trainer context u % N_T (its own stream and
@@ -327,44 +339,79 @@ def main():
     NT = args.trainers
     assert hyper.grad_clip_norm == 0.0 or NT == 1, "clipping with several trainers in flight is not wired here"
     assert NT >= 1 and updates % (NT + 1) == 0 if NT > 1 else True, "N_T + 1 must divide the updates per step"
+    overlap = NT > 1 and not args.no_overlap
     if NT > 1:
         R = NT + 1
-        ring = model.ring(R)
+        ring = model.ring(R + 1)  # + the predictor's slot, never written by a trainer
+        pred_slot = ring[R]
         tctx = [_abi.Context(model, TB) for _ in range(NT)]
         tstream = [torch.cuda.ExternalStream(c.stream) for c in tctx]
         tgrad = [dp.grad_view(c, P, f"cuda:{local}") for c in tctx] if world > 1 else None
         ev_g = [torch.cuda.Event() for _ in range(updates)]
         ev_a = [torch.cuda.Event() for _ in range(updates)]
         ev_r = torch.cuda.Event()
+        ev_p = torch.cuda.Event()
+        if args.trainer_sms == 0:
+            small = 2.5 * fwd_flops_per_sample(args.net) < 50e6
+            args.trainer_sms = 148 // NT if small else 148
+        for c in tctx:
+            c.set_sm_budget(args.trainer_sms)
+    pctx = _abi.Context(model, NA) if overlap else ctx
+    if overlap:
+        pctx.set_sm_budget(args.pred_sms)
+    pstream = torch.cuda.ExternalStream(pctx.stream) if overlap else stream
+    lv = pctx.last_values_ptr()
 
-    def step(i):
+    def predict(i, b):
+        """t_max predictor batches of N_A agents, sampling, n-step returns -> buffer b."""
         s = i % sets
         fr = frames[s].data_ptr()
-        pslot = ring[0] if NT > 1 else slot
+        pslot = pred_slot if NT > 1 else slot
+        acts, rts = actions2[b], rets2[b]
         for t in range(T):
-            ctx.forward_dev(fr + t * FRAME_BYTES, NA, True, slot=pslot, stride=fstride)
-            ctx.sample_dev(uni[s, t].data_ptr(), NA, actions.data_ptr() + 4 * t, stride=T)
-        ctx.compute_returns_dev(rewards[s].data_ptr(), offsets.data_ptr(), NA, terminal[s].data_ptr(), lv,
-                                hyper.gamma, rets.data_ptr())
+            pctx.forward_dev(fr + t * FRAME_BYTES, NA, True, slot=pslot, stride=fstride)
+            pctx.sample_dev(uni[s, t].data_ptr(), NA, acts.data_ptr() + 4 * t, stride=T)
+        pctx.compute_returns_dev(rewards[s].data_ptr(), offsets.data_ptr(), NA, terminal[s].data_ptr(), lv,
+                                 hyper.gamma, rts.data_ptr())
+
+    def step(i):
         if NT == 1:
+            predict(i, 0)
+            fr = frames[i % sets].data_ptr()
             for u in range(updates):  # data parallel: summed local gradient -> all-reduce -> RMSProp
                 dp.dp_update(ctx, fr + u * TB * FRAME_BYTES, True, actions.data_ptr() + 4 * u * TB,
                              rets.data_ptr() + 8 * u * TB, TB, slot, grad_view, stream, world)
             return
-        ev_r.record(stream)
+        if overlap:
+            # predictor branch (own context and stream) || trainers on the
+            # previous step's experiences
+            ev_r.record(stream)
+            ev_r.wait(pstream)
+            predict(i, i % 2)
+            ev_p.record(pstream)
+            ti, b = i - 1, (i - 1) % 2
+        else:
+            predict(i, 0)
+            ev_r.record(stream)
+            ti, b = i, 0
+        fr = frames[ti % sets].data_ptr()
+        acts, rts = actions2[b], rets2[b]
         for u in range(updates):
             j = u % NT
             (ev_a[u - NT] if u >= NT else ev_r).wait(tstream[j])
-            tctx[j].loss_grad_dev(fr + u * TB * FRAME_BYTES, True, actions.data_ptr() + 4 * u * TB,
-                                  rets.data_ptr() + 8 * u * TB, TB, ring[(u - NT + 1) % R], apply_clip=world == 1)
+            tctx[j].loss_grad_dev(fr + u * TB * FRAME_BYTES, True, acts.data_ptr() + 4 * u * TB,
+                                  rts.data_ptr() + 8 * u * TB, TB, ring[(u - NT + 1) % R], apply_clip=world == 1)
             ev_g[u].record(tstream[j])
             ev_g[u].wait(stream)
             if world > 1:  # default hyper: no clip, so nothing to do after the sum
                 dp.allreduce_sum_(tgrad[j], stream)
             ctx.apply_slots_dev(tctx[j], ring[u % R], ring[(u + 1) % R])
             ev_a[u].record(stream)
+        if overlap:
+            ev_p.wait(stream)  # the predictor is done reading its slot
+        ctx.copy_slot_dev(ring[updates % R], pred_slot)
 
-    contexts = [ctx] + (tctx if NT > 1 else [])
+    contexts = [ctx] + (tctx if NT > 1 else []) + ([pctx] if overlap else [])
 
     def time_kernel(tag, li=-1):
         for c in contexts:

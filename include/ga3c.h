@@ -206,6 +206,18 @@ int ga3c_model_ring(ga3c_model* m, int n, int* slots_out);
  * non-finite flag of context grad_from (NULL = c), stream-ordered on c's
  * stream; the caller orders grad_from's stream before it.  Capturable. */
 int ga3c_apply_rmsprop_slots_dev(ga3c_ctx* c, const ga3c_ctx* grad_from, int src_slot, int dst_slot);
+/* SMs this context's split-K plans try to fill (0 = all, or the
+ * GA3C_SPLIT_SMS environment variable).  With N_T trainer contexts in
+ * flight a share of the SMs per context costs less SM time per update
+ * (fewer, longer CTAs) than a full wave each.  Results do not change
+ * (every reduction is fixed-order for a given plan; parity tolerances hold
+ * for any plan). */
+int ga3c_ctx_set_sm_budget(ga3c_ctx* c, int sms);
+/* Copy parameter slot src_slot's theta and rms state into dst_slot,
+ * stream-ordered on c's stream (capturable): e.g. publish the last version of
+ * a device loop to a predictor-only slot that the trainers never write, so
+ * predictors and trainers run concurrently (GA3C, pipeline.hpp:87-91). */
+int ga3c_copy_slot_dev(ga3c_ctx* c, int src_slot, int dst_slot);
 /* On-device update counter of ga3c_apply_rmsprop_dev (blocking read). */
 int ga3c_ctx_read_dev_version(ga3c_ctx* c, uint64_t* version);
 

@@ -152,6 +152,8 @@ _SIGS = {
     "ga3c_ctx_timeline": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _P, C.POINTER(C.c_int)]),
     "ga3c_model_ring": (C.c_int, [_P, C.c_int, _P]),
     "ga3c_apply_rmsprop_slots_dev": (C.c_int, [_P, _P, C.c_int, C.c_int]),
+    "ga3c_copy_slot_dev": (C.c_int, [_P, C.c_int, C.c_int]),
+    "ga3c_ctx_set_sm_budget": (C.c_int, [_P, C.c_int]),
     "ga3c_frames_create": (_P, [_P, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "ga3c_frames_destroy": (None, [_P]),
     "ga3c_predict_frames": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_int, _P, _P, _P,
@@ -398,6 +400,12 @@ class Context:
     def apply_slots_dev(self, grad_from, src_slot, dst_slot):
         check(lib.ga3c_apply_rmsprop_slots_dev(self.h, grad_from.h if grad_from is not None else None, src_slot,
                                                dst_slot), self.model.error())
+
+    def set_sm_budget(self, sms):
+        check(lib.ga3c_ctx_set_sm_budget(self.h, sms), self.model.error())
+
+    def copy_slot_dev(self, src_slot, dst_slot):
+        check(lib.ga3c_copy_slot_dev(self.h, src_slot, dst_slot), self.model.error())
 
     def apply_rmsprop_dev(self):
         check(lib.ga3c_apply_rmsprop_dev(self.h), self.model.error())

@@ -87,6 +87,7 @@ struct ga3c_ctx {
   cudaEvent_t evs[16] = {};
   int ev_next = 0;
   int max_batch = 0;
+  int sms = 0;  // SMs a split-K plan fills (0 = GA3C_SPLIT_SMS or all)
   void* d_in = nullptr;
   float* act[GA3C_MAX_CONV + GA3C_MAX_HIDDEN] = {};
   float* dout[GA3C_MAX_CONV + GA3C_MAX_HIDDEN] = {};  // per-layer output gradient (backward DAG)
@@ -198,12 +199,14 @@ struct SplitPlan {
   int k_chunk = 0;
 };
 
-SplitPlan plan_splits(int M, int N, int K, bool allow_split) {
+int split_sms(const ga3c_ctx* c);
+
+SplitPlan plan_splits(const ga3c_ctx* c, int M, int N, int K, bool allow_split) {
   SplitPlan p;
   const int tiles = ((M + kBM - 1) / kBM) * ((N + kBN - 1) / kBN);
   int s = 1;
   if (allow_split) {
-    s = std::max(1, (2 * kNumSMs + tiles - 1) / tiles);
+    s = std::max(1, (2 * split_sms(c) + tiles - 1) / tiles);
     s = std::min(s, std::max(1, K / 128));
     while (s > 1 && static_cast<std::size_t>(s) * M * N > kRegionFloats) --s;
   }
@@ -232,6 +235,17 @@ bool env_flag(const char* name) {
 bool serial_bwd() {
   static const bool v = env_flag("GA3C_SERIAL_BWD");
   return v;
+}
+// SMs a split-K plan tries to fill (GA3C_SPLIT_SMS, default all 148): with
+// several trainer contexts in flight, fewer and longer CTAs per kernel cost
+// less SM time than one full wave each.
+int split_sms(const ga3c_ctx* c) {
+  static const int v = [] {
+    const char* e = std::getenv("GA3C_SPLIT_SMS");
+    const int n = e ? std::atoi(e) : 0;
+    return n > 0 ? n : kNumSMs;
+  }();
+  return c && c->sms > 0 ? c->sms : v;
 }
 bool no_cluster() {
   static const bool v = env_flag("GA3C_NO_CLUSTER");
@@ -427,7 +441,7 @@ bool u8_conv_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, co
   const int M = B * L.pixels();
   const int tiles = ((M + 127) / 128) * ((L.cout + bn - 1) / bn);
   const int chunks = L.in / 64;
-  int ks = no_cluster() ? 1 : std::max(1, std::min({8, chunks, kNumSMs / std::max(1, tiles)}));
+  int ks = no_cluster() ? 1 : std::max(1, std::min({8, chunks, split_sms(c) / std::max(1, tiles)}));
   const int kc = ((chunks + ks - 1) / ks) * 64;
   ks = (L.in + kc - 1) / kc;
   const bool shallow = tiles * ks > kNumSMs && ks == 1 && !env_flag("GA3C_DEEP_ONLY");
@@ -468,7 +482,7 @@ void conv_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const
       // partial tiles are summed through DSMEM in the epilogue.
       const int tiles = ((M + 127) / 128) * ((L.cout + bn - 1) / bn);
       const int chunks = L.in / 32;
-      int ks = no_cluster() ? 1 : std::max(1, std::min({8, chunks, kNumSMs / std::max(1, tiles)}));
+      int ks = no_cluster() ? 1 : std::max(1, std::min({8, chunks, split_sms(c) / std::max(1, tiles)}));
       const int kc = ((chunks + ks - 1) / ks) * 32;
       ks = (L.in + kc - 1) / kc;
       tc_dispatch<T, float, TC_EPI_BIAS_RELU>(c, GA3C_K_CONV_FWD, li, bn, A, W, M, L.cout, L.in, ks, kc, e);
@@ -480,7 +494,7 @@ void conv_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const
   DenseK w{theta + L.w_off, L.in};
   const int M = B * L.pixels();
   launch_gemm(c, GA3C_K_CONV_FWD, li, a, w, EpiBiasRelu{out, theta + L.b_off, L.cout}, M, L.cout,
-              L.in, plan_splits(M, L.cout, L.in, false));
+              L.in, plan_splits(c, M, L.cout, L.in, false));
 }
 
 // FC forward.  If `keep_partials` the split-K partials are left in c->part for
@@ -497,7 +511,7 @@ int fc_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const vo
       const int bn = tc_bn(B);
       const int tiles = ((L.out + 127) / 128) * ((B + bn - 1) / bn);
       const int chunks = L.in / 32;
-      int splits = std::max(1, std::min(chunks, kNumSMs / std::max(1, tiles)));
+      int splits = std::max(1, std::min(chunks, split_sms(c) / std::max(1, tiles)));
       while (splits > 1 && static_cast<std::size_t>(splits) * B * L.out > kRegionFloats) --splits;
       const int kc = ((chunks + splits - 1) / splits) * 32;
       splits = (L.in + kc - 1) / kc;
@@ -514,7 +528,7 @@ int fc_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const vo
   }
   DenseKIn<T> a{static_cast<const T*>(x), static_cast<int>(ld)};
   DenseK w{theta + L.w_off, L.in};
-  const SplitPlan p = plan_splits(B, L.out, L.in, true);
+  const SplitPlan p = plan_splits(c, B, L.out, L.in, true);
   if (keep_partials || p.splits > 1) {
     launch_gemm(c, GA3C_K_FC_FWD, li, a, w, EpiPartial{region(c, 0), B, L.out}, B, L.out, L.in, p);
     if (!keep_partials) {
@@ -542,7 +556,7 @@ void launch_splitk_grad(ga3c_ctx* c, int li, int splits, int M, int N, const Gra
 template <class LA, class LB>
 void wgrad_gemm(ga3c_ctx* c, int li, const LA& la, const LB& lb, const GradMap& gm, int M, int N,
                 int K, float* part) {
-  const SplitPlan p = plan_splits(M, N, K, true);
+  const SplitPlan p = plan_splits(c, M, N, K, true);
   if (p.splits == 1) {
     launch_gemm(c, GA3C_K_WGRAD, li, la, lb, EpiGrad{gm}, M, N, K, p);
   } else {
@@ -578,11 +592,20 @@ bool layer_wgrad_tc(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const
   if (!seg_ok(X, npix) || L.in % 32 != 0 || L.out % 4 != 0 || L.w_off % 4 != 0 ||
       (reinterpret_cast<uintptr_t>(dout) % 16) != 0)
     return false;
-  const int bn = L.out <= 32 ? 32 : (L.out <= 64 ? 64 : 128);
   const int mtiles = (L.in + 127) / 128;
-  const int ntiles = (L.out + bn - 1) / bn;
   const int chunks = (npix + 31) / 32;
-  int splits = std::max(1, std::min(chunks / 2, (kNumSMs + mtiles * ntiles - 1) / (mtiles * ntiles)));
+  // Narrowest N tile that still covers the outputs in one wave when the
+  // reduction is too short to split (FC at trainer batch sizes): more CTAs,
+  // each with a smaller epilogue.
+  int bn = L.out <= 32 ? 32 : (L.out <= 64 ? 64 : 128);
+  if (chunks < 4)
+    for (int cand = 32; cand < bn; cand *= 2)
+      if (mtiles * ((L.out + cand - 1) / cand) <= split_sms(c)) {
+        bn = cand;
+        break;
+      }
+  const int ntiles = (L.out + bn - 1) / bn;
+  int splits = std::max(1, std::min(chunks / 2, (split_sms(c) + mtiles * ntiles - 1) / (mtiles * ntiles)));
   while (splits > 1 && static_cast<std::size_t>(splits) * L.out * (L.in + 1) > kRegionFloats) --splits;
   const int kc = ((chunks + splits - 1) / splits) * 32;
   splits = (npix + kc - 1) / kc;
@@ -641,7 +664,7 @@ bool fc_dgrad_tc(ga3c_ctx* c, int li, const Layer& L, const float* theta, const 
   const int mtiles = (L.in + 127) / 128;
   const int chunks = (L.out + 31) / 32;
   static const bool no_mn = env_flag("GA3C_NO_CLUSTER_MN");
-  int ks = no_cluster() || no_mn ? 1 : std::max(1, std::min({8, chunks, kNumSMs / mtiles}));
+  int ks = no_cluster() || no_mn ? 1 : std::max(1, std::min({8, chunks, split_sms(c) / mtiles}));
   const int kc = ((chunks + ks - 1) / ks) * 32;
   ks = (L.out + kc - 1) / kc;
   WgradArgs a{W, doutT, ldT, B, L.in, L.out, kc, nullptr, GradMap{}, 0, 1, din, gate, L.in};
@@ -729,7 +752,7 @@ void layer_dgrad(ga3c_ctx* c, int li, const Layer& L, const float* theta, const 
     DenseK a{dout, L.out};
     DenseT w{theta + L.w_off, L.in};  // (n = i, k = o) -> W[o][i]
     launch_gemm(c, GA3C_K_DGRAD, li, a, w, EpiGate{din, gate, L.in}, B, L.in, L.out,
-                plan_splits(B, L.in, L.out, false));
+                plan_splits(c, B, L.in, L.out, false));
   }
 }
 
@@ -1556,6 +1579,27 @@ int ga3c_apply_rmsprop_slots_dev(ga3c_ctx* c, const ga3c_ctx* grad_from, int src
   auto set_err = [&](const std::string& e) { m->set_error(e); };
   launch_rmsprop(c, m->slots[src_slot], m->slots[dst_slot], c->dev_version, grad_from);
   GA3C_CUDA(cudaGetLastError());
+  return GA3C_OK;
+}
+
+int ga3c_ctx_set_sm_budget(ga3c_ctx* c, int sms) {
+  if (!c || sms < 0) return GA3C_INVALID_ARGUMENT;
+  c->sms = std::min(sms, kNumSMs);
+  return GA3C_OK;
+}
+
+int ga3c_copy_slot_dev(ga3c_ctx* c, int src_slot, int dst_slot) {
+  if (!c || src_slot < 0 || dst_slot < 0 || src_slot >= (int)c->m->slots.size() ||
+      dst_slot >= (int)c->m->slots.size())
+    return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  if (src_slot == dst_slot) return GA3C_OK;
+  const std::size_t bytes = m->lo.total * sizeof(float);
+  const Slot& s = m->slots[src_slot];
+  const Slot& d = m->slots[dst_slot];
+  GA3C_CUDA(cudaMemcpyAsync(d.theta, s.theta, bytes, cudaMemcpyDeviceToDevice, c->stream));
+  GA3C_CUDA(cudaMemcpyAsync(d.g, s.g, bytes, cudaMemcpyDeviceToDevice, c->stream));
   return GA3C_OK;
 }
 
