@@ -247,6 +247,26 @@ int split_sms(const ga3c_ctx* c) {
   }();
   return c && c->sms > 0 ? c->sms : v;
 }
+// Ring-depth cap (pipe::ring_depth) for a tensor-core launch whose CTAs
+// each stream `n` k-chunks: no deeper than n; at most ~112 KB (two CTAs per
+// SM) for multi-wave grids and for contexts sharing the GPU with other
+// contexts (an SM budget below all SMs); otherwise as deep as fits.
+int ring_cap(const ga3c_ctx* c, int n, long long ctas) {
+  static const bool deep_only = env_flag("GA3C_DEEP_ONLY");
+  if (deep_only) return 0;
+  if (n <= 2) return 2;
+  if (n == 3) return 3;
+  return (ctas > kNumSMs || split_sms(c) < kNumSMs) ? 1 : 0;
+}
+
+#define GA3C_CAP_SWITCH(cap, F) \
+  switch (cap) {                \
+    case 1: F(1); break;        \
+    case 2: F(2); break;        \
+    case 3: F(3); break;        \
+    default: F(0); break;       \
+  }
+
 bool no_cluster() {
   static const bool v = env_flag("GA3C_NO_CLUSTER");
   return v;
@@ -307,11 +327,11 @@ void launch_gemm(ga3c_ctx* c, int tag, int layer, const LA& la, const LB& lb, co
 
 // ------------------------------------------------------ tensor-core GEMMs
 
-template <typename TA, typename TB, int BN, int MODE, bool SHALLOW>
+template <typename TA, typename TB, int BN, int MODE, int CAP>
 void tc_launch_v(ga3c_ctx* c, int tag, int layer, const Seg& A, const Seg& B, int M, int N, int K, int splits,
                  int kc, const TcEpiArgs& epi) {
-  using S = ws::KKShape<TA, TB, BN, SHALLOW>;
-  auto kern = ws::tc_kk_ws_kernel<TA, TB, BN, MODE, SHALLOW>;
+  using S = ws::KKShape<TA, TB, BN, CAP>;
+  auto kern = ws::tc_kk_ws_kernel<TA, TB, BN, MODE, CAP>;
   static bool attr_set = false;  // idempotent; racing setters write the same value
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
@@ -326,16 +346,14 @@ void tc_launch_v(ga3c_ctx* c, int tag, int layer, const Seg& A, const Seg& B, in
     pdl_launch(c->cur, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, A, B, M, N, K, kc, epi);
 }
 
-// Grids of more than one wave get the shallow ring (two CTAs per SM).
 template <typename TA, typename TB, int BN, int MODE>
 void tc_launch(ga3c_ctx* c, int tag, int layer, const Seg& A, const Seg& B, int M, int N, int K, int splits,
                int kc, const TcEpiArgs& epi) {
-  static const bool deep_only = env_flag("GA3C_DEEP_ONLY");
   const long long ctas = static_cast<long long>((M + 127) / 128) * splits * ((N + BN - 1) / BN);
-  if (ctas > kNumSMs && splits == 1 && !deep_only)
-    tc_launch_v<TA, TB, BN, MODE, true>(c, tag, layer, A, B, M, N, K, splits, kc, epi);
-  else
-    tc_launch_v<TA, TB, BN, MODE, false>(c, tag, layer, A, B, M, N, K, splits, kc, epi);
+  const int cap = ring_cap(c, (std::min(kc, K) + 31) / 32, ctas);
+#define GA3C_F(C) tc_launch_v<TA, TB, BN, MODE, C>(c, tag, layer, A, B, M, N, K, splits, kc, epi)
+  GA3C_CAP_SWITCH(cap, GA3C_F)
+#undef GA3C_F
 }
 
 template <typename TA, typename TB, int MODE>
@@ -409,13 +427,13 @@ Im2col<T> im2col_of(const Layer& L, const void* x, long long bstride) {
   return g;
 }
 
-template <int BN, bool SHALLOW>
+template <int BN, int CAP>
 void u8_conv_launch(ga3c_ctx* c, int li, const Seg& A, const Seg& W, int M, int N, int K, int ks, int kc,
                     const TcEpiArgs& e) {
   using S = bf::U8Shape<BN>;
-  constexpr int NS = SHALLOW ? (S::NS_2 < S::NS_DEEP ? S::NS_2 : S::NS_DEEP) : S::NS_DEEP;
+  constexpr int NS = pipe::ring_depth(CAP, S::STAGE);
   constexpr int SMEM = NS * S::STAGE + 1024;
-  auto kern = bf::tc_u8_fwd_kernel<BN, SHALLOW>;
+  auto kern = bf::tc_u8_fwd_kernel<BN, CAP>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
@@ -444,20 +462,23 @@ bool u8_conv_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, co
   int ks = no_cluster() ? 1 : std::max(1, std::min({8, chunks, split_sms(c) / std::max(1, tiles)}));
   const int kc = ((chunks + ks - 1) / ks) * 64;
   ks = (L.in + kc - 1) / kc;
-  const bool shallow = tiles * ks > kNumSMs && ks == 1 && !env_flag("GA3C_DEEP_ONLY");
+  const int cap = ring_cap(c, (std::min(kc, L.in) + 63) / 64, static_cast<long long>(tiles) * ks);
   switch (bn) {
-    case 16:
-      shallow ? u8_conv_launch<16, true>(c, li, A, W, M, L.cout, L.in, ks, kc, e)
-              : u8_conv_launch<16, false>(c, li, A, W, M, L.cout, L.in, ks, kc, e);
-      break;
-    case 32:
-      shallow ? u8_conv_launch<32, true>(c, li, A, W, M, L.cout, L.in, ks, kc, e)
-              : u8_conv_launch<32, false>(c, li, A, W, M, L.cout, L.in, ks, kc, e);
-      break;
-    default:
-      shallow ? u8_conv_launch<64, true>(c, li, A, W, M, L.cout, L.in, ks, kc, e)
-              : u8_conv_launch<64, false>(c, li, A, W, M, L.cout, L.in, ks, kc, e);
-      break;
+    case 16: {
+#define GA3C_F(C) u8_conv_launch<16, C>(c, li, A, W, M, L.cout, L.in, ks, kc, e)
+      GA3C_CAP_SWITCH(cap, GA3C_F)
+#undef GA3C_F
+    } break;
+    case 32: {
+#define GA3C_F(C) u8_conv_launch<32, C>(c, li, A, W, M, L.cout, L.in, ks, kc, e)
+      GA3C_CAP_SWITCH(cap, GA3C_F)
+#undef GA3C_F
+    } break;
+    default: {
+#define GA3C_F(C) u8_conv_launch<64, C>(c, li, A, W, M, L.cout, L.in, ks, kc, e)
+      GA3C_CAP_SWITCH(cap, GA3C_F)
+#undef GA3C_F
+    } break;
   }
   return true;
 }
@@ -565,10 +586,10 @@ void wgrad_gemm(ga3c_ctx* c, int li, const LA& la, const LB& lb, const GradMap& 
   }
 }
 
-template <typename TX, int BN>
-void wgrad_tc_launch(ga3c_ctx* c, int li, const WgradArgs& a, dim3 grid, int tag = GA3C_K_WGRAD) {
-  using S = ws::MNShape<TX, BN>;
-  auto kern = ws::tc_mn_ws_kernel<TX, BN>;
+template <typename TX, int BN, int CAP>
+void wgrad_tc_launch_v(ga3c_ctx* c, int li, const WgradArgs& a, dim3 grid, int tag) {
+  using S = ws::MNShape<TX, BN, CAP>;
+  auto kern = ws::tc_mn_ws_kernel<TX, BN, CAP>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
@@ -579,6 +600,14 @@ void wgrad_tc_launch(ga3c_ctx* c, int li, const WgradArgs& a, dim3 grid, int tag
     pdl_launch_cluster(c->cur, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, dim3(1, grid.y, 1), a);
   else
     pdl_launch(c->cur, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, a);
+}
+
+template <typename TX, int BN>
+void wgrad_tc_launch(ga3c_ctx* c, int li, const WgradArgs& a, dim3 grid, int tag = GA3C_K_WGRAD) {
+  const int cap = ring_cap(c, (std::min(a.kc, a.npix) + 31) / 32, static_cast<long long>(grid.x) * grid.y * grid.z);
+#define GA3C_F(C) wgrad_tc_launch_v<TX, BN, C>(c, li, a, grid, tag)
+  GA3C_CAP_SWITCH(cap, GA3C_F)
+#undef GA3C_F
 }
 
 // Tensor-core weight gradient; returns false when the shape needs the SIMT path.
@@ -679,10 +708,10 @@ bool fc_dgrad_tc(ga3c_ctx* c, int li, const Layer& L, const float* theta, const 
 
 // Conv input gradient on the tensor cores (tc_dgrad.cuh): s*s stride-phase
 // implicit GEMMs; false when the geometry needs the SIMT kernels.
-template <int BN, bool SHALLOW>
+template <int BN, int CAP>
 void dgrad_tc_launch(ga3c_ctx* c, int li, const dg::DgradArgs& a, dim3 grid) {
-  using S = dg::DgShape<BN, SHALLOW>;
-  auto kern = dg::tc_dgrad_kernel<BN, SHALLOW>;
+  using S = dg::DgShape<BN, CAP>;
+  auto kern = dg::tc_dgrad_kernel<BN, CAP>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
@@ -704,12 +733,28 @@ bool conv_dgrad_tc(ga3c_ctx* c, int li, const Layer& L, const float* theta, cons
   const long long m0 = static_cast<long long>(B) * a0 * b0;
   const int ntiles = (L.cin + bn - 1) / bn;
   dim3 grid(static_cast<unsigned>((m0 + 127) / 128), L.stride * L.stride, ntiles);
-  const bool shallow = static_cast<long long>(grid.x) * grid.y * grid.z > kNumSMs;
+  const int cap = ring_cap(c, T * T * L.cout / 32, static_cast<long long>(grid.x) * grid.y * grid.z);
   switch (bn) {
-    case 16: shallow ? dgrad_tc_launch<16, true>(c, li, a, grid) : dgrad_tc_launch<16, false>(c, li, a, grid); break;
-    case 32: shallow ? dgrad_tc_launch<32, true>(c, li, a, grid) : dgrad_tc_launch<32, false>(c, li, a, grid); break;
-    case 64: shallow ? dgrad_tc_launch<64, true>(c, li, a, grid) : dgrad_tc_launch<64, false>(c, li, a, grid); break;
-    default: shallow ? dgrad_tc_launch<128, true>(c, li, a, grid) : dgrad_tc_launch<128, false>(c, li, a, grid); break;
+    case 16: {
+#define GA3C_F(C) dgrad_tc_launch<16, C>(c, li, a, grid)
+      GA3C_CAP_SWITCH(cap, GA3C_F)
+#undef GA3C_F
+    } break;
+    case 32: {
+#define GA3C_F(C) dgrad_tc_launch<32, C>(c, li, a, grid)
+      GA3C_CAP_SWITCH(cap, GA3C_F)
+#undef GA3C_F
+    } break;
+    case 64: {
+#define GA3C_F(C) dgrad_tc_launch<64, C>(c, li, a, grid)
+      GA3C_CAP_SWITCH(cap, GA3C_F)
+#undef GA3C_F
+    } break;
+    default: {
+#define GA3C_F(C) dgrad_tc_launch<128, C>(c, li, a, grid)
+      GA3C_CAP_SWITCH(cap, GA3C_F)
+#undef GA3C_F
+    } break;
   }
   return true;
 }

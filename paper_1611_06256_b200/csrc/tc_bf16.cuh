@@ -95,7 +95,6 @@ struct U8Shape {
   static constexpr int B_BYTES = 3 * BN * 128; // [hi; mid; lo] bf16 rows, SW128
   static constexpr int STAGE = A_STG + A_BYTES + B_STG + B_BYTES;
   static constexpr int NS_DEEP = pipe::stages_for(STAGE);
-  static constexpr int NS_2 = (112 * 1024) / STAGE < 2 ? 2 : (112 * 1024) / STAGE;
   static constexpr int ACC_COLS = 3 * BN;
   static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : (ACC_COLS <= 64 ? 64 : (ACC_COLS <= 128 ? 128 : 256));
   static constexpr int AU_PER = 128 * 8 / kProducers;  // 16-byte bf16 units per thread
@@ -106,11 +105,11 @@ struct U8Shape {
 // C[m][n] = ReLU(bias[n] + (1/256) * sum_k frame_u8(m, k) * W[n][k])
 // A: im2col Seg over u8 NHWC frames (rowlen % 32 == 0); W: dense fp32 [N][K]
 // (Seg with rows = N, rowlen = K); K % 64 == 0, BN in {16, 32, 64}.
-template <int BN, bool SHALLOW>
+template <int BN, int CAP>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_u8_fwd_kernel(Seg A, Seg B, int M, int N, int K, int kc, TcEpiArgs epi) {
   using S = U8Shape<BN>;
-  constexpr int NS = SHALLOW ? (S::NS_2 < S::NS_DEEP ? S::NS_2 : S::NS_DEEP) : S::NS_DEEP;
+  constexpr int NS = pipe::ring_depth(CAP, S::STAGE);
   static_assert(3 * BN <= 256 && BN % 16 == 0, "N-concatenated tile exceeds the MMA N limit");
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t ready[pipe::kMaxStages], done[pipe::kMaxStages], acc_bar;

@@ -39,16 +39,14 @@ struct DgradArgs {
   int B, IH, IW, cin, OH, OW, cout, k, s, T;
 };
 
-template <int BN, bool SHALLOW>
+template <int BN, int CAP>
 struct DgShape {
   static constexpr int A_HI = 128 * 128;     // 128 rows x 32 fp32
   static constexpr int A_BYTES = 2 * A_HI;   // hi + lo
   static constexpr int B_HI = BN * 128;
   static constexpr int B_BYTES = 2 * B_HI;   // hi rows [0,BN) then lo rows [BN,2BN)
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int NS_DEEP = pipe::stages_for(STAGE);
-  static constexpr int NS_2 = (112 * 1024) / STAGE < 2 ? 2 : (112 * 1024) / STAGE;
-  static constexpr int NS = SHALLOW ? (NS_2 < NS_DEEP ? NS_2 : NS_DEEP) : NS_DEEP;
+  static constexpr int NS = pipe::ring_depth(CAP, STAGE);
   static constexpr int SMEM = NS * STAGE + 1024;
   static constexpr int TMEM_COLS = ws::TmemCols<2 * BN>::V;
   static constexpr int AV = 128 * 8 / ws::kProducers;  // 16-byte A vectors per producer thread
@@ -56,9 +54,9 @@ struct DgShape {
   static constexpr int BPER = (BE + ws::kProducers - 1) / ws::kProducers;
 };
 
-template <int BN, bool SHALLOW>
+template <int BN, int CAP>
 __global__ void __launch_bounds__(ws::kThreads, 1) tc_dgrad_kernel(DgradArgs a) {
-  using S = DgShape<BN, SHALLOW>;
+  using S = DgShape<BN, CAP>;
   static_assert(BN % 16 == 0 && 2 * BN <= 256, "N-concatenated tile exceeds the MMA N limit");
   constexpr int kP = ws::kProducers;
   extern __shared__ uint8_t smem_raw[];

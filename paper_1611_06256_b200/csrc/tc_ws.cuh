@@ -52,7 +52,7 @@ struct TmemCols {
 // =========================================================== K-major GEMM
 // SHALLOW: at most ~112 KB of ring so two CTAs share an SM (multi-wave
 // grids: the second CTA's loads and MMAs cover the first one's epilogue).
-template <typename TA, typename TB, int BN, bool SHALLOW = false>
+template <typename TA, typename TB, int BN, int CAP = 0>
 struct KKShape {
   using TileA = pipe::KTile<TA, 128>;
   using TileB = pipe::KTile<TB, BN>;  // f32: hi rows [0,BN) then lo rows [BN,2BN) -- one 2BN-row tile
@@ -60,18 +60,17 @@ struct KKShape {
   static constexpr bool B_LO = sizeof(TB) == 4;
   static constexpr int STAGE = TileA::BYTES + TileB::BYTES;
   static constexpr int NS_DEEP = pipe::stages_for(STAGE);
-  static constexpr int NS_2 = (112 * 1024) / STAGE < 2 ? 2 : (112 * 1024) / STAGE;
-  static constexpr int NS = SHALLOW ? (NS_2 < NS_DEEP ? NS_2 : NS_DEEP) : NS_DEEP;
-  static_assert(NS >= 2, "tile too large for a 2-stage pipeline");
+  static constexpr int NS = pipe::ring_depth(CAP, STAGE);
+  static_assert(NS_DEEP >= 2, "tile too large for a 2-stage pipeline");
   static constexpr int SMEM = NS * STAGE + 1024;
   static constexpr int ACC_COLS = B_LO ? 2 * BN : BN;
   static constexpr int TMEM_COLS = TmemCols<ACC_COLS>::V;
 };
 
-template <typename TA, typename TB, int BN, int MODE, bool SHALLOW = false>
+template <typename TA, typename TB, int BN, int MODE, int CAP = 0>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_kk_ws_kernel(Seg A, Seg B, int M, int N, int K, int kc, TcEpiArgs epi) {
-  using S = KKShape<TA, TB, BN, SHALLOW>;
+  using S = KKShape<TA, TB, BN, CAP>;
   static_assert(!S::B_LO || 2 * BN <= 256, "N-concatenated tile exceeds the MMA N limit");
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t ready[pipe::kMaxStages], done[pipe::kMaxStages], acc_bar;
@@ -315,7 +314,7 @@ tc_kk_ws_kernel(Seg A, Seg B, int M, int N, int K, int kc, TcEpiArgs epi) {
 // =========================================================== MN-major GEMM
 // X tile: 32 pixels x 128 kk (hi, then lo or u8 staging).  D tile: per 4-row
 // k group, BN/32 hi atoms followed by BN/32 lo atoms (N-concatenated).
-template <typename TX, int BN>
+template <typename TX, int BN, int CAP = 0>
 struct MNShape {
   static constexpr bool X_LO = sizeof(TX) == 4;
   static constexpr int X_SBO = 4 * 512;
@@ -325,8 +324,8 @@ struct MNShape {
   static constexpr int D_SBO = 2 * D_ATOMS * 512;
   static constexpr int B_BYTES = 32 * 2 * BN * 4;
   static constexpr int STAGE = A_BYTES + A_STG + B_BYTES;
-  static constexpr int NS = pipe::stages_for(STAGE);
-  static_assert(NS >= 2, "tile too large for a 2-stage pipeline");
+  static constexpr int NS = pipe::ring_depth(CAP, STAGE);
+  static_assert(pipe::stages_for(STAGE) >= 2, "tile too large for a 2-stage pipeline");
   static constexpr int SMEM = NS * STAGE + 1024;
   static constexpr int TMEM_COLS = TmemCols<2 * BN>::V;
   static constexpr int DV = BN / 4;
@@ -334,10 +333,10 @@ struct MNShape {
   static constexpr int BN_PER = (BVEC + kProducers - 1) / kProducers;
 };
 
-template <typename TX, int BN>
+template <typename TX, int BN, int CAP = 0>
 __global__ void __launch_bounds__(kThreads, 1) tc_mn_ws_kernel(WgradArgs a) {
   static_assert(BN % 32 == 0 && 2 * BN <= 256, "MN-major tiles need 32-wide atoms, N <= 256");
-  using S = MNShape<TX, BN>;
+  using S = MNShape<TX, BN, CAP>;
   constexpr int DV = S::DV;
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t ready[pipe::kMaxStages], done[pipe::kMaxStages], acc_bar;
