@@ -36,6 +36,7 @@
 #include "tc_ws.cuh"
 #include "tc_bf16.cuh"
 #include "tc_dgrad.cuh"
+#include "tc_u8conv.cuh"
 #include "pdl.cuh"
 
 using namespace ga3c;
@@ -448,8 +449,59 @@ void u8_conv_launch(ga3c_ctx* c, int li, const Seg& A, const Seg& W, int M, int 
 }
 
 // Conv on raw u8 frames through the exact bf16 split (tc_bf16.cuh).
+// Persistent weight-stationary u8 conv (tc_u8conv.cuh); false when the
+// geometry is outside what it handles.
+template <int BN>
+void u8_persist_launch(ga3c_ctx* c, int li, const u8c::ConvArgs& a, dim3 grid) {
+  using S = u8c::Shape<BN>;
+  auto kern = u8c::tc_u8conv_kernel<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
+    attr_set = true;
+  }
+  Launch l(c, GA3C_K_CONV_FWD, li);
+  pdl_launch(c->cur, kern, grid, dim3(u8c::kThreads), S::SMEM, a);
+}
+
+bool u8_conv_persistent(ga3c_ctx* c, int li, const Layer& L, const float* theta, const uint8_t* x,
+                        long long bstride, float* out, int B) {
+  static const bool off = env_flag("GA3C_NO_PERSIST");
+  const int P = L.oh * L.ow;
+  const int rowb = L.iw * L.cin;
+  if (off || P < 128 || L.cin % 4 != 0 || rowb % 16 != 0 || L.in % 128 != 0 || L.in > u8c::kMaxK ||
+      (L.k * L.cin) % 16 != 0 || L.cout > 32 || L.cout % 4 != 0 || L.w_off % 4 != 0 || bstride % 16 != 0 ||
+      (reinterpret_cast<uintptr_t>(x) % 16) != 0)
+    return false;
+  // footprint bound: at most floor(127/ow)+2 output rows over at most two frames
+  const int span = 127 / L.ow;
+  const int rows = std::max((span + 1) * L.stride + L.k, span * L.stride + 2 * L.k);
+  // one tile per CTA gains nothing from persistence, and its 180 KB of smem
+  // would keep concurrent kernels off the SM: small grids take tc_bf16.cuh
+  if ((B * P + 127) / 128 < 2 * kNumSMs) return false;
+  const int fp_bytes = ((rows * rowb + 16) + 127) / 128 * 128;
+  const int fp_stages = std::min(u8c::kFpMaxStages, u8c::kFpRegion / fp_bytes);
+  if (fp_stages < 2) return false;
+  u8c::ConvArgs a{x, bstride, theta + L.w_off, theta + L.b_off, out, L.cout, B, L.ih, L.iw, L.cin, L.k,
+                  L.stride, L.oh, L.ow, L.cout, L.in, (B * P + 127) / 128, fp_bytes, fp_stages, 0};
+  static const int dbg = [] {
+    const char* e = std::getenv("GA3C_U8C_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.dbg = dbg;
+  const int bn = L.cout <= 16 ? 16 : 32;
+  dim3 grid(static_cast<unsigned>(std::min(a.tiles, split_sms(c))), (L.cout + bn - 1) / bn, 1);
+  if (bn == 16)
+    u8_persist_launch<16>(c, li, a, grid);
+  else
+    u8_persist_launch<32>(c, li, a, grid);
+  return true;
+}
+
 bool u8_conv_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const Seg& A, float* out, int B) {
   static const bool off = env_flag("GA3C_NO_BF16");
+  if (!off && u8_conv_persistent(c, li, L, theta, static_cast<const uint8_t*>(A.p), A.bstride, out, B))
+    return true;
   const int bn = tc_bn(L.cout);
   if (off || L.in % 64 != 0 || (L.k * L.cin) % 32 != 0 || bn > 64 || L.cout % 4 != 0 || L.w_off % 4 != 0 ||
       A.rowlen % 32 != 0)
