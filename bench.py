@@ -74,6 +74,9 @@ def parse():
                    help="N_T > 1: SMs each trainer context's split-K plans fill (ga3c_ctx_set_sm_budget); "
                         "0 = auto: a 1/N_T share when an update is latency-bound (< 50 MFLOP/sample), else all")
     p.add_argument("--pred-sms", type=int, default=0, help="same for the predictor context (0 = all)")
+    p.add_argument("--dp", default="fused", choices=["fused", "nccl"],
+                   help="N > 1 with N_T > 1: one fused reduce-scatter + RMSProp + all-gather kernel over NVLink "
+                        "peer memory (ga3c_dp_apply), or NCCL all-reduce + RMSProp")
     p.add_argument("--no-overlap", action="store_true",
                    help="N_T > 1: run the predictor phase before the trainers instead of beside them")
     p.add_argument("--no-graph", action="store_true", help="launch eagerly instead of CUDA graphs")
@@ -256,6 +259,8 @@ def config_of(args, world, sets=None):
             "params": param_count(args.net), "parallelism": f"dp{world}",
             "trainers_in_flight": args.trainers, "policy_lag_updates": args.trainers - 1,
             "predictor_trainer_overlap": args.trainers > 1 and not args.no_overlap,
+            "dp_update": (args.dp if world > 1 and args.trainers > 1 else
+                          ("nccl" if world > 1 else "none (1 GPU)")),
             "trainer_sm_budget": args.trainer_sms if args.trainers > 1 else 148,
             "l2": (f"inputs cycled over {sets} sets = {sets * n * FRAME_BYTES / 1e6:.0f} MB > 126 MB L2"
                    if sets else "n/a")}
@@ -356,6 +361,13 @@ def main():
             args.trainer_sms = 148 // NT if small else 148
         for c in tctx:
             c.set_sm_budget(args.trainer_sms)
+    fused = None
+    if world > 1 and NT > 1 and args.dp == "fused":
+        try:
+            fused = dp.FusedUpdate(model, tctx, ring[:R], rank, world)
+        except Exception as e:  # IPC unavailable: fall back to NCCL, and say so
+            print(f"[bench] fused DP update unavailable ({e}); using NCCL all-reduce", file=sys.stderr)
+            args.dp = "nccl"
     pctx = _abi.Context(model, NA) if overlap else ctx
     if overlap:
         pctx.set_sm_budget(args.pred_sms)
@@ -403,9 +415,12 @@ def main():
                                   rts.data_ptr() + 8 * u * TB, TB, ring[(u - NT + 1) % R], apply_clip=world == 1)
             ev_g[u].record(tstream[j])
             ev_g[u].wait(stream)
-            if world > 1:  # default hyper: no clip, so nothing to do after the sum
-                dp.allreduce_sum_(tgrad[j], stream)
-            ctx.apply_slots_dev(tctx[j], ring[u % R], ring[(u + 1) % R])
+            if fused is not None:  # reduce-scatter + RMSProp + all-gather in one kernel
+                fused.apply(ctx, j, ring[u % R], ring[(u + 1) % R])
+            else:
+                if world > 1:  # default hyper: no clip, so nothing to do after the sum
+                    dp.allreduce_sum_(tgrad[j], stream)
+                ctx.apply_slots_dev(tctx[j], ring[u % R], ring[(u + 1) % R])
             ev_a[u].record(stream)
         if overlap:
             ev_p.wait(stream)  # the predictor is done reading its slot

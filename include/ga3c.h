@@ -218,6 +218,34 @@ int ga3c_ctx_set_sm_budget(ga3c_ctx* c, int sms);
  * a device loop to a predictor-only slot that the trainers never write, so
  * predictors and trainers run concurrently (GA3C, pipeline.hpp:87-91). */
 int ga3c_copy_slot_dev(ga3c_ctx* c, int src_slot, int dst_slot);
+/* ---------------------------------------- data parallel, fused over NVLink
+ * One kernel per update replaces NCCL all-reduce(sum) + RMSProp on every
+ * replica: rank r reduces shard r of every
+ * rank's gradient over peer memory (fixed rank order), the non-finite reject
+ * and the optional clip are decided globally, RMSProp runs on the shard and
+ * theta' is stored into every rank's destination slot.  The rms state is
+ * sharded (each replica maintains only its own shard of g).  Peer pointers
+ * come from CUDA IPC (ga3c_ipc_*) or, for ranks that share a device, are the
+ * raw device pointers.  Replaces the NCCL path of dp.py's dp_update. */
+typedef struct ga3c_dp ga3c_dp;
+/* ctas: CTAs per call (<= 148, identical on every rank; all must be
+ * co-resident with the other ranks' calls). */
+ga3c_dp* ga3c_dp_create(ga3c_model* m, int rank, int world, int ctas, int* status);
+void ga3c_dp_destroy(ga3c_dp* dp);
+/* This rank's signal block (device memory, to be mapped into every peer). */
+void* ga3c_dp_signal(ga3c_dp* dp);
+/* Device pointer of a parameter slot's theta (for the peers' destination list). */
+int ga3c_model_slot_theta(ga3c_model* m, int slot, float** theta);
+/* One fused update on c's stream: gradient of grad_from (NULL = c), source
+ * and destination slots of this rank, and per-rank arrays (world entries,
+ * index = rank) of gradient buffers, destination thetas and signal blocks as
+ * mapped in this process.  Every rank must make the same sequence of calls. */
+int ga3c_dp_apply(ga3c_ctx* c, ga3c_dp* dp, const ga3c_ctx* grad_from, int src_slot, int dst_slot,
+                  float* const* peer_grads, float* const* peer_theta_dst, void* const* peer_signals);
+/* CUDA IPC of library allocations (64-byte handles). */
+int ga3c_ipc_get_handle(const void* dev_ptr, void* handle64);
+int ga3c_ipc_open_handle(const void* handle64, void** dev_ptr);
+int ga3c_ipc_close(void* dev_ptr);
 /* On-device update counter of ga3c_apply_rmsprop_dev (blocking read). */
 int ga3c_ctx_read_dev_version(ga3c_ctx* c, uint64_t* version);
 

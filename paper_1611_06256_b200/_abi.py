@@ -161,6 +161,14 @@ _SIGS = {
     "ga3c_train_frames": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, _P, _P, _P, C.c_int, _P, _P, C.c_double,
                                     C.c_int, _P, _P]),
     "ga3c_frames_read": (C.c_int, [_P, C.c_int, C.c_int, _P]),
+    "ga3c_dp_create": (_P, [_P, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]),
+    "ga3c_dp_destroy": (None, [_P]),
+    "ga3c_dp_signal": (_P, [_P]),
+    "ga3c_model_slot_theta": (C.c_int, [_P, C.c_int, C.POINTER(C.c_void_p)]),
+    "ga3c_dp_apply": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, _P, _P, _P]),
+    "ga3c_ipc_get_handle": (C.c_int, [_P, _P]),
+    "ga3c_ipc_open_handle": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
+    "ga3c_ipc_close": (C.c_int, [_P]),
 }
 
 K_TAGS = {"none": 0, "conv_fwd": 1, "fc_fwd": 2, "heads": 3, "loss_bwd": 4, "wgrad": 5, "dgrad": 6,
@@ -528,3 +536,53 @@ def train_frames(ctx: "Context", frames: Frames, agents, state_slots, actions, r
                                 rw.ctypes.data, off.ctypes.data, len(off) - 1, te.ctypes.data, bo.ctypes.data,
                                 gamma, 1 if apply_clip else 0, sc.ctypes.data, rets.ctypes.data), ctx.model.error())
     return sc, rets
+
+
+class FusedDP:
+    """ga3c_dp: the fused reduce-scatter + RMSProp + all-gather update of one
+    rank (include/ga3c.h).  `peers` are per-rank pointer lists as mapped in
+    this process (see dp.FusedAllreduce for the CUDA IPC exchange)."""
+
+    def __init__(self, model: Model, rank: int, world: int, ctas: int = 32):
+        st = C.c_int(0)
+        self.model = model
+        self.rank, self.world = rank, world
+        self.h = lib.ga3c_dp_create(model.h, rank, world, ctas, C.byref(st))
+        if not self.h:
+            check(st.value, model.error())
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.ga3c_dp_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def signal_ptr(self):
+        return lib.ga3c_dp_signal(self.h)
+
+    def apply(self, ctx, grad_from, src_slot, dst_slot, grads, theta_dst, signals):
+        W = self.world
+        arr = lambda xs: (C.c_void_p * W)(*[C.c_void_p(int(x)) for x in xs])
+        check(lib.ga3c_dp_apply(ctx.h, self.h, grad_from.h if grad_from is not None else None, src_slot, dst_slot,
+                                arr(grads), arr(theta_dst), arr(signals)), self.model.error())
+
+
+def slot_theta_ptr(model: Model, slot: int) -> int:
+    p = C.c_void_p(0)
+    check(lib.ga3c_model_slot_theta(model.h, slot, C.byref(p)), model.error())
+    return int(p.value)
+
+
+def ipc_handle(dev_ptr: int) -> bytes:
+    buf = (C.c_char * 64)()
+    check(lib.ga3c_ipc_get_handle(C.c_void_p(dev_ptr), buf))
+    return bytes(buf)
+
+
+def ipc_open(handle: bytes) -> int:
+    p = C.c_void_p(0)
+    buf = (C.c_char * 64).from_buffer_copy(handle)
+    check(lib.ga3c_ipc_open_handle(buf, C.byref(p)))
+    return int(p.value)

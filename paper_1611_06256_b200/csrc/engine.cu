@@ -37,6 +37,7 @@
 #include "tc_bf16.cuh"
 #include "tc_dgrad.cuh"
 #include "tc_u8conv.cuh"
+#include "dp_fused.cuh"
 #include "pdl.cuh"
 
 using namespace ga3c;
@@ -1698,6 +1699,105 @@ int ga3c_copy_slot_dev(ga3c_ctx* c, int src_slot, int dst_slot) {
   GA3C_CUDA(cudaMemcpyAsync(d.theta, s.theta, bytes, cudaMemcpyDeviceToDevice, c->stream));
   GA3C_CUDA(cudaMemcpyAsync(d.g, s.g, bytes, cudaMemcpyDeviceToDevice, c->stream));
   return GA3C_OK;
+}
+
+struct ga3c_dp {
+  ga3c_model* m = nullptr;
+  int rank = 0, world = 1, ctas = 1;
+  dpf::Signal* sig = nullptr;
+};
+
+ga3c_dp* ga3c_dp_create(ga3c_model* m, int rank, int world, int ctas, int* status) {
+  auto fail = [&](int st) -> ga3c_dp* {
+    if (status) *status = st;
+    return nullptr;
+  };
+  if (!m || world < 1 || world > dpf::kMaxRanks || rank < 0 || rank >= world || ctas < 1 || ctas > dpf::kMaxCtas)
+    return fail(GA3C_INVALID_ARGUMENT);
+  if (set_device(m)) return fail(GA3C_CUDA_ERROR);
+  auto* dp = new ga3c_dp;
+  dp->m = m;
+  dp->rank = rank;
+  dp->world = world;
+  dp->ctas = ctas;
+  if (cudaMalloc(&dp->sig, sizeof(dpf::Signal)) != cudaSuccess ||
+      cudaMemset(dp->sig, 0, sizeof(dpf::Signal)) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+    if (dp->sig) cudaFree(dp->sig);
+    delete dp;
+    m->set_error("ga3c_dp_create: device allocation failed");
+    return fail(GA3C_CUDA_ERROR);
+  }
+  if (status) *status = GA3C_OK;
+  return dp;
+}
+
+void ga3c_dp_destroy(ga3c_dp* dp) {
+  if (!dp) return;
+  set_device(dp->m);
+  cudaFree(dp->sig);
+  delete dp;
+}
+
+void* ga3c_dp_signal(ga3c_dp* dp) { return dp ? dp->sig : nullptr; }
+
+int ga3c_model_slot_theta(ga3c_model* m, int slot, float** theta) {
+  if (!m || !theta || slot < 0 || slot >= (int)m->slots.size()) return GA3C_INVALID_ARGUMENT;
+  *theta = m->slots[slot].theta;
+  return GA3C_OK;
+}
+
+int ga3c_dp_apply(ga3c_ctx* c, ga3c_dp* dp, const ga3c_ctx* grad_from, int src_slot, int dst_slot,
+                  float* const* peer_grads, float* const* peer_theta_dst, void* const* peer_signals) {
+  if (!c || !dp || dp->m != c->m || (grad_from && grad_from->m != c->m) || !peer_grads || !peer_theta_dst ||
+      !peer_signals || src_slot < 0 || dst_slot < 0 || src_slot >= (int)c->m->slots.size() ||
+      dst_slot >= (int)c->m->slots.size() || src_slot == dst_slot)
+    return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  const ga3c_ctx* g = grad_from ? grad_from : c;
+  dpf::Peers pr{};
+  pr.rank = dp->rank;
+  pr.world = dp->world;
+  for (int q = 0; q < dp->world; ++q) {
+    pr.grad[q] = peer_grads[q];
+    pr.theta_dst[q] = peer_theta_dst[q];
+    pr.sig[q] = static_cast<dpf::Signal*>(peer_signals[q]);
+    if (!pr.grad[q] || !pr.theta_dst[q] || !pr.sig[q]) return GA3C_INVALID_ARGUMENT;
+  }
+  if (pr.grad[dp->rank] != g->grad || pr.theta_dst[dp->rank] != m->slots[dst_slot].theta ||
+      pr.sig[dp->rank] != dp->sig)
+    return GA3C_INVALID_ARGUMENT;  // this rank's own entries must be its own buffers
+  const ga3c_hyper& hp = m->hp;
+  dpf::Step st{m->slots[src_slot].theta, m->slots[src_slot].g, m->slots[dst_slot].g, m->lo.total,
+               static_cast<float>(hp.alpha), static_cast<float>(1.0 - hp.alpha), static_cast<float>(hp.eta),
+               static_cast<float>(hp.eps_rms), hp.grad_clip_norm, c->dev_version};
+  Launch l(c, GA3C_K_RMSPROP, -1);
+  // plain launch (no PDL): the kernel spins on peers, it must not start early
+  dpf::dp_rmsprop_kernel<<<dp->ctas, dpf::kThreads, 0, c->cur>>>(pr, st);
+  GA3C_CUDA(cudaGetLastError());
+  return GA3C_OK;
+}
+
+int ga3c_ipc_get_handle(const void* dev_ptr, void* handle64) {
+  if (!dev_ptr || !handle64) return GA3C_INVALID_ARGUMENT;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)) != cudaSuccess) return GA3C_CUDA_ERROR;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle64, &h, sizeof(h));
+  return GA3C_OK;
+}
+
+int ga3c_ipc_open_handle(const void* handle64, void** dev_ptr) {
+  if (!handle64 || !dev_ptr) return GA3C_INVALID_ARGUMENT;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  if (cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return GA3C_CUDA_ERROR;
+  return GA3C_OK;
+}
+
+int ga3c_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return GA3C_INVALID_ARGUMENT;
+  return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? GA3C_OK : GA3C_CUDA_ERROR;
 }
 
 int ga3c_ctx_read_dev_version(ga3c_ctx* c, uint64_t* version) {

@@ -13,7 +13,9 @@ need no exchange.
 The functions here are the host-side plumbing; the arithmetic is the C ABI's
 (ga3c_loss_grad_dev with apply_clip=0, ga3c_clip_grad, ga3c_apply_rmsprop_dev)
 and the reduction is torch.distributed (NCCL on the B200 box, gloo in the
-CPU tests).
+CPU tests).  FusedUpdate replaces all-reduce + RMSProp with one kernel per
+update over NVLink peer memory (ga3c_dp_apply: reduce-scatter, sharded
+RMSProp, all-gather of theta'), wiring the peers' buffers with CUDA IPC.
 """
 from __future__ import annotations
 
@@ -61,3 +63,55 @@ def dp_update(ctx, d_states, u8, d_actions, d_returns, B_local, slot, gview, str
         allreduce_sum_(gview, stream)
         ctx.clip_grad()
     ctx.apply_rmsprop_dev()
+
+
+def peer_lists(local, gathered, rank, opener):
+    """Per-rank pointer lists from every rank's {name: [pointers or handles]}:
+    this rank's own pointers as they are, the peers' opened with `opener`."""
+    out = {}
+    for name in local:
+        out[name] = [[local[name][i] if q == rank else opener(gathered[q][name][i]) for q in range(len(gathered))]
+                     for i in range(len(local[name]))]
+    return out
+
+
+class FusedUpdate:
+    """Data-parallel update through ga3c_dp_apply.  Every rank passes the
+    same trainer contexts (by position) and ring slots (by id); their device
+    buffers are exchanged once as CUDA IPC handles over the process group."""
+
+    def __init__(self, model, grad_ctxs, slots, rank, world, ctas=32):
+        import torch.distributed as dist
+
+        from . import _abi
+        self.dp = _abi.FusedDP(model, rank, world, ctas)
+        self.slots = list(slots)
+        ptrs = {"grad": [c.grad_ptr() for c in grad_ctxs],
+                "theta": [_abi.slot_theta_ptr(model, sl) for sl in self.slots],
+                "sig": [self.dp.signal_ptr()]}
+        handles = {k: [_abi.ipc_handle(p) for p in v] for k, v in ptrs.items()}
+        gathered = [None] * world
+        dist.all_gather_object(gathered, handles)
+        self._opened = []
+
+        def opener(h):
+            p = _abi.ipc_open(h)
+            self._opened.append(p)
+            return p
+
+        self.peers = peer_lists(ptrs, gathered, rank, opener)
+        self.ctxs = list(grad_ctxs)
+
+    def apply(self, ctx, j, src_slot, dst_slot):
+        """RMSProp step from src_slot into dst_slot with trainer context j's
+        gradient, summed over every rank, on ctx's stream."""
+        dst = self.slots.index(dst_slot)
+        self.dp.apply(ctx, self.ctxs[j], src_slot, dst_slot, self.peers["grad"][j], self.peers["theta"][dst],
+                      self.peers["sig"][0])
+
+    def close(self):
+        from . import _abi
+        for p in self._opened:
+            _abi.lib.ga3c_ipc_close(p)
+        self._opened = []
+        self.dp.close()

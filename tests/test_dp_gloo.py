@@ -84,3 +84,19 @@ def test_shards_and_agent_sharding():
             assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
             assert max(b - a for a, b in parts) - min(b - a for a, b in parts) <= 1
     assert sorted(sum((agents_of(r, 4, 10) for r in range(4)), [])) == list(range(10))
+
+
+def test_peer_lists_keep_own_pointers_and_open_peers():
+    """FusedUpdate's IPC wiring: index = rank; this rank's own buffers as they
+    are, every peer's through the opener (CUDA IPC on the GPU box)."""
+    from paper_1611_06256_b200 import dp
+
+    world, rank = 3, 1
+    gathered = [{"grad": [f"g{q}a", f"g{q}b"], "sig": [f"s{q}"]} for q in range(world)]
+    local = {"grad": [100, 101], "sig": [200]}
+    opened = []
+    lists = dp.peer_lists(local, gathered, rank, lambda h: opened.append(h) or f"open({h})")
+    assert lists["grad"][0] == ["open(g0a)", 100, "open(g2a)"]
+    assert lists["grad"][1] == ["open(g0b)", 101, "open(g2b)"]
+    assert lists["sig"][0] == ["open(s0)", 200, "open(s2)"]
+    assert sorted(opened) == sorted(["g0a", "g2a", "g0b", "g2b", "s0", "s2"])
