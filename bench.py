@@ -365,8 +365,11 @@ def main():
     if world > 1 and NT > 1 and args.dp == "fused":
         try:
             fused = dp.FusedUpdate(model, tctx, ring[:R], rank, world)
-        except Exception as e:  # IPC unavailable: fall back to NCCL, and say so
+            if not fused.self_check(ctx, 0, P, f"cuda:{local}", ring[0], ring[1], ring[2]):
+                raise RuntimeError("self-check against NCCL all-reduce + RMSProp failed")
+        except Exception as e:  # IPC unavailable or a mismatch: fall back to NCCL, and say so
             print(f"[bench] fused DP update unavailable ({e}); using NCCL all-reduce", file=sys.stderr)
+            fused = None
             args.dp = "nccl"
     pctx = _abi.Context(model, NA) if overlap else ctx
     if overlap:

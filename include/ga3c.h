@@ -234,6 +234,9 @@ ga3c_dp* ga3c_dp_create(ga3c_model* m, int rank, int world, int ctas, int* statu
 void ga3c_dp_destroy(ga3c_dp* dp);
 /* This rank's signal block (device memory, to be mapped into every peer). */
 void* ga3c_dp_signal(ga3c_dp* dp);
+/* Synchronises the device; GA3C_CUDA_ERROR if any call of this dp timed out
+ * waiting for a peer (the call then left its destination unreliable). */
+int ga3c_dp_check(ga3c_dp* dp);
 /* Device pointer of a parameter slot's theta (for the peers' destination list). */
 int ga3c_model_slot_theta(ga3c_model* m, int slot, float** theta);
 /* One fused update on c's stream: gradient of grad_from (NULL = c), source

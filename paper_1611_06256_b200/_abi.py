@@ -164,6 +164,7 @@ _SIGS = {
     "ga3c_dp_create": (_P, [_P, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "ga3c_dp_destroy": (None, [_P]),
     "ga3c_dp_signal": (_P, [_P]),
+    "ga3c_dp_check": (C.c_int, [_P]),
     "ga3c_model_slot_theta": (C.c_int, [_P, C.c_int, C.POINTER(C.c_void_p)]),
     "ga3c_dp_apply": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, _P, _P, _P]),
     "ga3c_ipc_get_handle": (C.c_int, [_P, _P]),
@@ -561,6 +562,9 @@ class FusedDP:
 
     def signal_ptr(self):
         return lib.ga3c_dp_signal(self.h)
+
+    def check(self):
+        check(lib.ga3c_dp_check(self.h), self.model.error())
 
     def apply(self, ctx, grad_from, src_slot, dst_slot, grads, theta_dst, signals):
         W = self.world

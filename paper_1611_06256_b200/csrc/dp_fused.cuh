@@ -46,6 +46,7 @@ struct Signal {
   unsigned long long epoch;  // completed calls of this rank
   unsigned int count0, countA, countB;
   int nf_local;
+  int err;  // set when a barrier timed out (a peer never arrived): the call did nothing reliable
   unsigned long long flag0[kMaxRanks];  // written by rank q: epoch (entered the call)
   unsigned long long flagA[kMaxRanks];  // written by rank q: epoch << 1 | non-finite
   double ssA[kMaxRanks];                // written by rank q: its shard's sum of squares
@@ -93,14 +94,16 @@ __device__ __forceinline__ unsigned long long now_ns() {
 }
 
 // thread 0 of the CTA: wait until every rank wrote `want` (after >> shift).
-// A peer that never arrives (a rank died, or the ranks' call sequences
-// diverged) traps after 10 s instead of hanging the GPU.
-__device__ __forceinline__ void wait_all(const unsigned long long* f, int world, unsigned long long want,
+// A peer that never arrives (a rank died, the ranks' call sequences diverged,
+// peer memory not coherent) gives up after 2 s: the call sets Signal::err
+// (ga3c_dp_check reports it) instead of hanging the GPU.
+__device__ __forceinline__ bool wait_all(const unsigned long long* f, int world, unsigned long long want,
                                          int shift) {
   const unsigned long long t0 = now_ns();
   for (int q = 0; q < world; ++q)
     while ((ld_acquire(f + q) >> shift) != want)
-      if (now_ns() - t0 > 10000000000ull) __trap();
+      if (now_ns() - t0 > 2000000000ull) return false;
+  return true;
 }
 
 __global__ void __launch_bounds__(kThreads) dp_rmsprop_kernel(Peers pr, Step s) {
@@ -108,6 +111,7 @@ __global__ void __launch_bounds__(kThreads) dp_rmsprop_kernel(Peers pr, Step s) 
   __shared__ int nf_sh;
   __shared__ double ss_all_sh;
   __shared__ int nf_all_sh;
+  __shared__ int bail_sh;
   const int tid = threadIdx.x, G = gridDim.x;
   Signal* me = pr.sig[pr.rank];
   const unsigned long long ep = *reinterpret_cast<volatile unsigned long long*>(&me->epoch) + 1ull;
@@ -124,10 +128,12 @@ __global__ void __launch_bounds__(kThreads) dp_rmsprop_kernel(Peers pr, Step s) 
     __threadfence_system();
     if (atomicAdd(&me->count0, 1u) == static_cast<unsigned>(G * ep) - 1u)
       for (int q = 0; q < W; ++q) st_release(&pr.sig[q]->flag0[pr.rank], ep);
-    wait_all(me->flag0, W, ep, 0);
+    bail_sh = !wait_all(me->flag0, W, ep, 0);
+    if (bail_sh) atomicExch(&me->err, 1);
     nf_sh = 0;
   }
   __syncthreads();
+  if (bail_sh) return;
 
   // ---- phase 1: reduce this rank's shard (fixed rank order), non-finite flag, sum of squares
   double ss = 0.0;
@@ -181,7 +187,8 @@ __global__ void __launch_bounds__(kThreads) dp_rmsprop_kernel(Peers pr, Step s) 
         st_release(&pr.sig[q]->flagA[pr.rank], (ep << 1) | static_cast<unsigned long long>(nfl != 0));
       }
     }
-    wait_all(me->flagA, W, ep, 1);
+    bail_sh = !wait_all(me->flagA, W, ep, 1);
+    if (bail_sh) atomicExch(&me->err, 1);
     int nfa = 0;
     double sa = 0.0;
     for (int q = 0; q < W; ++q) {
@@ -192,6 +199,7 @@ __global__ void __launch_bounds__(kThreads) dp_rmsprop_kernel(Peers pr, Step s) 
     ss_all_sh = sa;
   }
   __syncthreads();
+  if (bail_sh) return;
 
   // ---- phase 2: RMSProp on the shard (or pass-through on reject), push theta' to every rank
   const bool reject = nf_all_sh != 0;
@@ -220,7 +228,7 @@ __global__ void __launch_bounds__(kThreads) dp_rmsprop_kernel(Peers pr, Step s) 
       if (!reject && s.version) *s.version += 1ull;
       *reinterpret_cast<volatile unsigned long long*>(&me->epoch) = ep;
     }
-    wait_all(me->flagB, W, ep, 0);
+    if (!wait_all(me->flagB, W, ep, 0)) atomicExch(&me->err, 1);
   }
   __syncthreads();
 }

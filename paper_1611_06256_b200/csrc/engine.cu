@@ -1740,6 +1740,21 @@ void ga3c_dp_destroy(ga3c_dp* dp) {
 
 void* ga3c_dp_signal(ga3c_dp* dp) { return dp ? dp->sig : nullptr; }
 
+int ga3c_dp_check(ga3c_dp* dp) {
+  if (!dp) return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = dp->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  if (set_device(m)) return GA3C_CUDA_ERROR;
+  GA3C_CUDA(cudaDeviceSynchronize());
+  int err = 0;
+  GA3C_CUDA(cudaMemcpy(&err, &dp->sig->err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err) {
+    set_err("ga3c_dp_apply: a peer never reached a barrier (timed out)");
+    return GA3C_CUDA_ERROR;
+  }
+  return GA3C_OK;
+}
+
 int ga3c_model_slot_theta(ga3c_model* m, int slot, float** theta) {
   if (!m || !theta || slot < 0 || slot >= (int)m->slots.size()) return GA3C_INVALID_ARGUMENT;
   *theta = m->slots[slot].theta;

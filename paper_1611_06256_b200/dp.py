@@ -109,6 +109,51 @@ class FusedUpdate:
         self.dp.apply(ctx, self.ctxs[j], src_slot, dst_slot, self.peers["grad"][j], self.peers["theta"][dst],
                       self.peers["sig"][0])
 
+    def self_check(self, ctx, j, P, device, src, dst_fused, dst_ref, stream=None):
+        """One fused update against NCCL all-reduce + ga3c_apply_rmsprop_slots_dev
+        on the same synthetic gradients (bitwise, on every rank); the two
+        destination slots are restored from src afterwards.  Returns True
+        when every rank agrees; on False the caller uses the NCCL path."""
+        import torch
+        import torch.distributed as dist
+
+        rank = dist.get_rank()
+        gv = grad_view(self.ctxs[j], P, device)
+
+        def fill():
+            i = torch.arange(P, device=device, dtype=torch.int64)
+            gv.copy_((((i * 7 + rank * 13) % 101) - 50).to(torch.float32) * 1e-4)
+
+        from . import _abi
+
+        def theta(slot):
+            class _V:
+                __cuda_array_interface__ = {"shape": (P,), "typestr": "<f4", "version": 3, "strides": None,
+                                            "data": (_abi.slot_theta_ptr(self.dp.model, slot), False)}
+            return torch.as_tensor(_V(), device=device)
+
+        ok = True
+        try:  # no collectives in here: a failure must not desynchronise the ranks
+            fill()
+            torch.cuda.synchronize()
+            self.apply(ctx, j, src, dst_fused)
+            self.dp.check()
+        except Exception:
+            ok = False
+        fill()
+        torch.cuda.synchronize()
+        allreduce_sum_(gv)  # every rank, exactly once
+        torch.cuda.synchronize()
+        ctx.apply_slots_dev(self.ctxs[j], src, dst_ref)
+        ctx.sync()
+        ok = ok and bool(torch.equal(theta(dst_fused), theta(dst_ref)))
+        ctx.copy_slot_dev(src, dst_fused)
+        ctx.copy_slot_dev(src, dst_ref)
+        ctx.sync()
+        flag = torch.tensor([1 if ok else 0], device=device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        return bool(flag.item())
+
     def close(self):
         from . import _abi
         for p in self._opened:
