@@ -66,7 +66,7 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=0)
     p.add_argument("--e2e-trainers", type=int, default=4, help="trainer threads in the e2e leg (0 = serial)")
     p.add_argument("--trainers", type=int, default=3,
-                   help="trainer contexts in flight in the device step (N_T; N_T + 1 must divide the updates)")
+                   help="trainer contexts in flight in the device step (N_T, policy lag N_T - 1 updates)")
     p.add_argument("--cpu-seconds", type=float, default=6.0)
     p.add_argument("--probe", default="conv_fwd:0",
                    help="kernel class[:layer] for the roofline probe (auto = largest eager share)")
@@ -343,10 +343,13 @@ def main():
     # trainer never reads a version that is being overwritten.
     NT = args.trainers
     assert hyper.grad_clip_norm == 0.0 or NT == 1, "clipping with several trainers in flight is not wired here"
-    assert NT >= 1 and updates % (NT + 1) == 0 if NT > 1 else True, "N_T + 1 must divide the updates per step"
+    # ring of R >= N_T + 1 slots; R divides the updates per step so every
+    # step starts from slot 0 (one captured graph per input set)
+    ring_sizes = [r for r in range(NT + 1, updates + 1) if updates % r == 0]
+    assert NT == 1 or ring_sizes, "N_T must be below the updates per step"
     overlap = NT > 1 and not args.no_overlap
     if NT > 1:
-        R = NT + 1
+        R = ring_sizes[0]
         ring = model.ring(R + 1)  # + the predictor's slot, never written by a trainer
         pred_slot = ring[R]
         tctx = [_abi.Context(model, TB) for _ in range(NT)]
