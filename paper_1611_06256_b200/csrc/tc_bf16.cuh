@@ -65,10 +65,11 @@ __device__ __forceinline__ void sts128u(uint32_t a, uint32_t x, uint32_t y, uint
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
 }
 
-// two u8 (as integers) -> packed bf16x2 (exact)
+// two u8 (as integers) -> packed bf16x2 (exact).  float(b) = (2^23 + b) - 2^23
+// via PRMT + FADD instead of I2F (quarter-rate XU pipe).
 __device__ __forceinline__ uint32_t u8x2_bf16(uint32_t b0, uint32_t b1) {
-  const uint32_t f0 = __float_as_uint(static_cast<float>(b0));
-  const uint32_t f1 = __float_as_uint(static_cast<float>(b1));
+  const uint32_t f0 = __float_as_uint(__uint_as_float(0x4B000000u | b0) - 8388608.0f);
+  const uint32_t f1 = __float_as_uint(__uint_as_float(0x4B000000u | b1) - 8388608.0f);
   return __byte_perm(f0, f1, 0x7632);  // upper halves: exact truncation of small integers
 }
 

@@ -92,12 +92,20 @@ __device__ __forceinline__ float4 lo4(float4 x) {
   return make_float4(lo_of(x.x), lo_of(x.y), lo_of(x.z), lo_of(x.w));
 }
 
+// byte i of w as the fp32 2^23 + byte (PRMT against 0x4B000000): no I2F,
+// which issues on the quarter-rate XU pipe
+__device__ __forceinline__ float magic_u8(uint32_t w, uint32_t sel) {
+  return __uint_as_float(__byte_perm(w, 0x4B000000u, sel));
+}
+
+// four u8 frame bytes -> fp32 x / 256, exactly: (2^23 + x) * 2^-8 - 2^15 is
+// one FFMA with an exact product and an exact result
 __device__ __forceinline__ float4 widen_u8(uint32_t w) {
   float4 f;
-  f.x = static_cast<float>(w & 0xFFu) * (1.0f / 256.0f);
-  f.y = static_cast<float>((w >> 8) & 0xFFu) * (1.0f / 256.0f);
-  f.z = static_cast<float>((w >> 16) & 0xFFu) * (1.0f / 256.0f);
-  f.w = static_cast<float>(w >> 24) * (1.0f / 256.0f);
+  f.x = __fmaf_rn(magic_u8(w, 0x7650u), 1.0f / 256.0f, -32768.0f);
+  f.y = __fmaf_rn(magic_u8(w, 0x7651u), 1.0f / 256.0f, -32768.0f);
+  f.z = __fmaf_rn(magic_u8(w, 0x7652u), 1.0f / 256.0f, -32768.0f);
+  f.w = __fmaf_rn(magic_u8(w, 0x7653u), 1.0f / 256.0f, -32768.0f);
   return f;
 }
 
