@@ -65,6 +65,7 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=0)
     p.add_argument("--e2e-trainers", type=int, default=4, help="trainer threads in the e2e leg (0 = serial)")
+    p.add_argument("--e2e-predictors", type=int, default=2, help="predictor threads in the e2e leg (N_P)")
     p.add_argument("--trainers", type=int, default=3,
                    help="trainer contexts in flight in the device step (N_T, policy lag N_T - 1 updates)")
     p.add_argument("--cpu-seconds", type=float, default=6.0)
@@ -710,14 +711,16 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
     # thread serves the agents while trainer threads, each with its own
     # context (stream), train on finished segments and apply to the latest
     # parameters (out-of-place snapshots, so predictions never read a
-    # half-written model).  The frame store keeps 2 steps of history, so a
-    # trainer may lag the predictor by one step.
+    # half-written model).
     import queue
     import threading
     ctx_t = [_abi.Context(model, max(NA, TB)) for _ in range(args.e2e_trainers)]
     store.close()
-    store = _abi.Frames(model, NA, 2 * T + 2)
-    q = queue.Queue(maxsize=1)
+    # training queue of train_queue_cap = 16 segments-batches (the
+    # reference's knob, knobs.hpp:15, default 32): the predictor runs up to
+    # a step ahead of the trainers, so the store keeps three steps of stacks
+    store = _abi.Frames(model, NA, 3 * T + 2)
+    q = queue.Queue(maxsize=updates)
 
     def trainer(j):
         c = ctx_t[j]
@@ -732,20 +735,36 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
                               r_h[s][sl].reshape(-1), seg_off, term_h[s][sl], boot[sl], hyper.gamma)
             c.apply_rmsprop()
 
+    # N_P predictor threads (GA3C's predictors), each with its own context,
+    # serving a contiguous group of agents
+    NP = max(1, args.e2e_predictors)
+    ctx_p = [ctx] + [_abi.Context(model, NA) for _ in range(NP - 1)]
+    from paper_1611_06256_b200.dp import shard
+    groups = [slice(a0, a1) for a0, a1 in (shard(NA, g, NP) for g in range(NP))]
+    from concurrent.futures import ThreadPoolExecutor
+    pool = ThreadPoolExecutor(max_workers=NP)
+
+    def predict_group(g, s, pt, acts, slots, vout):
+        gs = groups[g]
+        for t in range(T):
+            pi, v, sl, _ = _abi.predict_frames(ctx_p[g], store, newf[s][t][gs], agents[gs],
+                                               pt[gs] if t == 0 else None)
+            slots[gs, t] = sl
+            cdf = np.cumsum(pi.astype(np.float64), 1)
+            hit = u_h[s, t][gs, None] < cdf
+            a = hit.argmax(1)
+            a[~hit.any(1)] = N_ACTIONS - 1
+            acts[gs, t] = a
+        vout[gs] = v
+
     def predict_step(i, pt):
         s = i % hs
         acts = np.zeros((NA, T), np.int32)
         slots = np.zeros((NA, T), np.int32)
-        v = None
-        for t in range(T):
-            pi, v, sl, _ = _abi.predict_frames(ctx, store, newf[s][t], agents, pt if t == 0 else None)
-            slots[:, t] = sl
-            cdf = np.cumsum(pi.astype(np.float64), 1)
-            hit = u_h[s, t][:, None] < cdf
-            a = hit.argmax(1)
-            a[~hit.any(1)] = N_ACTIONS - 1
-            acts[:, t] = a
-        return s, acts, slots, v.astype(np.float64)
+        v = np.zeros(NA, np.float64)
+        for f in [pool.submit(predict_group, g, s, pt, acts, slots, v) for g in range(NP)]:
+            f.result()
+        return s, acts, slots, v
 
     dt = dt_serial
     mode = "serial calls"
@@ -775,7 +794,7 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
         torch.cuda.synchronize()
         dt_thr = time.perf_counter() - t0
         if dt_thr < dt:
-            dt, mode = dt_thr, f"1 predictor thread + {args.e2e_trainers} trainer threads"
+            dt, mode = dt_thr, f"{NP} predictor threads + {args.e2e_trainers} trainer threads"
     for c in ctx_t:
         c.close()
     store.close()

@@ -23,6 +23,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -52,6 +53,7 @@ constexpr std::size_t kPartFloats = std::size_t(32) << 20;  // split-K scratch p
 constexpr int kRegions = GA3C_MAX_CONV + GA3C_MAX_HIDDEN + 2;
 constexpr std::size_t kRegionFloats = kPartFloats / kRegions / 64 * 64;  // 256 B aligned
 constexpr int kMaxActions = 64;
+constexpr std::size_t kStageBytes = std::size_t(1) << 20;
 
 struct Slot {
   float* theta = nullptr;
@@ -118,6 +120,12 @@ struct ga3c_ctx {
   double* r_out = nullptr;
   std::size_t r_cap = 0, r_seg_cap = 0;
   int* h_flag = nullptr;  // pinned
+  // staging for the host-buffer calls' small inputs and outputs: packed into
+  // pinned memory and moved with ONE async copy each way (pageable
+  // cudaMemcpyAsync is synchronous and costs microseconds per call)
+  uint8_t* h_stage = nullptr;  // pinned, kStageBytes
+  uint8_t* d_stage = nullptr;  // device, kStageBytes
+  std::size_t stage_bytes = 0;
   int32_t* f_idx = nullptr;  // frame-store index staging
   std::size_t f_idx_cap = 0;
   std::uint64_t launches = 0;
@@ -199,6 +207,35 @@ void pdl_launch_cluster(cudaStream_t st, void (*kern)(KArgs...), dim3 grid, dim3
 struct SplitPlan {
   int splits = 1;
   int k_chunk = 0;
+};
+
+// Packs small host inputs into the context's pinned stage; flush() moves them
+// to the device stage with one async copy.  put() returns the device address
+// of the packed copy (nullptr when the stage is full: the caller falls back
+// to a direct copy).  Outputs: take() reserves pinned space a D2H lands in.
+struct Stager {
+  ga3c_ctx* c;
+  std::size_t off = 0;
+  template <typename T>
+  T* put(const T* src, std::size_t n) {
+    const std::size_t b = n * sizeof(T);
+    const std::size_t o = (off + 15) & ~static_cast<std::size_t>(15);
+    if (o + b > c->stage_bytes) return nullptr;
+    if (b) std::memcpy(c->h_stage + o, src, b);
+    off = o + b;
+    return reinterpret_cast<T*>(c->d_stage + o);
+  }
+  bool flush() {
+    return off == 0 || cudaMemcpyAsync(c->d_stage, c->h_stage, off, cudaMemcpyHostToDevice, c->stream) == cudaSuccess;
+  }
+  // pinned host space for outputs, after everything put() so far
+  template <typename T>
+  T* take(std::size_t n) {
+    const std::size_t o = (off + 15) & ~static_cast<std::size_t>(15);
+    if (o + n * sizeof(T) > c->stage_bytes) return nullptr;
+    off = o + n * sizeof(T);
+    return reinterpret_cast<T*>(c->h_stage + o);
+  }
 };
 
 int split_sms(const ga3c_ctx* c);
@@ -1009,6 +1046,7 @@ int run_loss_grad(ga3c_ctx* c, const float* theta, const void* d_in, bool u8, co
   return GA3C_OK;
 }
 
+
 // Frame store kernels.  A stacked pixel is one u32 (4 frames, oldest in the
 // low byte); pushing shifts the oldest out and the new frame in, or fills
 // all four with the new frame at an episode start.
@@ -1050,18 +1088,6 @@ __global__ void frames_gather_kernel(const uint32_t* __restrict__ ring, std::siz
       *reinterpret_cast<const uint4*>(ring + so);
 }
 
-int frames_idx_reserve(ga3c_ctx* c, std::size_t n) {
-  if (n <= c->f_idx_cap) return 0;
-  cudaStreamSynchronize(c->stream);
-  cudaFree(c->f_idx);
-  c->f_idx = nullptr;
-  c->f_idx_cap = std::max<std::size_t>(n, 1024);
-  if (cudaMalloc(&c->f_idx, c->f_idx_cap * sizeof(int32_t)) != cudaSuccess) {
-    c->f_idx_cap = 0;
-    return 1;
-  }
-  return 0;
-}
 
 // RMSProp from slot `src` into slot `dst` with the gradient (and its
 // non-finite flag) of context `g` (default: c itself), on c's stream.
@@ -1350,6 +1376,9 @@ ga3c_ctx* ga3c_ctx_create(ga3c_model* m, int max_batch, int* status) {
   alloc(&c->part, kPartFloats * sizeof(float));
   alloc(&c->clip_part, kNumSMs * sizeof(double));
   if (ok) ok = cudaMallocHost(&c->h_flag, sizeof(int)) == cudaSuccess;
+  c->stage_bytes = std::max<std::size_t>(kStageBytes, static_cast<std::size_t>(B) * 64);
+  if (ok) ok = cudaMallocHost(&c->h_stage, c->stage_bytes) == cudaSuccess;
+  alloc(&c->d_stage, c->stage_bytes);
   if (ok) ok = cudaMemset(c->dev_version, 0, sizeof(unsigned long long)) == cudaSuccess;
   if (ok) ok = cudaMemset(c->flag, 0, sizeof(int)) == cudaSuccess;
   if (ok) {
@@ -1375,7 +1404,7 @@ void ga3c_ctx_destroy(ga3c_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   void* ps[] = {c->d_in, c->hin, c->pi32, c->pi64, c->v, c->v64, c->dhead, c->dhT, c->scal,
                 c->scal_sum, c->d_actions, c->d_rets, c->grad, c->flag, c->dev_version, c->part,
-                c->clip_part, c->r_rew, c->r_off, c->r_term, c->r_boot, c->r_out, c->f_idx};
+                c->clip_part, c->r_rew, c->r_off, c->r_term, c->r_boot, c->r_out, c->f_idx, c->d_stage};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (auto* a : c->act)
@@ -1390,6 +1419,7 @@ void ga3c_ctx_destroy(ga3c_ctx* c) {
   for (auto e : c->evs)
     if (e) cudaEventDestroy(e);
   if (c->h_flag) cudaFreeHost(c->h_flag);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
   for (auto e : c->events) cudaEventDestroy(e);
   for (auto g : c->graphs) cudaGraphExecDestroy(g);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -1999,7 +2029,8 @@ int ga3c_ctx_graph_launch(ga3c_ctx* c, int graph_id) {
 static int loss_grad_segments(ga3c_ctx* c, int slot, const void* states, bool u8, int B,
                               const int32_t* actions, const double* rewards, const int32_t* off,
                               int n_seg, const uint8_t* terminal, const double* bootstrap, double gamma,
-                              int apply_clip, double* scalars, double* returns_out, bool dev_ready = false) {
+                              int apply_clip, double* scalars, double* returns_out, bool dev_ready = false,
+                              Stager* sg_in = nullptr, const std::function<void()>& after_flush = {}) {
   if (!c || B < 1 || B > c->max_batch || (!states && !dev_ready) || !actions || !rewards || !off || n_seg < 1 ||
       !terminal || !bootstrap)
     return GA3C_INVALID_ARGUMENT;
@@ -2038,26 +2069,37 @@ static int loss_grad_segments(ga3c_ctx* c, int slot, const void* states, bool u8
   if (pinned_here) ga3c_snapshot_acquire(m, &s, nullptr);
   int rc = GA3C_OK;
   const std::size_t bytes = dim * B * (u8 ? 1 : sizeof(float));
+  // small inputs packed into the pinned stage: one copy (plus the states)
+  Stager own{c};
+  Stager& sg = sg_in ? *sg_in : own;
+  const int32_t* d_act = sg.put(actions, B);
+  const double* d_rew = sg.put(rewards, B);
+  const int32_t* d_off = sg.put(off, n_seg + 1);
+  const uint8_t* d_term = sg.put(terminal, n_seg);
+  const double* d_boot = sg.put(bootstrap, n_seg);
+  double* h_scal = scalars ? sg.take<double>(3) : nullptr;
+  double* h_ret = returns_out ? sg.take<double>(B) : nullptr;
+  if (!d_act || !d_rew || !d_off || !d_term || !d_boot || (scalars && !h_scal) || (returns_out && !h_ret)) {
+    if (pinned_here) ga3c_snapshot_release(m, s);
+    set_err("loss_grad_segments: batch exceeds the context's staging area");
+    return GA3C_INVALID_ARGUMENT;
+  }
   if ((!dev_ready && cudaMemcpyAsync(c->d_in, states, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess) ||
-      cudaMemcpyAsync(c->d_actions, actions, sizeof(int32_t) * B, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
-      cudaMemcpyAsync(c->r_rew, rewards, sizeof(double) * B, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
-      cudaMemcpyAsync(c->r_off, off, sizeof(int32_t) * (n_seg + 1), cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
-      cudaMemcpyAsync(c->r_term, terminal, n_seg, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
-      cudaMemcpyAsync(c->r_boot, bootstrap, sizeof(double) * n_seg, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+      !sg.flush())
     rc = GA3C_CUDA_ERROR;
   if (!rc) {
+    if (after_flush) after_flush();
     {
       Launch l(c, GA3C_K_RETURNS, -1);
-      pdl_launch(c->cur, returns_kernel, dim3((n_seg + 127) / 128), dim3(128), 0, c->r_rew,
-                 (const int32_t*)c->r_off, n_seg, (const uint8_t*)c->r_term, (const double*)c->r_boot, gamma,
-                 c->d_rets);
+      pdl_launch(c->cur, returns_kernel, dim3((n_seg + 127) / 128), dim3(128), 0, d_rew, d_off, n_seg, d_term,
+                 d_boot, gamma, c->d_rets);
     }
-    run_loss_grad(c, m->slots[s].theta, c->d_in, u8, c->d_actions, c->d_rets, B, apply_clip != 0);
+    run_loss_grad(c, m->slots[s].theta, c->d_in, u8, d_act, c->d_rets, B, apply_clip != 0);
     if (scalars &&
-        cudaMemcpyAsync(scalars, c->scal_sum, sizeof(double) * 3, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+        cudaMemcpyAsync(h_scal, c->scal_sum, sizeof(double) * 3, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
       rc = GA3C_CUDA_ERROR;
     if (!rc && returns_out &&
-        cudaMemcpyAsync(returns_out, c->d_rets, sizeof(double) * B, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+        cudaMemcpyAsync(h_ret, c->d_rets, sizeof(double) * B, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
       rc = GA3C_CUDA_ERROR;
   }
   cudaError_t e = cudaStreamSynchronize(c->stream);
@@ -2065,6 +2107,8 @@ static int loss_grad_segments(ga3c_ctx* c, int slot, const void* states, bool u8
     rc = GA3C_CUDA_ERROR;
     set_err(std::string("loss_grad_segments: ") + cudaGetErrorString(e));
   }
+  if (!rc && scalars) std::memcpy(scalars, h_scal, sizeof(double) * 3);
+  if (!rc && returns_out) std::memcpy(returns_out, h_ret, sizeof(double) * B);
   if (pinned_here) ga3c_snapshot_release(m, s);
   return rc;
 }
@@ -2123,32 +2167,39 @@ int ga3c_predict_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* ne
   }
   int rc = GA3C_OK;
   if (n > 0) {
-    if (frames_idx_reserve(c, 4 * n)) rc = GA3C_CUDA_ERROR;
-    // dense stacked states at d_in, the new frames right after them
+    // dense stacked states at d_in, the new frames right after them; the
+    // index table in, pi and v out through the pinned stage
     uint8_t* dense = static_cast<uint8_t*>(c->d_in);
     uint8_t* newf = dense + static_cast<std::size_t>(c->max_batch) * m->lo.in_dim;
+    const int A = m->lo.n_actions;
+    Stager sg{c};
+    const int32_t* d_idx = sg.put(idx.data(), idx.size());
+    float* h_pi = sg.take<float>(static_cast<std::size_t>(n) * A);
+    float* h_v = sg.take<float>(n);
+    if (!d_idx || !h_pi || !h_v) rc = GA3C_INVALID_ARGUMENT;
     if (!rc && (cudaMemcpyAsync(newf, new_frames, f->frame_px * n, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
-                cudaMemcpyAsync(c->f_idx, idx.data(), sizeof(int32_t) * 4 * n, cudaMemcpyHostToDevice,
-                                c->stream) != cudaSuccess))
+                !sg.flush()))
       rc = GA3C_CUDA_ERROR;
     if (!rc) {
       {
         Launch l(c, GA3C_K_OTHER, -1);
         pdl_launch(c->cur, frames_push_kernel, dim3((unsigned)((f->frame_px / 4 + 255) / 256), n), dim3(256), 0,
                    reinterpret_cast<uint32_t*>(f->ring), f->frame_px, f->history,
-                   reinterpret_cast<const uint32_t*>(newf), (const int32_t*)c->f_idx, n,
-                   reinterpret_cast<uint32_t*>(dense));
+                   reinterpret_cast<const uint32_t*>(newf), d_idx, n, reinterpret_cast<uint32_t*>(dense));
       }
       run_forward(c, m->slots[s].theta, dense, true, n);
-      const int A = m->lo.n_actions;
-      if (cudaMemcpyAsync(pi, c->pi32, sizeof(float) * n * A, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
-          cudaMemcpyAsync(v, c->v, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+      if (cudaMemcpyAsync(h_pi, c->pi32, sizeof(float) * n * A, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+          cudaMemcpyAsync(h_v, c->v, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
         rc = GA3C_CUDA_ERROR;
     }
     cudaError_t e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) {
       rc = GA3C_CUDA_ERROR;
       set_err(std::string("predict_frames: ") + cudaGetErrorString(e));
+    }
+    if (!rc) {
+      std::memcpy(pi, h_pi, sizeof(float) * n * A);
+      std::memcpy(v, h_v, sizeof(float) * n);
     }
   }
   if (pinned_here) ga3c_snapshot_release(m, s);
@@ -2165,21 +2216,22 @@ int ga3c_train_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const int32_t* agen
     if (agents[b] < 0 || agents[b] >= f->n_agents || state_slots[b] < 0 || state_slots[b] >= f->history)
       return GA3C_INVALID_ARGUMENT;
   ga3c_model* m = c->m;
-  auto set_err = [&](const std::string& e) { m->set_error(e); };
   if (set_device(m)) return GA3C_CUDA_ERROR;
-  if (frames_idx_reserve(c, 2 * B)) return GA3C_CUDA_ERROR;
   std::vector<int32_t> idx(2 * static_cast<std::size_t>(B));
   std::copy(agents, agents + B, idx.begin());
   std::copy(state_slots, state_slots + B, idx.begin() + B);
-  GA3C_CUDA(cudaMemcpyAsync(c->f_idx, idx.data(), sizeof(int32_t) * 2 * B, cudaMemcpyHostToDevice, c->stream));
-  {
-    Launch l(c, GA3C_K_OTHER, -1);
-    pdl_launch(c->cur, frames_gather_kernel, dim3((unsigned)((f->frame_px / 4 + 255) / 256), B), dim3(256), 0,
-               reinterpret_cast<const uint32_t*>(f->ring), f->frame_px, f->history, (const int32_t*)c->f_idx, B,
-               reinterpret_cast<uint32_t*>(c->d_in));
-  }
+  Stager sg{c};
+  const int32_t* d_idx = sg.put(idx.data(), idx.size());
+  if (!d_idx) return GA3C_INVALID_ARGUMENT;
+  // the gather runs after the single staged copy, before the returns/loss kernels
   return loss_grad_segments(c, slot, nullptr, true, B, actions, rewards, seg_offsets, n_seg, terminal, bootstrap,
-                            gamma, apply_clip, scalars, returns_out, true);
+                            gamma, apply_clip, scalars, returns_out, true, &sg, [&] {
+                              Launch l(c, GA3C_K_OTHER, -1);
+                              pdl_launch(c->cur, frames_gather_kernel,
+                                         dim3((unsigned)((f->frame_px / 4 + 255) / 256), B), dim3(256), 0,
+                                         reinterpret_cast<const uint32_t*>(f->ring), f->frame_px, f->history,
+                                         d_idx, B, reinterpret_cast<uint32_t*>(c->d_in));
+                            });
 }
 
 ga3c_frames* ga3c_frames_create(ga3c_model* m, int n_agents, int history, int* status) {
