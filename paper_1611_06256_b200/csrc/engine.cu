@@ -724,7 +724,11 @@ bool layer_wgrad_tc(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const
         break;
       }
   const int ntiles = (L.out + bn - 1) / bn;
-  int splits = std::max(1, std::min(chunks / 2, (split_sms(c) + mtiles * ntiles - 1) / (mtiles * ntiles)));
+  // a context with the whole GPU plans two CTAs per SM (ring cap 1), so the
+  // conversion-heavy producers of one CTA overlap the other's
+  static const bool one = env_flag("GA3C_WGRAD_1CTA");
+  const int wsms = split_sms(c) * (!one && split_sms(c) >= kNumSMs ? 2 : 1);
+  int splits = std::max(1, std::min(chunks / 2, (wsms + mtiles * ntiles - 1) / (mtiles * ntiles)));
   while (splits > 1 && static_cast<std::size_t>(splits) * L.out * (L.in + 1) > kRegionFloats) --splits;
   const int kc = ((chunks + splits - 1) / splits) * 32;
   splits = (npix + kc - 1) / kc;

@@ -47,13 +47,13 @@ constexpr int stages_for(int stage_bytes) {
   return (220 * 1024) / stage_bytes < kMaxStages ? (220 * 1024) / stage_bytes : kMaxStages;
 }
 // Ring depth for a stage cap: 0 = as deep as ~220 KB of shared memory
-// allows (one CTA per SM), 1 = at most ~112 KB (two CTAs per SM: a
+// allows (one CTA per SM), 1 = at most ~100 KB (two CTAs per SM: a
 // multi-wave grid, or CTAs of concurrent kernels, share the SM), n >= 2 = at
 // most n stages (a CTA that only ever streams n chunks needs no more; the
 // smaller footprint lets other kernels' CTAs co-reside).  Never below 2.
 constexpr int ring_depth(int cap, int stage_bytes) {
   const int deep = stages_for(stage_bytes);
-  const int two = (112 * 1024) / stage_bytes;
+  const int two = (100 * 1024) / stage_bytes;  // + static smem and alignment: two CTAs fit in 228 KB
   const int d = cap == 0 ? deep : (cap == 1 ? (two < deep ? two : deep) : (cap < deep ? cap : deep));
   return d < 2 ? 2 : d;
 }
