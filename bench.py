@@ -63,6 +63,8 @@ def parse():
     p.add_argument("--sets", type=int, default=0, help="input sets cycled (0 = enough to exceed L2)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-loop", action="store_true", help="skip the C++ GA3C loop leg (ga3c_loop)")
+    p.add_argument("--loop-seconds", type=float, default=5.0)
     p.add_argument("--e2e-steps", type=int, default=0)
     p.add_argument("--e2e-trainers", type=int, default=4, help="trainer threads in the e2e leg (0 = serial)")
     p.add_argument("--e2e-predictors", type=int, default=2, help="predictor threads in the e2e leg (N_P)")
@@ -590,6 +592,10 @@ def main():
         e2e = e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world, grad_view,
                       stream, dist)
 
+    loop = None
+    if rank == 0 and world == 1 and not args.no_loop and args.net == "dnn_a":
+        loop = loop_leg(args)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         r = cpu_leg(args.net, NA, T, TB, args.cpu_seconds)
@@ -604,13 +610,36 @@ def main():
             "config": config_of(args, world, sets),
             "pps": value, "tps_updates_per_s": updates / (ms_step / 1e3),
             "fwd_mflop_per_prediction": fwd_flops_per_sample(args.net) / 1e6,
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "ga3c_loop": loop, "gpu_launches": launches,
             "clocks": clk, "kernel_breakdown_ms_per_step": breakdown,
             "cuda_graph": graphs is not None,
         }
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def loop_leg(args):
+    """BASELINE configs[1] as the reference runs it: the C++ host engine
+    (ga3c_pipeline_run = qac::run, pipeline.cpp:100-611) with agent threads
+    stepping synthetic 84x84x4 frame environments (envs.cpp Frames, no step
+    delay), N_P predictor threads batching the prediction queue into
+    ga3c_forward_u8, N_T trainer threads coalescing >= min_train_batch
+    experiences into ga3c_loss_grad_segments_u8 + ga3c_apply_rmsprop.  Whole
+    28 KB states cross PCIe both ways (the reference's data path); the knobs
+    are the paper's best DNN A point (N_A = 128, N_P = N_T = 2)."""
+    from paper_1611_06256_b200 import qac
+    opt = qac.PipelineOptions(net=qac.dnn_a(), env=qac.frames(step_delay_us=0, episode_len=64))
+    opt.knobs = qac.KnobConfig(n_agents=args.agents, n_predictors=2, n_trainers=2, pred_batch_max=args.agents,
+                               min_train_batch=args.train_batch)
+    opt.stop = qac.StopCondition(max_seconds=args.loop_seconds)
+    r = qac.run(opt)
+    return {"value": r.avg_samples_per_s, "unit": "samples/s", "tps_updates_per_s": r.avg_tps,
+            "pps": r.avg_pps, "updates": r.total_updates, "wall_s": r.wall_time_s, "mean_policy_lag": r.mean_lag,
+            "knobs": {"n_agents": args.agents, "n_predictors": 2, "n_trainers": 2,
+                      "pred_batch_max": args.agents, "min_train_batch": args.train_batch},
+            "path": "C++ host engine (ga3c_pipeline_run): agent threads + prediction/training queues + "
+                    "ga3c_forward_u8 / ga3c_loss_grad_segments_u8 / ga3c_apply_rmsprop"}
 
 
 def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world, grad_view, stream, dist):
