@@ -95,6 +95,33 @@ def test_dnn_a_loss_and_gradients(B):
     check_grad(spec, th, fr, O.frames_to_states(fr), acts, rets)
 
 
+# B >= 95 frames is >= 2 tiles per SM: conv1 runs the persistent int8 kernel
+# (tc_u8conv.cuh) -- tiles straddling two frames, multi-tile CTAs, the TMA
+# footprint ring wrapping around.
+@pytest.mark.parametrize("B", [128, 256])
+def test_dnn_a_forward_persistent_conv1(B):
+    spec = O.dnn_a()
+    th = theta32(spec, O.derive_seed(1, [O.SEED_MODEL_INIT]))
+    fr = O.synthetic_frames(40 + B, B)
+    check_forward(spec, th, fr, O.frames_to_states(fr))
+
+
+def test_dnn_a_loss_and_gradients_persistent_conv1():
+    B = 128
+    spec = O.dnn_a()
+    th = theta32(spec, O.derive_seed(1, [O.SEED_MODEL_INIT]))
+    fr = O.synthetic_frames(50, B)
+    acts, rets = O.synthetic_batch(50, B, 6)
+    check_grad(spec, th, fr, O.frames_to_states(fr), acts, rets)
+
+
+def test_large_dnn_stride1_forward_persistent_conv1():
+    spec = O.dnn_large(1)  # 77x77 conv1 outputs: 371 tiles at B = 8, odd rows straddle tiles
+    th = theta32(spec, 3)
+    fr = O.synthetic_frames(6, 8)
+    check_forward(spec, th, fr, O.frames_to_states(fr))
+
+
 def test_dnn_a_golden(golden):
     g = golden("dnn_a")
     spec = O.dnn_a()
