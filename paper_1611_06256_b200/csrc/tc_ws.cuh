@@ -50,7 +50,7 @@ struct TmemCols {
 };
 
 // =========================================================== K-major GEMM
-// SHALLOW: at most ~112 KB of ring so two CTAs share an SM (multi-wave
+// CAP (pipe::ring_depth): 1 = at most ~100 KB of ring so two CTAs share an SM (multi-wave
 // grids: the second CTA's loads and MMAs cover the first one's epilogue).
 template <typename TA, typename TB, int BN, int CAP = 0>
 struct KKShape {
