@@ -827,7 +827,13 @@ bool conv_dgrad_tc(ga3c_ctx* c, int li, const Layer& L, const float* theta, cons
   const long long m0 = static_cast<long long>(B) * a0 * b0;
   const int ntiles = (L.cin + bn - 1) / bn;
   dim3 grid(static_cast<unsigned>((m0 + 127) / 128), L.stride * L.stride, ntiles);
-  const int cap = ring_cap(c, T * T * L.cout / 32, static_cast<long long>(grid.x) * grid.y * grid.z);
+  // GA3C_DGRAD_CAP forces a ring cap (A/B measurement: large s1 conv2 dgrad
+  // cap 0 = 97 us, 1 = 68 us, 2 = 68 us, 3 = 97 us -- two CTAs per SM win)
+  static const int force = [] {
+    const char* e = std::getenv("GA3C_DGRAD_CAP");
+    return e ? std::atoi(e) : -1;
+  }();
+  const int cap = force >= 0 ? force : ring_cap(c, T * T * L.cout / 32, static_cast<long long>(grid.x) * grid.y * grid.z);
   switch (bn) {
     case 16: {
 #define GA3C_F(C) dgrad_tc_launch<16, C>(c, li, a, grid)
