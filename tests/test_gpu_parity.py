@@ -375,3 +375,40 @@ def test_deterministic_gradients():
     d1, s1 = ctx.loss_grad(fr, acts, rets)
     d2, s2 = ctx.loss_grad(fr, acts, rets)
     assert np.array_equal(d1, d2) and np.array_equal(s1, s2)
+
+
+@pytest.mark.parametrize("sms", [16, 49])
+def test_sm_budget_changes_plans_not_results(sms):
+    """ga3c_ctx_set_sm_budget re-plans every split-K (fewer, longer CTAs);
+    the gradient stays within the parity tolerance of the oracle and is
+    deterministic for a given budget."""
+    B = 40
+    spec = O.dnn_a()
+    th = theta32(spec, O.derive_seed(1, [O.SEED_MODEL_INIT]))
+    fr = O.synthetic_frames(60, B)
+    acts, rets = O.synthetic_batch(60, B, 6)
+    m, ctx = make(spec, max_batch=B)
+    m.load(th)
+    ctx.set_sm_budget(sms)
+    d1, _ = ctx.loss_grad(fr, acts, rets)
+    d2, _ = ctx.loss_grad(fr, acts, rets)
+    assert np.array_equal(d1, d2)
+    rd, _ = O.loss_and_gradients(spec, HYPER, th.astype(np.float64), O.frames_to_states(fr), acts, rets)
+    grad_close(d1, rd)
+
+
+def test_copy_slot_publishes_parameters():
+    spec = O.make_spec((12, 12, 2), [(4, 4, 2)], [8], 4)
+    m, ctx = make(spec, max_batch=4)
+    th = theta32(spec, 5)
+    m.load(th)
+    a, b = m.ring(2)
+    from paper_1611_06256_b200 import _abi
+    import torch
+    ctx.copy_slot_dev(a, b)
+    ctx.sync()
+
+    class _V:
+        __cuda_array_interface__ = {"shape": (m.P,), "typestr": "<f4", "version": 3, "strides": None,
+                                    "data": (_abi.slot_theta_ptr(m, b), False)}
+    assert np.array_equal(torch.as_tensor(_V(), device="cuda").cpu().numpy(), th)
