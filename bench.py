@@ -129,6 +129,23 @@ def work_per_step(net, agents, tmax, tb):
     return w
 
 
+def bytes_per_step(net, agents, tmax, tb):
+    """Algorithmic HBM bytes per step of each forward-layer class: the layer's
+    input (u8 frames for conv1, fp32 activations otherwise) and its fp32
+    output, read/written once per launch (weights are negligible)."""
+    layers, _ = layer_geometry(net)
+    n_fwd = agents * tmax + agents * tmax  # predictor + trainer recompute
+    b = {}
+    h, w, c = FRAME
+    in_bytes = h * w * c  # u8 state
+    for li, l in enumerate(layers):
+        out = l["N"] * l["P"] * 4
+        key = "conv_fwd" if l["kind"] == "conv" else "fc_fwd"
+        b[(key, li)] = float(in_bytes + out) * n_fwd
+        in_bytes = out
+    return b
+
+
 def fwd_flops_per_sample(net):
     layers, heads = layer_geometry(net)
     return sum(2.0 * l["K"] * l["N"] * l["P"] for l in layers) + 2.0 * heads["K"] * heads["N"]
@@ -563,12 +580,24 @@ def main():
     hbm, bf16, bf16_sus, peak_src = measured_peaks()
     probed_steps = probe_steps
     w = work[probe] * probed_steps
+    # the kernel's bound is the lower roofline: below the ridge (measured bf16
+    # peak / measured HBM bandwidth) its arithmetic intensity makes it HBM-bound
+    byts = bytes_per_step(args.net, NA, T, TB).get(probe)
+    ai = work[probe] / byts if byts else None
     if probe[0] == "rmsprop":
         achieved = w / (probe_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s"}
+    elif ai is not None and ai < bf16 * 1e3 / hbm:
+        achieved = byts * probed_steps / (probe_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "arithmetic_intensity_flop_per_byte": ai, "ridge_flop_per_byte": bf16 * 1e3 / hbm,
+                "tflops_achieved": w / (probe_ms / 1e3) / 1e12, "tflops_frac_of_bf16_peak":
+                w / (probe_ms / 1e3) / 1e12 / bf16}
     else:
         achieved = w / (probe_ms / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s"}
+        if ai is not None:
+            roof.update({"arithmetic_intensity_flop_per_byte": ai, "ridge_flop_per_byte": bf16 * 1e3 / hbm})
     traffic, traffic_src = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
