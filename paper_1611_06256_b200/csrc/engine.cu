@@ -516,7 +516,11 @@ bool u8_conv_persistent(ga3c_ctx* c, int li, const Layer& L, const float* theta,
   const int rows = std::max((span + 1) * L.stride + L.k, span * L.stride + 2 * L.k);
   // one tile per CTA gains nothing from persistence, and its 180 KB of smem
   // would keep concurrent kernels off the SM: small grids take tc_bf16.cuh
-  if ((B * P + 127) / 128 < 2 * kNumSMs) return false;
+  static const int min_tiles = [] {
+    const char* e = std::getenv("GA3C_PERSIST_MIN_TILES");
+    return e ? std::atoi(e) : 2 * kNumSMs;
+  }();
+  if ((B * P + 127) / 128 < min_tiles) return false;
   const int fp_bytes = ((rows * rowb + 16) + 127) / 128 * 128;
   const int fp_stages = std::min(u8c::kFpMaxStages, u8c::kFpRegion / fp_bytes);
   if (fp_stages < 2) return false;
