@@ -83,6 +83,10 @@ def parse():
     p.add_argument("--no-overlap", action="store_true",
                    help="N_T > 1: run the predictor phase before the trainers instead of beside them")
     p.add_argument("--no-graph", action="store_true", help="launch eagerly instead of CUDA graphs")
+    p.add_argument("--no-graph-warm", action="store_true",
+                   help="skip the graph warm-up launches (theta_fingerprint then depends only on W and K)")
+    p.add_argument("--graph-steps", type=int, default=0,
+                   help="steps chained per CUDA graph (0 = the largest of 4..1 dividing --steps)")
     p.add_argument("--timeline", default="", help="write a per-launch timeline of one eager step here")
     return p.parse_args()
 
@@ -333,6 +337,7 @@ def main():
     # ---- synthetic inputs resident in HBM (agent-major frame rings) ----
     set_bytes = n * FRAME_BYTES
     sets = args.sets or max(2, int(np.ceil(160e6 / set_bytes)))
+    sets += sets % 2  # even: the double-buffered experience parity survives the cycle wrap
     g = torch.Generator(device="cuda")
     g.manual_seed(1234 + rank)
     frames = torch.randint(0, 256, (sets, NA, T) + FRAME, dtype=torch.uint8, device="cuda", generator=g)
@@ -362,6 +367,7 @@ def main():
     # stream and write out of place into a ring of N_T + 1 device slots, so a
     # trainer never reads a version that is being overwritten.
     NT = args.trainers
+    GMAX = 4  # steps one CUDA graph may chain
     assert hyper.grad_clip_norm == 0.0 or NT == 1, "clipping with several trainers in flight is not wired here"
     # ring of R >= N_T + 1 slots; R divides the updates per step so every
     # step starts from slot 0 (one captured graph per input set)
@@ -375,10 +381,13 @@ def main():
         tctx = [_abi.Context(model, TB) for _ in range(NT)]
         tstream = [torch.cuda.ExternalStream(c.stream) for c in tctx]
         tgrad = [dp.grad_view(c, P, f"cuda:{local}") for c in tctx] if world > 1 else None
-        ev_g = [torch.cuda.Event() for _ in range(updates)]
-        ev_a = [torch.cuda.Event() for _ in range(updates)]
+        # events per update of a multi-step graph (update index continuous
+        # across the steps one graph captures, see `step`)
+        ev_g = [torch.cuda.Event() for _ in range(updates * GMAX)]
+        ev_a = [torch.cuda.Event() for _ in range(updates * GMAX)]
         ev_r = torch.cuda.Event()
-        ev_p = torch.cuda.Event()
+        ev_p = [torch.cuda.Event() for _ in range(GMAX)]
+        ev_end = [torch.cuda.Event() for _ in range(GMAX)]
         if args.trainer_sms == 0:
             small = 2.5 * fwd_flops_per_sample(args.net) < 50e6
             args.trainer_sms = 148 // NT if small else 148
@@ -412,7 +421,7 @@ def main():
         pctx.compute_returns_dev(rewards[s].data_ptr(), offsets.data_ptr(), NA, terminal[s].data_ptr(), lv,
                                  hyper.gamma, rts.data_ptr())
 
-    def step(i):
+    def step(i, pos=0):
         if NT == 1:
             predict(i, 0)
             fr = frames[i % sets].data_ptr()
@@ -420,37 +429,54 @@ def main():
                 dp.dp_update(ctx, fr + u * TB * FRAME_BYTES, True, actions.data_ptr() + 4 * u * TB,
                              rets.data_ptr() + 8 * u * TB, TB, slot, grad_view, stream, world)
             return
+        # pos: position of this step inside a multi-step graph (0 = first,
+        # or eager).  Update U = pos * updates + u is continuous across the
+        # chained steps, so trainer U waits only for apply U - N_T and the
+        # first updates of step pos + 1 overlap the last ones of step pos.
+        base = pos * updates
         if overlap:
             # predictor branch (own context and stream) || trainers on the
-            # previous step's experiences
-            ev_r.record(stream)
-            ev_r.wait(pstream)
+            # previous step's experiences.  The predictor of a chained step
+            # waits for the previous step's end (its slot was refreshed and
+            # the experience buffer it overwrites was consumed).
+            if pos == 0:
+                ev_r.record(stream)
+                ev_r.wait(pstream)
+            else:
+                ev_end[pos - 1].wait(pstream)
             predict(i, i % 2)
-            ev_p.record(pstream)
+            ev_p[pos].record(pstream)
             ti, b = i - 1, (i - 1) % 2
+            ready = ev_r if pos == 0 else ev_p[pos - 1]  # this step's experiences exist
         else:
             predict(i, 0)
             ev_r.record(stream)
             ti, b = i, 0
+            ready = ev_r
         fr = frames[ti % sets].data_ptr()
         acts, rts = actions2[b], rets2[b]
         for u in range(updates):
-            j = u % NT
-            (ev_a[u - NT] if u >= NT else ev_r).wait(tstream[j])
+            U = base + u
+            j = U % NT
+            if u < NT:
+                ready.wait(tstream[j])
+            if U >= NT:
+                ev_a[U - NT].wait(tstream[j])  # version U - N_T + 1 exists; context j's last gradient was applied
             tctx[j].loss_grad_dev(fr + u * TB * FRAME_BYTES, True, acts.data_ptr() + 4 * u * TB,
-                                  rts.data_ptr() + 8 * u * TB, TB, ring[(u - NT + 1) % R], apply_clip=world == 1)
-            ev_g[u].record(tstream[j])
-            ev_g[u].wait(stream)
+                                  rts.data_ptr() + 8 * u * TB, TB, ring[(U - NT + 1) % R], apply_clip=world == 1)
+            ev_g[U].record(tstream[j])
+            ev_g[U].wait(stream)
             if fused is not None:  # reduce-scatter + RMSProp + all-gather in one kernel
-                fused.apply(ctx, j, ring[u % R], ring[(u + 1) % R])
+                fused.apply(ctx, j, ring[U % R], ring[(U + 1) % R])
             else:
                 if world > 1:  # default hyper: no clip, so nothing to do after the sum
                     dp.allreduce_sum_(tgrad[j], stream)
-                ctx.apply_slots_dev(tctx[j], ring[u % R], ring[(u + 1) % R])
-            ev_a[u].record(stream)
+                ctx.apply_slots_dev(tctx[j], ring[U % R], ring[(U + 1) % R])
+            ev_a[U].record(stream)
         if overlap:
-            ev_p.wait(stream)  # the predictor is done reading its slot
+            ev_p[pos].wait(stream)  # the predictor is done reading its slot
         ctx.copy_slot_dev(ring[updates % R], pred_slot)
+        ev_end[pos].record(stream)
 
     contexts = [ctx] + (tctx if NT > 1 else []) + ([pctx] if overlap else [])
 
@@ -517,6 +543,8 @@ def main():
         probe = (t, int(l) if l else -1)
     ctx.sync()
     graphs = None
+    G = args.graph_steps or next(g for g in range(GMAX, 0, -1) if args.steps % g == 0)  # steps chained per graph
+    assert 1 <= G <= GMAX and args.steps % G == 0, "--graph-steps must divide --steps (and be <= 4)"
     if not args.no_graph and world == 1:
         # one CUDA graph per input set: the whole GA3C iteration replays as a
         # single launch (kernel timing probes are captured as event nodes)
@@ -524,11 +552,13 @@ def main():
         l_cap = launches_all()
         for s in range(sets):
             ctx.graph_begin()
-            step(s)
+            for pos in range(G):
+                step(s * G + pos, pos)
             graphs.append(ctx.graph_end())
-        launches_per_step = (launches_all() - l_cap) // sets
-        for s in range(sets):  # warm the instantiated graphs
-            ctx.graph_launch(graphs[s])
+        launches_per_step = (launches_all() - l_cap) // (sets * G)
+        if not args.no_graph_warm:
+            for s in range(sets):  # warm the instantiated graphs
+                ctx.graph_launch(graphs[s])
         ctx.sync()
     else:
         time_kernel(probe[0], probe[1])  # eager: probe inside the timed region
@@ -544,10 +574,11 @@ def main():
     l0 = launches_all()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for i in range(args.steps):
-        if graphs is not None:
-            ctx.graph_launch(graphs[(args.warmup + i) % sets])
-        else:
+    if graphs is not None:
+        for i in range(args.steps // G):
+            ctx.graph_launch(graphs[i % sets])
+    else:
+        for i in range(args.steps):
             step(args.warmup + i)
     ev1.record(stream)
     ev1.synchronize()
@@ -557,6 +588,16 @@ def main():
         launches = launches_per_step * args.steps
     ms_total = ev0.elapsed_time(ev1)
     clk = clocks.stop()
+    # fingerprint of the parameters the timed steps produced (every update
+    # reads a fixed version, so this is schedule-independent: equal across
+    # --graph-steps settings and runs unless a dependency is missing)
+    th_now = torch.zeros(P, dtype=torch.float32, device="cuda")
+    if NT > 1:
+        class _V:
+            __cuda_array_interface__ = {"shape": (P,), "typestr": "<f4", "version": 3, "strides": None,
+                                        "data": (_abi.slot_theta_ptr(model, ring[0]), False)}
+        th_now = torch.as_tensor(_V(), device="cuda")
+    theta_fingerprint = float(th_now.double().abs().sum().item()) if NT > 1 else None
     probe_steps = args.steps
     if graphs is not None:
         # CUDA events cannot time kernels inside a graph replay: time the probed
@@ -641,7 +682,8 @@ def main():
             "fwd_mflop_per_prediction": fwd_flops_per_sample(args.net) / 1e6,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "ga3c_loop": loop, "gpu_launches": launches,
             "clocks": clk, "kernel_breakdown_ms_per_step": breakdown,
-            "cuda_graph": graphs is not None,
+            "cuda_graph": graphs is not None, "steps_per_graph": G if graphs is not None else None,
+            "theta_fingerprint": theta_fingerprint,
         }
         print(json.dumps(out), flush=True)
     if world > 1:
