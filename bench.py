@@ -86,7 +86,7 @@ def parse():
     p.add_argument("--no-graph-warm", action="store_true",
                    help="skip the graph warm-up launches (theta_fingerprint then depends only on W and K)")
     p.add_argument("--graph-steps", type=int, default=0,
-                   help="steps chained per CUDA graph (0 = the largest of 4..1 dividing --steps)")
+                   help="steps chained per CUDA graph (0 = the largest of 8..1 dividing --steps)")
     p.add_argument("--timeline", default="", help="write a per-launch timeline of one eager step here")
     return p.parse_args()
 
@@ -367,7 +367,7 @@ def main():
     # stream and write out of place into a ring of N_T + 1 device slots, so a
     # trainer never reads a version that is being overwritten.
     NT = args.trainers
-    GMAX = 4  # steps one CUDA graph may chain
+    GMAX = 8  # steps one CUDA graph may chain
     assert hyper.grad_clip_norm == 0.0 or NT == 1, "clipping with several trainers in flight is not wired here"
     # ring of R >= N_T + 1 slots; R divides the updates per step so every
     # step starts from slot 0 (one captured graph per input set)
@@ -544,7 +544,7 @@ def main():
     ctx.sync()
     graphs = None
     G = args.graph_steps or next(g for g in range(GMAX, 0, -1) if args.steps % g == 0)  # steps chained per graph
-    assert 1 <= G <= GMAX and args.steps % G == 0, "--graph-steps must divide --steps (and be <= 4)"
+    assert 1 <= G <= GMAX and args.steps % G == 0, "--graph-steps must divide --steps (and be <= 8)"
     if not args.no_graph and world == 1:
         # one CUDA graph per input set: the whole GA3C iteration replays as a
         # single launch (kernel timing probes are captured as event nodes)

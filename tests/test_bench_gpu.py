@@ -1,9 +1,9 @@
-"""The benchmark's device step chains up to 4 GA3C iterations per CUDA graph,
+"""The benchmark's device step chains up to 8 GA3C iterations per CUDA graph,
 with the update index continuous across them so the first updates of one
 iteration overlap the last of the previous one (bench.py `step`).  Every
 update reads a fixed parameter version (policy lag N_T - 1), so the
 parameters after a run are schedule-independent: the fingerprint must be
-bitwise equal for 1, 2 and 4 iterations per graph -- a missing dependency
+bitwise equal for 1, 2, 4 and 8 iterations per graph -- a missing dependency
 between the chained iterations would show up here."""
 import json
 import os
@@ -31,3 +31,4 @@ def test_chained_graph_steps_are_schedule_independent(extra):
     assert f1 is not None
     assert _fingerprint(2, extra) == f1
     assert _fingerprint(4, extra) == f1
+    assert _fingerprint(8, extra) == f1
