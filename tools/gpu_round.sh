@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/${TAG}_smi.txt
 timeout 600 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_pytest_gpu.txt 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.txt 2>&1
-timeout 900 python bench.py > gpurun_out/${TAG}_bench_dnn_a.json 2> gpurun_out/${TAG}_bench_dnn_a.err
+timeout 900 python bench.py --steps 320 > gpurun_out/${TAG}_bench_dnn_a.json 2> gpurun_out/${TAG}_bench_dnn_a.err
 timeout 900 python bench.py --net large1 --steps 60 > gpurun_out/${TAG}_bench_large1.json 2> gpurun_out/${TAG}_bench_large1.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${TAG}_bench_reference.json 2> gpurun_out/${TAG}_bench_reference.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches_dnn_a.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > /dev/null 2>&1
