@@ -588,6 +588,8 @@ def main():
         launches = launches_per_step * args.steps
     ms_total = ev0.elapsed_time(ev1)
     clk = clocks.stop()
+    if fused is not None:
+        fused.dp.check()  # raises if any fused update timed out waiting for a peer
     # fingerprint of the parameters the timed steps produced (every update
     # reads a fixed version, so this is schedule-independent: equal across
     # --graph-steps settings and runs unless a dependency is missing)

@@ -114,6 +114,9 @@ __global__ void __launch_bounds__(kThreads) dp_rmsprop_kernel(Peers pr, Step s) 
   __shared__ int bail_sh;
   const int tid = threadIdx.x, G = gridDim.x;
   Signal* me = pr.sig[pr.rank];
+  // a previous call timed out: the ranks' epochs no longer agree, so do not
+  // wait again (ga3c_dp_check reports the error; the caller falls back)
+  if (*reinterpret_cast<volatile int*>(&me->err)) return;
   const unsigned long long ep = *reinterpret_cast<volatile unsigned long long*>(&me->epoch) + 1ull;
   const int W = pr.world;
   std::size_t per = (s.n + W - 1) / W;
