@@ -149,3 +149,31 @@ def test_fused_update_clips_the_reduced_gradient():
     for q in range(W):
         np.testing.assert_allclose(out[q], want, rtol=1e-6, atol=1e-9)
     assert np.array_equal(out[0], out[1])  # replicas identical
+
+
+@pytest.mark.timeout(120)
+def test_missing_peer_times_out_instead_of_hanging():
+    """Rank 1 never calls: rank 0's barrier gives up after 2 s, ga3c_dp_check
+    reports it, and later calls return at once instead of waiting again."""
+    import time
+
+    import torch
+
+    import pyoracle as O
+    from paper_1611_06256_b200 import _abi
+
+    W = 2
+    spec_o = O.make_spec((12, 12, 2), [(4, 4, 2)], [8], 4)
+    models, rings, ctxs, dps, th, g0 = _setup(W, spec_o, _abi.default_hyper())
+    gp = [c.grad_ptr() for c in ctxs]
+    tp = [_abi.slot_theta_ptr(models[q], rings[q][1]) for q in range(W)]
+    sp = [d.signal_ptr() for d in dps]
+    t0 = time.time()
+    dps[0].apply(ctxs[0], None, rings[0][0], rings[0][1], gp, tp, sp)
+    with pytest.raises(_abi.GA3CError):
+        dps[0].check()
+    assert 1.5 < time.time() - t0 < 30
+    t1 = time.time()
+    dps[0].apply(ctxs[0], None, rings[0][0], rings[0][1], gp, tp, sp)
+    torch.cuda.synchronize()
+    assert time.time() - t1 < 1.0
