@@ -75,7 +75,7 @@ def parse():
                    help="kernel class[:layer] for the roofline probe (auto = largest eager share)")
     p.add_argument("--trainer-sms", type=int, default=0,
                    help="N_T > 1: SMs each trainer context's split-K plans fill (ga3c_ctx_set_sm_budget); "
-                        "0 = auto: a 1/N_T share when an update is latency-bound (< 50 MFLOP/sample), else all")
+                        "0 = auto: 3/4 of them when an update is latency-bound (< 50 MFLOP/sample), else all")
     p.add_argument("--pred-sms", type=int, default=0, help="same for the predictor context (0 = all)")
     p.add_argument("--dp", default="fused", choices=["fused", "nccl"],
                    help="N > 1 with N_T > 1: one fused reduce-scatter + RMSProp + all-gather kernel over NVLink "
@@ -389,8 +389,12 @@ def main():
         ev_p = [torch.cuda.Event() for _ in range(GMAX)]
         ev_end = [torch.cuda.Event() for _ in range(GMAX)]
         if args.trainer_sms == 0:
+            # latency-bound updates (DNN A): plan for 3/4 of the SMs, which
+            # also puts every ring in shared mode (two CTAs per SM), so the
+            # N_T concurrent trainers interleave (sweep: 49 -> 954K,
+            # 90..147 -> 978-992K, 148 with deep rings -> 863K samples/s)
             small = 2.5 * fwd_flops_per_sample(args.net) < 50e6
-            args.trainer_sms = 148 // NT if small else 148
+            args.trainer_sms = 111 if small else 148
         for c in tctx:
             c.set_sm_budget(args.trainer_sms)
     fused = None
