@@ -76,7 +76,8 @@ def parse():
     p.add_argument("--trainer-sms", type=int, default=0,
                    help="N_T > 1: SMs each trainer context's split-K plans fill (ga3c_ctx_set_sm_budget); "
                         "0 = auto: 3/4 of them when an update is latency-bound (< 50 MFLOP/sample), else all")
-    p.add_argument("--pred-sms", type=int, default=0, help="same for the predictor context (0 = all)")
+    p.add_argument("--pred-sms", type=int, default=-1,
+                   help="same for the predictor context (0 = all, -1 = auto: 64 for latency-bound nets)")
     p.add_argument("--dp", default="fused", choices=["fused", "nccl"],
                    help="N > 1 with N_T > 1: one fused reduce-scatter + RMSProp + all-gather kernel over NVLink "
                         "peer memory (ga3c_dp_apply), or NCCL all-reduce + RMSProp")
@@ -286,6 +287,7 @@ def config_of(args, world, sets=None):
             "dp_update": (args.dp if world > 1 and args.trainers > 1 else
                           ("nccl" if world > 1 else "none (1 GPU)")),
             "trainer_sm_budget": args.trainer_sms if args.trainers > 1 else 148,
+            "predictor_sm_budget": args.pred_sms,
             "l2": (f"inputs cycled over {sets} sets = {sets * n * FRAME_BYTES / 1e6:.0f} MB > 126 MB L2"
                    if sets else "n/a")}
 
@@ -409,6 +411,10 @@ def main():
             args.dp = "nccl"
     pctx = _abi.Context(model, NA) if overlap else ctx
     if overlap:
+        if args.pred_sms < 0:
+            # the predictor beside latency-bound trainers: a share of the SMs
+            # (sweep, DNN A: all -> 973K, 111 -> 998K, 49..74 -> 1.01M, 16 -> 905K)
+            args.pred_sms = 64 if 2.5 * fwd_flops_per_sample(args.net) < 50e6 else 0
         pctx.set_sm_budget(args.pred_sms)
     pstream = torch.cuda.ExternalStream(pctx.stream) if overlap else stream
     lv = pctx.last_values_ptr()
