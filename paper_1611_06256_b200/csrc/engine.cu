@@ -618,6 +618,29 @@ template <typename T>
 int fc_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const void* x, float* out,
                int B, bool keep_partials, long long in_stride) {
   const long long ld = in_stride > 0 ? in_stride : L.in;
+  static const bool direct = env_flag("GA3C_FC_DIRECT");
+  if (keep_partials && direct) {
+    // (A/B, off by default) batch rows x output units, split-K reduced inside
+    // a cluster (DSMEM), bias + ReLU in the epilogue: h is final, the heads
+    // read it directly.  Measured slower for DNN A (0.90M vs 1.01M samples/s:
+    // 16 CTAs x 11 k-chunks vs 42 CTAs x 2 plus the heads' reduction).
+    Seg X = dense_seg(x, B, ld, L.in, sizeof(T) == 1);
+    Seg W = dense_seg(theta + L.w_off, L.out, L.in, L.in, false);
+    X.rows = B;
+    W.rows = L.out;
+    if (seg_ok(X, B) && seg_ok(W, L.out) && L.in % 32 == 0 && (L.w_off % 4) == 0 && L.out % 4 == 0 &&
+        L.out <= 256) {
+      const int bn = tc_bn(L.out);
+      const int tiles = ((B + 127) / 128) * ((L.out + bn - 1) / bn);
+      const int chunks = L.in / 32;
+      int ks = no_cluster() ? 1 : std::max(1, std::min({8, chunks, split_sms(c) / std::max(1, tiles)}));
+      const int kc = ((chunks + ks - 1) / ks) * 32;
+      ks = (L.in + kc - 1) / kc;
+      TcEpiArgs e{theta + L.b_off, out, L.out};
+      tc_dispatch<T, float, TC_EPI_BIAS_RELU>(c, GA3C_K_FC_FWD, li, bn, X, W, B, L.out, L.in, ks, kc, e);
+      return 0;
+    }
+  }
   {
     Seg X = dense_seg(x, B, ld, L.in, sizeof(T) == 1);
     Seg W = dense_seg(theta + L.w_off, L.out, L.in, L.in, false);
@@ -966,7 +989,7 @@ int run_forward(ga3c_ctx* c, const float* theta, const void* d_in, bool u8, int 
     }
   } else {
     h = c->act[lo.n_trunk - 1];
-    if (!lo.trunk[lo.n_trunk - 1].is_conv) {
+    if (!lo.trunk[lo.n_trunk - 1].is_conv && n_split > 0) {  // 0: the FC wrote h itself
       part = region(c, 0);
       fc_bias = theta + lo.trunk[lo.n_trunk - 1].b_off;
     }
