@@ -649,7 +649,12 @@ int fc_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const vo
       const int bn = tc_bn(B);
       const int tiles = ((L.out + 127) / 128) * ((B + bn - 1) / bn);
       const int chunks = L.in / 32;
+      static const int force = [] {  // A/B: GA3C_FC_SPLITS caps the K splits
+        const char* e = std::getenv("GA3C_FC_SPLITS");
+        return e ? std::atoi(e) : 0;
+      }();
       int splits = std::max(1, std::min(chunks, split_sms(c) / std::max(1, tiles)));
+      if (force > 0) splits = std::min(splits, force);
       while (splits > 1 && static_cast<std::size_t>(splits) * B * L.out > kRegionFloats) --splits;
       const int kc = ((chunks + splits - 1) / splits) * 32;
       splits = (L.in + kc - 1) / kc;
