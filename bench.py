@@ -555,7 +555,10 @@ def main():
     graphs = None
     G = args.graph_steps or next(g for g in range(GMAX, 0, -1) if args.steps % g == 0)  # steps chained per graph
     assert 1 <= G <= GMAX and args.steps % G == 0, "--graph-steps must divide --steps (and be <= 8)"
-    if not args.no_graph and world == 1:
+    # graphs on every rank when the data-parallel exchange is the fused
+    # kernel (a plain launch, capturable; every rank replays the same
+    # sequence); the NCCL fallback runs eagerly
+    if not args.no_graph and (world == 1 or fused is not None):
         # one CUDA graph per input set: the whole GA3C iteration replays as a
         # single launch (kernel timing probes are captured as event nodes)
         graphs = []
