@@ -718,7 +718,7 @@ void wgrad_tc_launch_v(ga3c_ctx* c, int li, const WgradArgs& a, dim3 grid, int t
     attr_set = true;
   }
   Launch l(c, tag, li);
-  if (a.mode == 1 && grid.y > 1)  // split-K reduced inside a cluster
+  if ((a.mode == 1 || a.cluster) && grid.y > 1)  // split-K reduced inside a cluster
     pdl_launch_cluster(c->cur, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, dim3(1, grid.y, 1), a);
   else
     pdl_launch(c->cur, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, a);
@@ -764,7 +764,31 @@ bool layer_wgrad_tc(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const
   while (splits > 1 && static_cast<std::size_t>(splits) * L.out * (L.in + 1) > kRegionFloats) --splits;
   const int kc = ((chunks + splits - 1) / splits) * 32;
   splits = (npix + kc - 1) / kc;
-  WgradArgs a{X, dout, L.out, L.out, L.in, npix, kc, part, gm, splits == 1, 0, nullptr, nullptr, 0};
+  // GA3C_WGRAD_CLUSTER (A/B, off): at most 8 splits, reduced through DSMEM
+  // in the kernel (dtheta stored directly) instead of partials + a reduction
+  // kernel.  Correct (parity green) but measured much slower -- DNN A 0.81M
+  // vs 1.01M, large s1 57K vs 104K samples/s: the MN pipeline is bound by
+  // per-chunk load latency at shallow ring depths, so long CTAs lose to many
+  // short split CTAs plus the reduction kernel.
+  static const bool clu = env_flag("GA3C_WGRAD_CLUSTER");
+  bool cl = false;
+  if (clu && splits > 1) {
+    const int s8 = std::min(splits, 8);
+    const int kc8 = ((chunks + s8 - 1) / s8) * 32;
+    splits = (npix + kc8 - 1) / kc8;
+    cl = splits > 1;
+    if (cl) {
+      WgradArgs a8{X, dout, L.out, L.out, L.in, npix, kc8, part, gm, 1, 0, nullptr, nullptr, 0, 1};
+      dim3 grid8(mtiles, splits, ntiles);
+      switch (bn) {
+        case 32: wgrad_tc_launch<TX, 32>(c, li, a8, grid8); break;
+        case 64: wgrad_tc_launch<TX, 64>(c, li, a8, grid8); break;
+        default: wgrad_tc_launch<TX, 128>(c, li, a8, grid8); break;
+      }
+      return true;
+    }
+  }
+  WgradArgs a{X, dout, L.out, L.out, L.in, npix, kc, part, gm, splits == 1, 0, nullptr, nullptr, 0, 0};
   dim3 grid(mtiles, splits, ntiles);
   switch (bn) {
     case 32: wgrad_tc_launch<TX, 32>(c, li, a, grid); break;
@@ -822,7 +846,7 @@ bool fc_dgrad_tc(ga3c_ctx* c, int li, const Layer& L, const float* theta, const 
   int ks = no_cluster() || no_mn ? 1 : std::max(1, std::min({8, chunks, split_sms(c) / mtiles}));
   const int kc = ((chunks + ks - 1) / ks) * 32;
   ks = (L.out + kc - 1) / kc;
-  WgradArgs a{W, doutT, ldT, B, L.in, L.out, kc, nullptr, GradMap{}, 0, 1, din, gate, L.in};
+  WgradArgs a{W, doutT, ldT, B, L.in, L.out, kc, nullptr, GradMap{}, 0, 1, din, gate, L.in, 0};
   dim3 grid(mtiles, ks, 1);
   switch (bn) {
     case 32: wgrad_tc_launch<float, 32>(c, li, a, grid, GA3C_K_DGRAD); break;

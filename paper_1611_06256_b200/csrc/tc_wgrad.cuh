@@ -37,6 +37,10 @@ struct WgradArgs {
   float* out;
   const float* gate;
   int ldo;
+  // mode 0 with grid.y > 1 splits: reduce the partial tiles (and the bias
+  // column) through DSMEM inside a (1, grid.y, 1) cluster and store dtheta
+  // directly (no split-K partials, no reduction kernel)
+  int cluster;
 };
 
 namespace detail {

@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_mn_ws_kernel(WgradArgs a) {
   __shared__ uint64_t ready[pipe::kMaxStages], done[pipe::kMaxStages], acc_bar;
   __shared__ uint32_t tmem_base_sh;
   __shared__ float bias_red[4 * kProducers];
+  __shared__ float bias_cl[BN];  // cluster split: this rank's bias partials
   uint8_t* smem = detail::align1024(smem_raw);
   const uint32_t sbase = tc::smem_u32(smem);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_mn_ws_kernel(WgradArgs a) {
   const int nchunks = (pe - pb + 31) / 32;
   const bool do_bias = blockIdx.x == 0 && a.mode == 0;
   // mode 1 with grid.y > 1: split-K over a (1, grid.y, 1) cluster
-  const bool csplit = a.mode == 1 && gridDim.y > 1;
+  const bool csplit = (a.mode == 1 || a.cluster) && gridDim.y > 1;
 
   const int xp = tid >> 3, xv = tid & 7;
   int xcoff[4];
@@ -620,7 +621,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_mn_ws_kernel(WgradArgs a) {
         float sacc = 0.f;
         for (int r = 0; r < R; ++r) sacc += bias_red[r * BN + tid];
         const int co = n0 + tid;
-        if (co < a.cout) {
+        if (csplit) {
+          bias_cl[tid] = sacc;  // reduced across the cluster below
+        } else if (co < a.cout) {
           if (a.direct)
             a.gm.store(co, a.Kw, sacc);
           else
@@ -635,6 +638,20 @@ __global__ void __launch_bounds__(kThreads, 1) tc_mn_ws_kernel(WgradArgs a) {
     // tiles stay readable until every rank is done
     if (warp == kMmaWarp) tc::cluster_sync();
     tc::cluster_sync();
+    if (a.mode == 0 && blockIdx.x == 0) {
+      // bias column: rank 0 sums the ranks' partials in rank order
+      if (tc::cluster_rank() == 0 && tid < BN && n0 + tid < a.cout) {
+        const uint32_t off = tc::smem_u32(bias_cl + tid);
+        float t = 0.f;
+        for (int k = 0; k < static_cast<int>(gridDim.y); ++k) {
+          float y;
+          asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(y) : "r"(tc::mapa(off, k)) : "memory");
+          t += y;
+        }
+        a.gm.store(n0 + tid, a.Kw, t);
+      }
+      tc::cluster_sync();  // the ranks' bias partials stay readable until read
+    }
   }
   TRACE(3);
   tc::tc_fence_before();
