@@ -615,16 +615,23 @@ def main():
     theta_fingerprint = float(th_now.double().abs().sum().item()) if NT > 1 else None
     probe_steps = args.steps
     if graphs is not None:
-        # CUDA events cannot time kernels inside a graph replay: time the probed
-        # kernel with events on its stream over K eager steps right after
+        # the probed kernel timed inside the real step: one more G-step graph,
+        # captured with event-record nodes around every launch of the probed
+        # kernel class (on the stream it runs on), replayed once after the
+        # timed region
         time_kernel(probe[0], probe[1])
-        probe_steps = max(3, min(args.steps, 50))
-        for i in range(probe_steps):
-            busy()
-            step(args.warmup + i)
-            ctx.sync()
+        ctx.graph_begin()
+        for pos in range(G):
+            step(pos, pos)
+        pg = ctx.graph_end()
+        ctx.graph_launch(pg)
+        ctx.sync()
+        torch.cuda.synchronize()
+        probe_steps = G
     probe_ms, probe_n = kernel_time()
     time_kernel("none")
+    probe_pass = ("one extra replay of a graph of the timed steps with event nodes around the probed "
+                  "kernel's launches" if graphs is not None else "inside the timed region")
     if world > 1:
         t = torch.tensor([ms_total], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -666,9 +673,7 @@ def main():
                  "kernel": f"{probe[0]}[layer {probe[1]}]", "launches": probe_n,
                  "avg_launch_us": 1e3 * probe_ms / max(1, probe_n),
                  "share_of_step": probe_ms / (ms_step * probed_steps),
-                 "probe_pass": ("eager steps after the graph-timed region, each queued behind a spin so "
-                                "launches run back to back" if graphs is not None
-                                else "inside the timed region"),
+                 "probe_pass": probe_pass,
                  "peak_source": f"{peak_src} ({'HBM copy' if probe[0] == 'rmsprop' else 'cuBLAS bf16 burst'})"})
 
     # ---- end to end through the C ABI with host buffers ----

@@ -332,6 +332,7 @@ void join_from(ga3c_ctx* c, cudaStream_t s) {
 struct Launch {
   ga3c_ctx* c;
   bool on;
+  bool ext = false;
   Launch(ga3c_ctx* c_, int tag, int layer) : c(c_) {
     on = c->timed_tag == GA3C_K_ALL ||
          (c->timed_tag == tag && (c->timed_layer < 0 || c->timed_layer == layer));
@@ -344,12 +345,15 @@ struct Launch {
       const int sid = c->cur == c->stream ? 0 : (c->cur == c->side[0] ? 1 : 2);
       c->ev_meta.resize(c->ev_used / 2 + 1);
       c->ev_meta[c->ev_used / 2] = tag | ((layer + 1) << 8) | (sid << 16);
-      cudaEventRecord(c->events[c->ev_used], c->cur);
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(c->cur, &cs);
+      ext = cs == cudaStreamCaptureStatusActive;  // captured: an event-record node replayed with the graph
+      cudaEventRecordWithFlags(c->events[c->ev_used], c->cur, ext ? cudaEventRecordExternal : cudaEventRecordDefault);
     }
   }
   ~Launch() {
     if (on) {
-      cudaEventRecord(c->events[c->ev_used + 1], c->cur);
+      cudaEventRecordWithFlags(c->events[c->ev_used + 1], c->cur, ext ? cudaEventRecordExternal : cudaEventRecordDefault);
       c->ev_used += 2;
     }
     c->launches++;
@@ -2003,6 +2007,13 @@ int ga3c_sample_actions_dev(ga3c_ctx* c, const float* d_pi, const double* d_u, i
 
 int ga3c_ctx_time_kernel(ga3c_ctx* c, int tag, int layer) {
   if (!c || tag < 0 || tag > GA3C_K_ALL) return GA3C_INVALID_ARGUMENT;
+  // events are created up front: a graph capture of the bracketed launches
+  // must not create them (it records them as event nodes)
+  while (tag != GA3C_K_NONE && c->events.size() < 4096) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) break;
+    c->events.push_back(e);
+  }
   c->timed_tag = tag;
   c->timed_layer = layer;
   c->ev_used = 0;
