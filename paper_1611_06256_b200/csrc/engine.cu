@@ -730,7 +730,15 @@ void wgrad_tc_launch_v(ga3c_ctx* c, int li, const WgradArgs& a, dim3 grid, int t
 
 template <typename TX, int BN>
 void wgrad_tc_launch(ga3c_ctx* c, int li, const WgradArgs& a, dim3 grid, int tag = GA3C_K_WGRAD) {
-  const int cap = ring_cap(c, (std::min(a.kc, a.npix) + 31) / 32, static_cast<long long>(grid.x) * grid.y * grid.z);
+  // A/B: GA3C_MN_CAP forces the ring cap of the MN GEMMs (DNN A: deep 0.85M,
+  // cap 3 0.95M, cap 2 / default 1.01M samples/s -- occupancy beats depth)
+  static const int force = [] {
+    const char* e = std::getenv("GA3C_MN_CAP");
+    return e ? std::atoi(e) : -1;
+  }();
+  const int cap = force >= 0 ? force
+                             : ring_cap(c, (std::min(a.kc, a.npix) + 31) / 32,
+                                        static_cast<long long>(grid.x) * grid.y * grid.z);
 #define GA3C_F(C) wgrad_tc_launch_v<TX, BN, C>(c, li, a, grid, tag)
   GA3C_CAP_SWITCH(cap, GA3C_F)
 #undef GA3C_F
