@@ -660,7 +660,6 @@ rmsprop_kernel(const float* __restrict__ th_in, const float* __restrict__ g_in,
                std::size_t n, const int* __restrict__ flag, unsigned long long* version, float alpha,
                float oma, float eta, float eps) {
   pdl_enter();
-  if (*flag) return;
   const std::size_t n4 = n / 4;
   const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
   const std::size_t t0 = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -669,6 +668,21 @@ rmsprop_kernel(const float* __restrict__ th_in, const float* __restrict__ g_in,
   const float4* D = reinterpret_cast<const float4*>(d);
   float4* TO = reinterpret_cast<float4*>(th_out);
   float4* GO = reinterpret_cast<float4*>(g_out);
+  if (*flag) {
+    // rejected (nnet.cpp:299-301): an out-of-place destination receives the
+    // source unchanged, so the slot ring still holds the latest parameters
+    if (th_out != th_in) {
+      for (std::size_t i = t0; i < n4; i += stride) {
+        TO[i] = T[i];
+        GO[i] = G[i];
+      }
+      for (std::size_t i = n4 * 4 + t0; i < n; i += stride) {
+        th_out[i] = th_in[i];
+        g_out[i] = g_in[i];
+      }
+    }
+    return;
+  }
   for (std::size_t i = t0; i < n4; i += stride) {
     float4 t = T[i], g = G[i];
     const float4 dd = __ldcs(D + i);

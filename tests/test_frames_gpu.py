@@ -103,3 +103,33 @@ def test_ring_apply_matches_published_apply():
     ctx2.apply_rmsprop(d)
     pi2, v2, _ = ctx2.forward(states)
     assert np.array_equal(pi1, pi2) and np.array_equal(v1, v2)
+
+
+def test_ring_apply_rejected_step_leaves_source_in_destination():
+    """A non-finite gradient rejects the step (nnet.cpp:299-301); out of place
+    the destination slot must then hold the unchanged source parameters."""
+    import torch
+    _abi, m1, ctx1, _ = setup()
+    rng = np.random.default_rng(4)
+    states = rng.integers(0, 256, (8, H * W * 4), dtype=np.uint8)
+    acts = rng.integers(0, 6, 8).astype(np.int32)
+    rets = np.full(8, 3e38)  # finite returns whose gradient overflows fp32
+    d, _ = ctx1.loss_grad(states, acts, rets)
+    assert not np.all(np.isfinite(d))
+    ring = m1.ring(3)
+
+    def theta(slot):
+        class _V:
+            __cuda_array_interface__ = {"shape": (m1.P,), "typestr": "<f4", "version": 3, "strides": None,
+                                        "data": (_abi.slot_theta_ptr(m1, slot), False)}
+        return torch.as_tensor(_V(), device="cuda").cpu().numpy().copy()
+
+    # make the destination differ from the source first: a valid step into it
+    ctx2 = _abi.Context(m1, 8)
+    ctx2.loss_grad(states, acts, rng.standard_normal(8))
+    ctx2.apply_slots_dev(ctx2, ring[0], ring[2])
+    ctx2.sync()
+    assert not np.array_equal(theta(ring[2]), theta(ring[1]))
+    ctx1.apply_slots_dev(ctx1, ring[1], ring[2])  # rejected: ctx1's gradient is non-finite
+    ctx1.sync()
+    assert np.array_equal(theta(ring[2]), theta(ring[1]))
