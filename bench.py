@@ -748,7 +748,7 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
     NA, T, TB = args.agents, args.tmax, args.train_batch
     n = NA * T
     updates = n // TB
-    k = args.e2e_steps or max(3, min(args.steps, 30))
+    k = args.e2e_steps or max(3, min(args.steps, 60))
     hs = min(sets, 2)
     px = FRAME[0] * FRAME[1]
     # newest frame of every agent at every step: the last channel of the stacked synthetic states
