@@ -263,6 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_u8conv_kernel(ConvArgs a) {
   if (warp < kMmaWarp) {
     // ------------------------------------------------ A expansion
     const bool fast = a.k == 8 && nparts == 2;  // 8x8 kernels over 4 channels (GA3C conv1)
+    const bool aligned16 = (a.s * a.cin) % 16 == 0 && rowb % 16 == 0;
     for (int i = 0; i < ntiles; ++i) {
       const int st = i & 1, fs = i % NFP;
       const uint32_t fp = sFp + fs * a.fp_bytes;
@@ -288,13 +289,26 @@ __global__ void __launch_bounds__(kThreads, 1) tc_u8conv_kernel(ConvArgs a) {
           const uint32_t src0 = fp + (second ? b0r : 0) + (oy * a.s - (second ? s1.y0 : s0.y0)) * rowb +
                                 ox * a.s * a.cin;
           if (fast) {
-            // all 32 loads in flight before the 8 stores
+            // all loads in flight before the 8 stores; 16-byte loads when every
+            // pixel's run starts 16-byte aligned (stride * cin % 16 == 0)
             uint32_t v[8][4];
+            if (aligned16) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const uint32_t src = src0 + (half + 2 * (u >> 1)) * rowb + (u & 1) * 16;
+              for (int u = 0; u < 8; ++u) {
+                const uint32_t src = src0 + (half + 2 * (u >> 1)) * rowb + (u & 1) * 16;
+                const float4 w = pipe::lds128(src);
+                v[u][0] = __float_as_uint(w.x);
+                v[u][1] = __float_as_uint(w.y);
+                v[u][2] = __float_as_uint(w.z);
+                v[u][3] = __float_as_uint(w.w);
+              }
+            } else {
 #pragma unroll
-              for (int q = 0; q < 4; ++q) v[u][q] = pipe::lds32(src + 4 * q);
+              for (int u = 0; u < 8; ++u) {
+                const uint32_t src = src0 + (half + 2 * (u >> 1)) * rowb + (u & 1) * 16;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[u][q] = pipe::lds32(src + 4 * q);
+              }
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
