@@ -529,12 +529,7 @@ bool u8_conv_persistent(ga3c_ctx* c, int li, const Layer& L, const float* theta,
   const int fp_stages = std::min(u8c::kFpMaxStages, u8c::kFpRegion / fp_bytes);
   if (fp_stages < 2) return false;
   u8c::ConvArgs a{x, bstride, theta + L.w_off, theta + L.b_off, out, L.cout, B, L.ih, L.iw, L.cin, L.k,
-                  L.stride, L.oh, L.ow, L.cout, L.in, (B * P + 127) / 128, fp_bytes, fp_stages, 0};
-  static const int dbg = [] {
-    const char* e = std::getenv("GA3C_U8C_DBG");
-    return e ? std::atoi(e) : 0;
-  }();
-  a.dbg = dbg;
+                  L.stride, L.oh, L.ow, L.cout, L.in, (B * P + 127) / 128, fp_bytes, fp_stages};
   const int bn = L.cout <= 16 ? 16 : 32;
   dim3 grid(static_cast<unsigned>(std::min(a.tiles, split_sms(c))), (L.cout + bn - 1) / bn, 1);
   if (bn == 16)

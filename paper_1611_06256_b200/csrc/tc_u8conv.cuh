@@ -63,7 +63,6 @@ struct ConvArgs {
   int B, ih, iw, cin, k, s, oh, ow, N, K;
   int tiles;  // ceil(B * oh * ow / 128)
   int fp_bytes, fp_stages;  // footprint ring geometry (fp_bytes % 128 == 0)
-  int dbg;    // timing experiments only (GA3C_U8C_DBG): 1 skip expansion, 2 skip stores, 4 skip MMAs
 };
 
 // kind::i8 instruction descriptor: c_format S32 (2), a_format u8 (0),
@@ -277,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_u8conv_kernel(ConvArgs a) {
       const int b0r = (((s0.y1 - s0.y0 + 1) * rowb) + 15) & ~15;
       // two threads per pixel row r (alternate kh); a (kh, 16-byte part)
       // unit is 16 contiguous footprint bytes -> one SW128 16-byte unit
-      if (!(a.dbg & 1)) {
+      {
         const int r = tid & 127, half = tid >> 7;
         const int m = m0 + r;
         const uint32_t drow = at + static_cast<uint32_t>(((r >> 3) << 10) | ((r & 7) << 7));
@@ -349,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_u8conv_kernel(ConvArgs a) {
         tc::tc_fence_after();
         const uint32_t at = sA + st * S::A_BYTES;
         const uint32_t acc = tmem + st * S::ACC;
-        for (int c = 0; c < ((a.dbg & 4) ? 0 : kch); ++c) {
+        for (int c = 0; c < kch; ++c) {
           const uint32_t ac = at + c * (128 * 128), wc = sW + c * (S::NW * 128);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)  // 4 x K=32 (32 bytes) per 128-byte row
@@ -415,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_u8conv_kernel(ConvArgs a) {
       // the quad's 32 rows are 32 consecutive pixels: this warp's column half, float4 rows
       const int mq = (static_cast<int>(blockIdx.x) + i * static_cast<int>(gridDim.x)) * 128 + quad * 32;
       constexpr int V4 = HB / 4;
-      for (int e = lane; e < ((a.dbg & 2) ? 0 : 32 * V4); e += 32) {
+      for (int e = lane; e < 32 * V4; e += 32) {
         const int rr = e / V4, q4 = e - rr * V4;
         const int m = mq + rr;
         const int col = cb + 4 * q4;
