@@ -80,7 +80,7 @@ class FusedUpdate:
     same trainer contexts (by position) and ring slots (by id); their device
     buffers are exchanged once as CUDA IPC handles over the process group."""
 
-    def __init__(self, model, grad_ctxs, slots, rank, world, ctas=32):
+    def __init__(self, model, grad_ctxs, slots, rank, world, ctas=64):
         import torch.distributed as dist
 
         from . import _abi
