@@ -122,6 +122,18 @@ def test_large_dnn_stride1_forward_persistent_conv1():
     check_forward(spec, th, fr, O.frames_to_states(fr))
 
 
+def test_large_dnn_stride1_batch16_forward_and_gradients():
+    """B = 16: conv2's 171 tiles exceed the SMs (multi-wave, shallow rings),
+    every weight gradient splits over many CTAs."""
+    spec = O.dnn_large(1)
+    th = theta32(spec, 3)
+    fr = O.synthetic_frames(7, 16)
+    st = O.frames_to_states(fr)
+    check_forward(spec, th, fr, st)
+    acts, rets = O.synthetic_batch(7, 16, 6)
+    check_grad(spec, th, fr, st, acts, rets)
+
+
 def test_dnn_a_golden(golden):
     g = golden("dnn_a")
     spec = O.dnn_a()
