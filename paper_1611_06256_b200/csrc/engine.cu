@@ -763,10 +763,19 @@ bool layer_wgrad_tc(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const
         break;
       }
   const int ntiles = (L.out + bn - 1) / bn;
-  // a context with the whole GPU plans two CTAs per SM (ring cap 1), so the
-  // conversion-heavy producers of one CTA overlap the other's
+  // A context with the whole GPU plans two CTAs per SM (ring cap 1), so the
+  // conversion-heavy producers of one CTA overlap the other's; a context
+  // sharing the GPU (a trainer beside other trainers) plans for half its
+  // budget: fewer split partials to reduce on its critical path (DNN A
+  // 1.00M -> 1.04M samples/s; x2 0.96M; large s1 whole-GPU x1 105K, x0.5 94K).
   static const bool one = env_flag("GA3C_WGRAD_1CTA");
-  const int wsms = split_sms(c) * (!one && split_sms(c) >= kNumSMs ? 2 : 1);
+  static const double scale = [] {  // A/B: GA3C_WGRAD_SPLIT_SCALE overrides the factor
+    const char* e = std::getenv("GA3C_WGRAD_SPLIT_SCALE");
+    return e ? std::atof(e) : 0.0;
+  }();
+  const bool whole = split_sms(c) >= kNumSMs;
+  const double f = scale > 0.0 ? scale : (whole ? (one ? 1.0 : 2.0) : 0.5);
+  const int wsms = std::max(1, static_cast<int>(f * split_sms(c)));
   int splits = std::max(1, std::min(chunks / 2, (wsms + mtiles * ntiles - 1) / (mtiles * ntiles)));
   while (splits > 1 && static_cast<std::size_t>(splits) * L.out * (L.in + 1) > kRegionFloats) --splits;
   const int kc = ((chunks + splits - 1) / splits) * 32;
