@@ -306,6 +306,16 @@ int ring_cap(const ga3c_ctx* c, int n, long long ctas) {
     default: F(0); break;       \
   }
 
+// SMs a cluster split-K plan (conv forward, FC input gradient) targets:
+// GA3C_CLUSTER_SCALE x the context's budget (A/B; default 1).
+int cluster_sms(const ga3c_ctx* c) {
+  static const double f = [] {
+    const char* e = std::getenv("GA3C_CLUSTER_SCALE");
+    return e && std::atof(e) > 0.0 ? std::atof(e) : 1.0;
+  }();
+  return std::max(1, static_cast<int>(f * split_sms(c)));
+}
+
 bool no_cluster() {
   static const bool v = env_flag("GA3C_NO_CLUSTER");
   return v;
@@ -552,7 +562,7 @@ bool u8_conv_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, co
   const int M = B * L.pixels();
   const int tiles = ((M + 127) / 128) * ((L.cout + bn - 1) / bn);
   const int chunks = L.in / 64;
-  int ks = no_cluster() ? 1 : std::max(1, std::min({8, chunks, split_sms(c) / std::max(1, tiles)}));
+  int ks = no_cluster() ? 1 : std::max(1, std::min({8, chunks, cluster_sms(c) / std::max(1, tiles)}));
   const int kc = ((chunks + ks - 1) / ks) * 64;
   ks = (L.in + kc - 1) / kc;
   const int cap = ring_cap(c, (std::min(kc, L.in) + 63) / 64, static_cast<long long>(tiles) * ks);
@@ -596,7 +606,7 @@ void conv_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const
       // partial tiles are summed through DSMEM in the epilogue.
       const int tiles = ((M + 127) / 128) * ((L.cout + bn - 1) / bn);
       const int chunks = L.in / 32;
-      int ks = no_cluster() ? 1 : std::max(1, std::min({8, chunks, split_sms(c) / std::max(1, tiles)}));
+      int ks = no_cluster() ? 1 : std::max(1, std::min({8, chunks, cluster_sms(c) / std::max(1, tiles)}));
       const int kc = ((chunks + ks - 1) / ks) * 32;
       ks = (L.in + kc - 1) / kc;
       tc_dispatch<T, float, TC_EPI_BIAS_RELU>(c, GA3C_K_CONV_FWD, li, bn, A, W, M, L.cout, L.in, ks, kc, e);
@@ -632,7 +642,7 @@ int fc_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const vo
       const int bn = tc_bn(L.out);
       const int tiles = ((B + 127) / 128) * ((L.out + bn - 1) / bn);
       const int chunks = L.in / 32;
-      int ks = no_cluster() ? 1 : std::max(1, std::min({8, chunks, split_sms(c) / std::max(1, tiles)}));
+      int ks = no_cluster() ? 1 : std::max(1, std::min({8, chunks, cluster_sms(c) / std::max(1, tiles)}));
       const int kc = ((chunks + ks - 1) / ks) * 32;
       ks = (L.in + kc - 1) / kc;
       TcEpiArgs e{theta + L.b_off, out, L.out};
@@ -859,7 +869,7 @@ bool fc_dgrad_tc(ga3c_ctx* c, int li, const Layer& L, const float* theta, const 
   const int mtiles = (L.in + 127) / 128;
   const int chunks = (L.out + 31) / 32;
   static const bool no_mn = env_flag("GA3C_NO_CLUSTER_MN");
-  int ks = no_cluster() || no_mn ? 1 : std::max(1, std::min({8, chunks, split_sms(c) / mtiles}));
+  int ks = no_cluster() || no_mn ? 1 : std::max(1, std::min({8, chunks, cluster_sms(c) / mtiles}));
   const int kc = ((chunks + ks - 1) / ks) * 32;
   ks = (L.out + kc - 1) / kc;
   WgradArgs a{W, doutT, ldT, B, L.in, L.out, kc, nullptr, GradMap{}, 0, 1, din, gate, L.in, 0};
