@@ -60,6 +60,10 @@ struct Slot {
   float* g = nullptr;
   std::uint64_t version = 0;
   int refs = 0;
+  // written by an asynchronous apply still in flight: device readers wait on
+  // `ready`, host readers synchronise on it
+  cudaEvent_t ready = nullptr;
+  bool pending = false;
 };
 
 }  // namespace
@@ -73,6 +77,9 @@ struct ga3c_model {
   std::mutex update_m;  // serializes writers                   (pipeline.cpp:40)
   std::vector<Slot> slots;
   int cur = 0;
+  // completion of the last asynchronous apply: the next writer orders after it
+  cudaEvent_t apply_done = nullptr;
+  bool apply_pending = false;
   std::mutex err_m;
   std::string last_error;
   void set_error(const std::string& e) {
@@ -120,6 +127,9 @@ struct ga3c_ctx {
   double* r_out = nullptr;
   std::size_t r_cap = 0, r_seg_cap = 0;
   int* h_flag = nullptr;  // pinned
+  // non-finite flag of this context's last gradient, read back by the
+  // host-buffer gradient calls (-1 = unknown: apply must read it itself)
+  int grad_flag = -1;
   // staging for the host-buffer calls' small inputs and outputs: packed into
   // pinned memory and moved with ONE async copy each way (pageable
   // cudaMemcpyAsync is synchronous and costs microseconds per call)
@@ -1204,6 +1214,17 @@ int set_device(ga3c_model* m) {
   return GA3C_OK;
 }
 
+// Orders c's stream after an asynchronous apply still writing slot s.
+void wait_slot(ga3c_ctx* c, int s) {
+  const Slot& sl = c->m->slots[s];
+  if (sl.pending && !c->capturing) cudaStreamWaitEvent(c->stream, sl.ready, 0);
+}
+
+// Host side: waits until slot s is written.
+void sync_slot(ga3c_model* m, int s) {
+  if (m->slots[s].pending) cudaEventSynchronize(m->slots[s].ready);
+}
+
 // Allocates (or reuses) a slot with no readers that is not the current one.
 // Caller holds update_m and read_m.
 int free_slot_locked(ga3c_model* m) {
@@ -1334,10 +1355,13 @@ ga3c_model* ga3c_model_create(const ga3c_net_spec* spec, const ga3c_hyper* hp, i
 void ga3c_model_destroy(ga3c_model* m) {
   if (!m) return;
   cudaSetDevice(m->device);
+  cudaDeviceSynchronize();  // asynchronous applies may still be writing slots
   for (auto& s : m->slots) {
     cudaFree(s.theta);
     cudaFree(s.g);
+    if (s.ready) cudaEventDestroy(s.ready);
   }
+  if (m->apply_done) cudaEventDestroy(m->apply_done);
   delete m;
 }
 
@@ -1346,6 +1370,7 @@ int ga3c_model_load(ga3c_model* m, const float* theta, const float* g, uint64_t 
   auto set_err = [&](const std::string& e) { m->set_error(e); };
   if (set_device(m)) return GA3C_CUDA_ERROR;
   std::lock_guard<std::mutex> ulk(m->update_m);
+  if (m->apply_pending) GA3C_CUDA(cudaEventSynchronize(m->apply_done));  // no write in flight
   int f;
   {
     std::lock_guard<std::mutex> lk(m->read_m);
@@ -1371,6 +1396,7 @@ int ga3c_model_read(ga3c_model* m, float* theta, float* g, uint64_t* version) {
   int s;
   uint64_t v;
   if (ga3c_snapshot_acquire(m, &s, &v)) return GA3C_INVALID_ARGUMENT;
+  sync_slot(m, s);
   const std::size_t bytes = m->lo.total * sizeof(float);
   int rc = GA3C_OK;
   if (theta && cudaMemcpy(theta, m->slots[s].theta, bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
@@ -1546,6 +1572,7 @@ int ga3c_forward_dev(ga3c_ctx* c, int slot, const void* d_states, int states_are
   ga3c_model* m = c->m;
   auto set_err = [&](const std::string& e) { m->set_error(e); };
   const float* theta = m->slots[slot].theta;
+  wait_slot(c, slot);
   run_forward(c, theta, d_states, states_are_u8 != 0, B, state_stride);
   const int A = m->lo.n_actions;
   if (d_pi && d_pi != c->pi32)
@@ -1579,7 +1606,10 @@ static int forward_host(ga3c_ctx* c, int slot, const void* states, bool u8, int 
     const std::size_t bytes = dim * B * (u8 ? 1 : sizeof(float));
     if (cudaMemcpyAsync(c->d_in, states, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
       rc = GA3C_CUDA_ERROR;
-    if (!rc) run_forward(c, m->slots[s].theta, c->d_in, u8, B);
+    if (!rc) {
+      wait_slot(c, s);
+      run_forward(c, m->slots[s].theta, c->d_in, u8, B);
+    }
     const int A = m->lo.n_actions;
     if (!rc && cudaMemcpyAsync(pi, c->pi32, sizeof(float) * B * A, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
       rc = GA3C_CUDA_ERROR;
@@ -1614,6 +1644,8 @@ int ga3c_loss_grad_dev(ga3c_ctx* c, int slot, const void* d_states, int states_a
     return GA3C_INVALID_ARGUMENT;
   ga3c_model* m = c->m;
   auto set_err = [&](const std::string& e) { m->set_error(e); };
+  wait_slot(c, slot);
+  c->grad_flag = -1;
   run_loss_grad(c, m->slots[slot].theta, d_states, states_are_u8 != 0, d_actions, d_returns, B,
                 apply_clip != 0, state_stride);
   GA3C_CUDA(cudaGetLastError());
@@ -1642,8 +1674,13 @@ static int loss_grad_host(ga3c_ctx* c, int slot, const void* states, bool u8,
       cudaMemcpyAsync(c->d_actions, actions, sizeof(int32_t) * B, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
       cudaMemcpyAsync(c->d_rets, rets, sizeof(double) * B, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
     rc = GA3C_CUDA_ERROR;
-  if (!rc)
+  c->grad_flag = -1;
+  if (!rc) {
+    wait_slot(c, s);
     run_loss_grad(c, m->slots[s].theta, c->d_in, u8, c->d_actions, c->d_rets, B, apply_clip != 0);
+  }
+  if (!rc && cudaMemcpyAsync(c->h_flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+    rc = GA3C_CUDA_ERROR;
   if (!rc && dtheta &&
       cudaMemcpyAsync(dtheta, c->grad, sizeof(float) * m->lo.total, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
     rc = GA3C_CUDA_ERROR;
@@ -1655,6 +1692,7 @@ static int loss_grad_host(ga3c_ctx* c, int slot, const void* states, bool u8,
     rc = GA3C_CUDA_ERROR;
     set_err(std::string("loss_grad: ") + cudaGetErrorString(e));
   }
+  if (!rc) c->grad_flag = *c->h_flag;
   if (pinned_here) ga3c_snapshot_release(m, s);
   return rc;
 }
@@ -1708,6 +1746,18 @@ int ga3c_apply_rmsprop(ga3c_ctx* c, const float* dtheta, int* applied, uint64_t*
   auto set_err = [&](const std::string& e) { m->set_error(e); };
   if (set_device(m)) return GA3C_CUDA_ERROR;
   const std::size_t n = m->lo.total;
+  // The gradient's non-finite flag is already on the host when this
+  // context's last gradient came from a host-buffer call (which waited for
+  // it): then the step is applied asynchronously -- RMSProp is enqueued on
+  // this context's stream, the destination slot is published at once with
+  // an event that every later reader of the slot (device or host) orders
+  // after, and the call returns without a device round trip.
+  const bool async = !dtheta && c->grad_flag >= 0 && !c->capturing;
+  if (async && c->grad_flag) {  // rejected (nnet.cpp:299-301): nothing changes
+    c->grad_flag = -1;
+    if (applied) *applied = 0;
+    return GA3C_NOT_APPLIED;
+  }
   std::lock_guard<std::mutex> ulk(m->update_m);
   int src, dst;
   {
@@ -1724,6 +1774,29 @@ int ga3c_apply_rmsprop(ga3c_ctx* c, const float* dtheta, int* applied, uint64_t*
     unpin();
     return GA3C_OUT_OF_MEMORY;
   }
+  // every write orders after the previous asynchronous apply (it read its
+  // source and wrote its destination, either of which may be src / dst here)
+  if (m->apply_pending) GA3C_CUDA(cudaStreamWaitEvent(c->stream, m->apply_done, 0));
+  if (async) {
+    c->grad_flag = -1;
+    Slot& d = m->slots[dst];
+    if (!d.ready) GA3C_CUDA(cudaEventCreateWithFlags(&d.ready, cudaEventDisableTiming));
+    if (!m->apply_done) GA3C_CUDA(cudaEventCreateWithFlags(&m->apply_done, cudaEventDisableTiming));
+    launch_rmsprop(c, m->slots[src], d, nullptr);
+    GA3C_CUDA(cudaEventRecord(d.ready, c->stream));
+    GA3C_CUDA(cudaEventRecord(m->apply_done, c->stream));
+    {
+      std::lock_guard<std::mutex> lk(m->read_m);
+      d.pending = true;
+      m->apply_pending = true;
+      d.version = m->slots[src].version + 1;
+      if (applied_on) *applied_on = m->slots[src].version;
+      m->cur = dst;
+      m->slots[src].refs--;
+    }
+    if (applied) *applied = 1;
+    return GA3C_OK;
+  }
   if (dtheta) {
     // host gradient: upload and recompute the non-finite flag on the device
     if (cudaMemcpyAsync(c->grad, dtheta, n * sizeof(float), cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
@@ -1735,6 +1808,7 @@ int ga3c_apply_rmsprop(ga3c_ctx* c, const float* dtheta, int* applied, uint64_t*
     Launch l(c, GA3C_K_OTHER, -1);
     pdl_launch(c->cur, check_finite_kernel, dim3(kNumSMs), dim3(256), 0, c->grad, n, c->flag);
   }
+  c->grad_flag = -1;
   launch_rmsprop(c, m->slots[src], m->slots[dst], nullptr);
   cudaMemcpyAsync(c->h_flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
   cudaError_t e = cudaStreamSynchronize(c->stream);
@@ -1742,6 +1816,12 @@ int ga3c_apply_rmsprop(ga3c_ctx* c, const float* dtheta, int* applied, uint64_t*
     unpin();
     set_err(std::string("apply_rmsprop: ") + cudaGetErrorString(e));
     return GA3C_CUDA_ERROR;
+  }
+  {
+    // everything this call ordered after has completed
+    std::lock_guard<std::mutex> lk(m->read_m);
+    m->apply_pending = false;
+    for (auto& sl : m->slots) sl.pending = false;
   }
   if (*c->h_flag) {
     unpin();
@@ -2178,7 +2258,10 @@ static int loss_grad_segments(ga3c_ctx* c, int slot, const void* states, bool u8
   const double* d_boot = sg.put(bootstrap, n_seg);
   double* h_scal = scalars ? sg.take<double>(3) : nullptr;
   double* h_ret = returns_out ? sg.take<double>(B) : nullptr;
-  if (!d_act || !d_rew || !d_off || !d_term || !d_boot || (scalars && !h_scal) || (returns_out && !h_ret)) {
+  int* h_flg = sg.take<int>(1);
+  c->grad_flag = -1;
+  if (!d_act || !d_rew || !d_off || !d_term || !d_boot || (scalars && !h_scal) || (returns_out && !h_ret) ||
+      !h_flg) {
     if (pinned_here) ga3c_snapshot_release(m, s);
     set_err("loss_grad_segments: batch exceeds the context's staging area");
     return GA3C_INVALID_ARGUMENT;
@@ -2193,8 +2276,11 @@ static int loss_grad_segments(ga3c_ctx* c, int slot, const void* states, bool u8
       pdl_launch(c->cur, returns_kernel, dim3((n_seg + 127) / 128), dim3(128), 0, d_rew, d_off, n_seg, d_term,
                  d_boot, gamma, c->d_rets);
     }
+    wait_slot(c, s);
     run_loss_grad(c, m->slots[s].theta, c->d_in, u8, d_act, c->d_rets, B, apply_clip != 0);
-    if (scalars &&
+    if (cudaMemcpyAsync(h_flg, c->flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+      rc = GA3C_CUDA_ERROR;
+    if (!rc && scalars &&
         cudaMemcpyAsync(h_scal, c->scal_sum, sizeof(double) * 3, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
       rc = GA3C_CUDA_ERROR;
     if (!rc && returns_out &&
@@ -2206,6 +2292,7 @@ static int loss_grad_segments(ga3c_ctx* c, int slot, const void* states, bool u8
     rc = GA3C_CUDA_ERROR;
     set_err(std::string("loss_grad_segments: ") + cudaGetErrorString(e));
   }
+  if (!rc) c->grad_flag = *h_flg;
   if (!rc && scalars) std::memcpy(scalars, h_scal, sizeof(double) * 3);
   if (!rc && returns_out) std::memcpy(returns_out, h_ret, sizeof(double) * B);
   if (pinned_here) ga3c_snapshot_release(m, s);
@@ -2286,6 +2373,7 @@ int ga3c_predict_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* ne
                    reinterpret_cast<uint32_t*>(f->ring), f->frame_px, f->history,
                    reinterpret_cast<const uint32_t*>(newf), d_idx, n, reinterpret_cast<uint32_t*>(dense));
       }
+      wait_slot(c, s);
       run_forward(c, m->slots[s].theta, dense, true, n);
       if (cudaMemcpyAsync(h_pi, c->pi32, sizeof(float) * n * A, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
           cudaMemcpyAsync(h_v, c->v, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
