@@ -54,8 +54,14 @@ struct DgShape {
   static constexpr int BPER = (BE + ws::kProducers - 1) / ws::kProducers;
 };
 
+// Register cap: two 288-thread CTAs per SM (ring caps 1-2) need <= 96
+// registers per thread -- each SM sub-partition holds 5 of the 18 warps in
+// 16K registers.  Uncapped (104) the occupancy limit was one CTA per SM
+// (ncu launch__occupancy_limit_registers = 1) and large s1's conv2 dgrad
+// took 112 us instead of 71.
 template <int BN, int CAP>
-__global__ void __launch_bounds__(ws::kThreads, 1) tc_dgrad_kernel(DgradArgs a) {
+__global__ void __launch_bounds__(ws::kThreads) __maxnreg__((CAP == 1 || CAP == 2) && BN <= 64 ? 96 : 255)
+    tc_dgrad_kernel(DgradArgs a) {
   using S = DgShape<BN, CAP>;
   static_assert(BN % 16 == 0 && 2 * BN <= 256, "N-concatenated tile exceeds the MMA N limit");
   constexpr int kP = ws::kProducers;

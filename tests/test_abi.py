@@ -95,3 +95,40 @@ def test_no_cpu_fallback_without_gpu():
 
 def O_spec_to_abi():
     return _spec_c(O.make_spec(4, [], [8], 3))
+
+
+def _resource_usage():
+    """(demangled kernel name, registers) for every kernel in the library."""
+    import subprocess
+    so = os.path.join(ROOT, "paper_1611_06256_b200", "libga3c_b200.so")
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--dump-resource-usage", so], capture_output=True,
+                         text=True).stdout
+    mangled = re.findall(r"Function (\S+):\s*\n\s*REG:(\d+)", out)
+    names = subprocess.run(["c++filt"], input="\n".join(m for m, _ in mangled), capture_output=True,
+                           text=True).stdout.splitlines()
+    return [(n, int(r)) for n, (_, r) in zip(names, mangled)]
+
+
+def test_two_cta_kernels_fit_two_per_sm():
+    """Ring caps 1 and 2 plan two 288-thread warp-specialised CTAs per SM
+    (engine.cu ring_cap).  Registers are allocated per SM sub-partition: 18
+    warps put 5 on one sub-partition, so 16K / (5 * 32) -> at most 96 per
+    thread.  Above that the hardware runs one CTA per SM and the planned
+    overlap silently disappears (large s1 conv2 dgrad: 71 -> 112 us)."""
+    rows = _resource_usage()
+    checked = 0
+    for name, reg in rows:
+        m = re.match(r"void ga3c::(dg::tc_dgrad_kernel|ws::tc_mn_ws_kernel|ws::tc_kk_ws_kernel)<(.*)>\(", name)
+        if not m:
+            continue
+        args = [a.strip() for a in m.group(2).split(",")]
+        if m.group(1).endswith("tc_dgrad_kernel"):
+            bn, cap = int(args[0]), int(args[1])
+        elif m.group(1).endswith("tc_mn_ws_kernel"):
+            bn, cap = int(args[1]), int(args[2])
+        else:
+            bn, cap = int(args[2]), int(args[4])
+        if cap in (1, 2) and bn <= 64:
+            checked += 1
+            assert reg <= 96, f"{name}: {reg} registers -> one CTA per SM at ring cap {cap}"
+    assert checked >= 10
