@@ -68,7 +68,9 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=0)
     p.add_argument("--e2e-windows", type=int, default=3)
     p.add_argument("--e2e-trainers", type=int, default=4, help="trainer threads in the e2e leg (0 = serial)")
-    p.add_argument("--e2e-predictors", type=int, default=2, help="predictor threads in the e2e leg (N_P)")
+    # N_P = 1 measured best (DNN A e2e, median of 3 windows: N_P/N_T 1/4 644-665K, 2/4 584-610K, 3/4 514K,
+    # 2/6 546K; large s1 1/3 102K, 2/4 99K): more host threads contend for the GIL and the 16 vCPUs
+    p.add_argument("--e2e-predictors", type=int, default=1, help="predictor threads in the e2e leg (N_P)")
     p.add_argument("--trainers", type=int, default=3,
                    help="trainer contexts in flight in the device step (N_T, policy lag N_T - 1 updates)")
     p.add_argument("--cpu-seconds", type=float, default=6.0)
@@ -844,8 +846,10 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
     store.close()
     # training queue of train_queue_cap = 16 segments-batches (the
     # reference's knob, knobs.hpp:15, default 32): the predictor runs up to
-    # a step ahead of the trainers, so the store keeps three steps of stacks
-    store = _abi.Frames(model, NA, 3 * T + 2)
+    # two steps ahead of the oldest update still training (one step queued,
+    # one being predicted), three if a trainer thread stalls while the
+    # others drain a whole step, so the store keeps four steps of stacks
+    store = _abi.Frames(model, NA, 4 * T + 2)
     q = queue.Queue(maxsize=updates)
 
     def trainer(j):
@@ -890,8 +894,11 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
         acts = np.zeros((NA, T), np.int32)
         slots = np.zeros((NA, T), np.int32)
         v = np.zeros(NA, np.float64)
-        for f in [pool.submit(predict_group, g, s, pt, acts, slots, v) for g in range(NP)]:
-            f.result()
+        if NP == 1:  # the main thread is the predictor: no hand-off
+            predict_group(0, s, pt, acts, slots, v)
+        else:
+            for f in [pool.submit(predict_group, g, s, pt, acts, slots, v) for g in range(NP)]:
+                f.result()
         return s, acts, slots, v
 
     dt = dt_serial
