@@ -562,37 +562,48 @@ splitk_grad8_kernel(const float* __restrict__ part, int n_split, int M, int N, G
 // Tensor-core weight-gradient partials: weights [split][cout][Kw] (16-byte
 // aligned rows) followed by the bias sums [split][cout].  Output element i of
 // the virtual [cout][Kw+1] matrix (bias in the last column).
-__device__ __forceinline__ float wg_part(const float* __restrict__ part, int s, int n_split, int cout,
-                                         int Kw, int co, int kk) {
-  return kk < Kw ? part[(static_cast<std::size_t>(s) * cout + co) * Kw + kk]
-                 : part[static_cast<std::size_t>(n_split) * cout * Kw + static_cast<std::size_t>(s) * cout + co];
+// Element (co, kk) of split k sits at base + k * stride (weights, then the
+// bias block).  32-bit index math (cout * (Kw + 1) < 2^31, checked by the
+// host), done before the PDL wait so it overlaps the producer's tail.
+struct SplitCol {
+  std::size_t base, stride;
+};
+__device__ __forceinline__ SplitCol split_col(int n_split, int cout, int Kw, int co, int kk) {
+  if (kk < Kw)
+    return {static_cast<std::size_t>(co) * Kw + kk, static_cast<std::size_t>(cout) * Kw};
+  return {static_cast<std::size_t>(n_split) * cout * Kw + co, static_cast<std::size_t>(cout)};
 }
 
 __global__ void splitk_wgrad_kernel(const float* __restrict__ part, int n_split, int cout, int Kw,
                                     GradMap g) {
+  const unsigned N = static_cast<unsigned>(Kw) + 1u;
+  const unsigned total = static_cast<unsigned>(cout) * N;
+  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int co = static_cast<int>(i / N), kk = static_cast<int>(i - (i / N) * N);
+  const SplitCol c = split_col(n_split, cout, Kw, co, kk);
   pdl_enter();
-  const int N = Kw + 1;
-  const std::size_t total = static_cast<std::size_t>(cout) * N;
-  const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= total) return;
-  const int co = static_cast<int>(i / N), kk = static_cast<int>(i % N);
   float s = 0.0f;
-  for (int k = 0; k < n_split; ++k) s += wg_part(part, k, n_split, cout, Kw, co, kk);
+#pragma unroll 4
+  for (int k = 0; k < n_split; ++k) s += part[c.base + k * c.stride];
   g.store(co, kk, s);
 }
 
 __global__ void __launch_bounds__(256)
 splitk_wgrad8_kernel(const float* __restrict__ part, int n_split, int cout, int Kw, GradMap g) {
-  pdl_enter();
   __shared__ float red[8][33];
-  const int N = Kw + 1;
-  const std::size_t total = static_cast<std::size_t>(cout) * N;
+  const unsigned N = static_cast<unsigned>(Kw) + 1u;
+  const unsigned total = static_cast<unsigned>(cout) * N;
   const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
-  const std::size_t i = static_cast<std::size_t>(blockIdx.x) * 32 + lane;
-  const int co = static_cast<int>(i / N), kk = static_cast<int>(i % N);
+  const unsigned i = blockIdx.x * 32u + lane;
+  const int co = static_cast<int>(i / N), kk = static_cast<int>(i - (i / N) * N);
+  const SplitCol c = split_col(n_split, cout, Kw, co, kk);
+  pdl_enter();
   float s = 0.0f;
-  if (i < total)
-    for (int k = q; k < n_split; k += 8) s += wg_part(part, k, n_split, cout, Kw, co, kk);
+  if (i < total) {
+#pragma unroll 4
+    for (int k = q; k < n_split; k += 8) s += part[c.base + k * c.stride];
+  }
   red[q][lane] = s;
   __syncthreads();
   if (q == 0 && i < total) {
