@@ -308,6 +308,15 @@ int ring_cap(const ga3c_ctx* c, int n, long long ctas) {
   return (ctas > kNumSMs || split_sms(c) < kNumSMs) ? 1 : 0;
 }
 
+// Raise a kernel's dynamic shared memory limit once per instantiation.  The
+// static's initialisation is thread-safe: predictor and trainer threads may
+// make their first launches concurrently.
+#define GA3C_SMEM_ONCE(kern, bytes)                                                                         \
+  static const bool smem_once_ = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                                       bytes),                                              \
+                                  true);                                                                    \
+  (void)smem_once_
+
 #define GA3C_CAP_SWITCH(cap, F) \
   switch (cap) {                \
     case 1: F(1); break;        \
@@ -395,11 +404,7 @@ void tc_launch_v(ga3c_ctx* c, int tag, int layer, const Seg& A, const Seg& B, in
                  int kc, const TcEpiArgs& epi) {
   using S = ws::KKShape<TA, TB, BN, CAP>;
   auto kern = ws::tc_kk_ws_kernel<TA, TB, BN, MODE, CAP>;
-  static bool attr_set = false;  // idempotent; racing setters write the same value
-  if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
-    attr_set = true;
-  }
+  GA3C_SMEM_ONCE(kern, S::SMEM);
   dim3 grid((M + 127) / 128, splits, (N + BN - 1) / BN);
   Launch l(c, tag, layer);
   if (MODE == TC_EPI_BIAS_RELU && splits > 1)  // split-K reduced inside a cluster
@@ -497,11 +502,7 @@ void u8_conv_launch(ga3c_ctx* c, int li, const Seg& A, const Seg& W, int M, int 
   constexpr int NS = pipe::ring_depth(CAP, S::STAGE);
   constexpr int SMEM = NS * S::STAGE + 1024;
   auto kern = bf::tc_u8_fwd_kernel<BN, CAP>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    attr_set = true;
-  }
+  GA3C_SMEM_ONCE(kern, SMEM);
   dim3 grid((M + 127) / 128, ks, (N + BN - 1) / BN);
   Launch l(c, GA3C_K_CONV_FWD, li);
   if (ks > 1)
@@ -517,11 +518,7 @@ template <int BN>
 void u8_persist_launch(ga3c_ctx* c, int li, const u8c::ConvArgs& a, dim3 grid) {
   using S = u8c::Shape<BN>;
   auto kern = u8c::tc_u8conv_kernel<BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
-    attr_set = true;
-  }
+  GA3C_SMEM_ONCE(kern, S::SMEM);
   Launch l(c, GA3C_K_CONV_FWD, li);
   pdl_launch(c->cur, kern, grid, dim3(u8c::kThreads), S::SMEM, a);
 }
@@ -731,11 +728,7 @@ template <typename TX, int BN, int CAP>
 void wgrad_tc_launch_v(ga3c_ctx* c, int li, const WgradArgs& a, dim3 grid, int tag) {
   using S = ws::MNShape<TX, BN, CAP>;
   auto kern = ws::tc_mn_ws_kernel<TX, BN, CAP>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
-    attr_set = true;
-  }
+  GA3C_SMEM_ONCE(kern, S::SMEM);
   Launch l(c, tag, li);
   if ((a.mode == 1 || a.cluster) && grid.y > 1)  // split-K reduced inside a cluster
     pdl_launch_cluster(c->cur, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, dim3(1, grid.y, 1), a);
@@ -898,11 +891,7 @@ template <int BN, int CAP>
 void dgrad_tc_launch(ga3c_ctx* c, int li, const dg::DgradArgs& a, dim3 grid) {
   using S = dg::DgShape<BN, CAP>;
   auto kern = dg::tc_dgrad_kernel<BN, CAP>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
-    attr_set = true;
-  }
+  GA3C_SMEM_ONCE(kern, S::SMEM);
   Launch l(c, GA3C_K_DGRAD, li);
   pdl_launch(c->cur, kern, grid, dim3(ws::kThreads), S::SMEM, a);
 }
@@ -960,10 +949,10 @@ void layer_dgrad(ga3c_ctx* c, int li, const Layer& L, const float* theta, const 
     const int npix = B * L.ih * L.iw;
     const std::size_t smem = static_cast<std::size_t>(L.cout) * L.k * L.k * 16 * sizeof(float);
     auto kern = L.cout == 32 ? conv_dgrad_32x4s2_kernel : conv_dgrad_64x4s2_kernel;
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[L.cout == 64]) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr_set[L.cout == 64] = true;
+    if (L.cout == 32) {
+      GA3C_SMEM_ONCE(conv_dgrad_32x4s2_kernel, 200 * 1024);
+    } else {
+      GA3C_SMEM_ONCE(conv_dgrad_64x4s2_kernel, 200 * 1024);
     }
     Launch l(c, GA3C_K_DGRAD, li);
     pdl_launch(c->cur, kern, dim3((npix + 63) / 64, L.cin / 16), dim3(256), smem, dout, theta + L.w_off,
@@ -972,11 +961,7 @@ void layer_dgrad(ga3c_ctx* c, int li, const Layer& L, const float* theta, const 
       static_cast<std::size_t>(L.cout) * L.k * L.k * 16 * sizeof(float) <= 200 * 1024) {
     const int npix = B * L.ih * L.iw;
     const std::size_t smem = static_cast<std::size_t>(L.cout) * L.k * L.k * 16 * sizeof(float);
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(conv_dgrad16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr_set = true;
-    }
+    GA3C_SMEM_ONCE(conv_dgrad16_kernel, 200 * 1024);
     Launch l(c, GA3C_K_DGRAD, li);
     pdl_launch(c->cur, conv_dgrad16_kernel, dim3(dim3((npix + 63) / 64, L.cin / 16)), dim3(256), smem, 
         dout, theta + L.w_off, gate, din, B, L.ih, L.iw, L.cin, L.oh, L.ow, L.cout, L.k, L.stride);
