@@ -767,14 +767,25 @@ bool layer_wgrad_tc(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const
   const int chunks = (npix + 31) / 32;
   // Narrowest N tile that still covers the outputs in one wave when the
   // reduction is too short to split (FC at trainer batch sizes): more CTAs,
-  // each with a smaller epilogue.
+  // each with a smaller epilogue.  When no tile fits one wave (large s1 FC,
+  // 145 row tiles), the narrowest: small CTAs at ring cap 2 interleave with
+  // the other trainers' kernels (large s1 105.5K -> 106.6K samples/s with
+  // 32 vs 128, although the kernel alone is 24 vs 22 us).
   int bn = L.out <= 32 ? 32 : (L.out <= 64 ? 64 : 128);
-  if (chunks < 4)
+  if (chunks < 4) {
+    int pick = 32;
     for (int cand = 32; cand < bn; cand *= 2)
       if (mtiles * ((L.out + cand - 1) / cand) <= split_sms(c)) {
-        bn = cand;
+        pick = cand;
         break;
       }
+    bn = std::min(bn, pick);
+  }
+  static const int force_bn = [] {  // A/B: GA3C_WGRAD_BN forces the N tile (32/64/128)
+    const char* e = std::getenv("GA3C_WGRAD_BN");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (chunks < 4 && (force_bn == 32 || force_bn == 64 || force_bn == 128)) bn = force_bn;
   const int ntiles = (L.out + bn - 1) / bn;
   // A context with the whole GPU plans two CTAs per SM (ring cap 1), so the
   // conversion-heavy producers of one CTA overlap the other's; a context
