@@ -92,7 +92,20 @@ def parse():
     p.add_argument("--graph-steps", type=int, default=0,
                    help="steps chained per CUDA graph (0 = the largest of 8..1 dividing --steps)")
     p.add_argument("--timeline", default="", help="write a per-launch timeline of one eager step here")
-    return p.parse_args()
+    args = p.parse_args()
+    # Automatic SM budgets, resolved here so both arms print the same config.
+    # Latency-bound updates (DNN A): trainers plan for 3/4 of the SMs, which
+    # also puts every ring in shared mode (two CTAs per SM), so the N_T
+    # concurrent trainers interleave (sweep: 49 -> 954K, 90..147 ->
+    # 978-992K, 148 with deep rings -> 863K samples/s); the predictor beside
+    # them plans for a share (all -> 973K, 111 -> 998K, 49..74 -> 1.01M,
+    # 16 -> 905K).
+    small = 2.5 * fwd_flops_per_sample(args.net) < 50e6
+    if args.trainer_sms == 0:
+        args.trainer_sms = 111 if small else 148
+    if args.pred_sms < 0:
+        args.pred_sms = 64 if small else 0
+    return args
 
 
 # ----------------------------------------------------------------- helpers
@@ -290,7 +303,7 @@ def config_of(args, world, sets=None):
             "dp_update": (args.dp if world > 1 and args.trainers > 1 else
                           ("nccl" if world > 1 else "none (1 GPU)")),
             "trainer_sm_budget": args.trainer_sms if args.trainers > 1 else 148,
-            "predictor_sm_budget": args.pred_sms,
+            "predictor_sm_budget": (args.pred_sms if args.trainers > 1 and not args.no_overlap else None),
             "l2": (f"inputs cycled over {sets} sets = {sets * n * FRAME_BYTES / 1e6:.0f} MB > 126 MB L2"
                    if sets else "n/a")}
 
@@ -393,13 +406,6 @@ def main():
         ev_r = torch.cuda.Event()
         ev_p = [torch.cuda.Event() for _ in range(GMAX)]
         ev_end = [torch.cuda.Event() for _ in range(GMAX)]
-        if args.trainer_sms == 0:
-            # latency-bound updates (DNN A): plan for 3/4 of the SMs, which
-            # also puts every ring in shared mode (two CTAs per SM), so the
-            # N_T concurrent trainers interleave (sweep: 49 -> 954K,
-            # 90..147 -> 978-992K, 148 with deep rings -> 863K samples/s)
-            small = 2.5 * fwd_flops_per_sample(args.net) < 50e6
-            args.trainer_sms = 111 if small else 148
         for c in tctx:
             c.set_sm_budget(args.trainer_sms)
     fused = None
@@ -414,10 +420,6 @@ def main():
             args.dp = "nccl"
     pctx = _abi.Context(model, NA) if overlap else ctx
     if overlap:
-        if args.pred_sms < 0:
-            # the predictor beside latency-bound trainers: a share of the SMs
-            # (sweep, DNN A: all -> 973K, 111 -> 998K, 49..74 -> 1.01M, 16 -> 905K)
-            args.pred_sms = 64 if 2.5 * fwd_flops_per_sample(args.net) < 50e6 else 0
         pctx.set_sm_budget(args.pred_sms)
     pstream = torch.cuda.ExternalStream(pctx.stream) if overlap else stream
     lv = pctx.last_values_ptr()

@@ -1,0 +1,40 @@
+"""bench.py's JSON contract on CPU: the reference arm (the oracle port on the
+host cores) runs here, and its line carries the keys the driver reads, with
+the same config the GPU arm prints (SM budgets resolved in parse())."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+
+
+def test_param_counts_match_the_layouts():
+    assert bench.param_count("dnn_a") == 677943
+    assert bench.param_count("large1") == 4794503
+    assert abs(bench.fwd_flops_per_sample("dnn_a") / 1e6 - 5.934592) < 1e-6
+
+
+def test_reference_arm_json_contract():
+    if not os.path.exists(os.path.join(ROOT, "oracle", "libga3c_oracle.so")):
+        pytest.skip("oracle not built (run __graft_entry__.build())")
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
+    assert d["e2e"]["value"] == d["value"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    cb = d["cpu_baseline"]
+    assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["value"] == d["value"]
+    cfg = d["config"]
+    assert cfg["net"] == "dnn_a" and cfg["updates_per_step"] == 16 and cfg["params"] == 677943
+    # the GPU arm resolves the same automatic budgets
+    assert cfg["trainer_sm_budget"] == 111 and cfg["predictor_sm_budget"] == 64
