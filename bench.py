@@ -753,7 +753,9 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
     NA, T, TB = args.agents, args.tmax, args.train_batch
     n = NA * T
     updates = n // TB
-    k = args.e2e_steps or max(3, min(args.steps, 100))
+    # windows of 100 steps whatever --steps is: the host-threaded leg needs
+    # ~0.1 s windows to be stable (10-step windows: 0.57-0.61M vs 0.72M)
+    k = args.e2e_steps or 100
     hs = min(sets, 2)
     px = FRAME[0] * FRAME[1]
     # newest frame of every agent at every step: the last channel of the stacked synthetic states
