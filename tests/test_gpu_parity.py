@@ -424,3 +424,28 @@ def test_copy_slot_publishes_parameters():
         __cuda_array_interface__ = {"shape": (m.P,), "typestr": "<f4", "version": 3, "strides": None,
                                     "data": (_abi.slot_theta_ptr(m, b), False)}
     assert np.array_equal(torch.as_tensor(_V(), device="cuda").cpu().numpy(), th)
+
+
+def test_apply_rmsprop_dev_in_place_and_reject():
+    """ga3c_apply_rmsprop_dev (the graph-capturable in-place apply) matches the
+    fp32 restatement bitwise on the context gradient, and a non-finite
+    gradient leaves theta, g and the version untouched (nnet.cpp:299-301;
+    the kernel issues the reject-flag load beside the data loads)."""
+    spec = O.make_spec(4, [], [8], 3)
+    m, ctx = make(spec)
+    th = theta32(spec, 11)
+    m.load(th)
+    st = np.array([[0.5, 0.0, -0.5, 1.0], [1.0, -1.0, 0.25, 0.0]], np.float32)
+    d, _ = ctx.loss_grad(st, [2, 0], [1.5, -0.5])
+    v0 = ctx.dev_version()
+    ctx.apply_rmsprop_dev()
+    t1, g1, _ = m.read()
+    rt, rg, _ = O.rmsprop_update_f32(HYPER, th, np.zeros_like(th), d)
+    # the device loop counts its updates on the device (no host publish)
+    assert np.array_equal(t1, rt) and np.array_equal(g1, rg) and ctx.dev_version() == v0 + 1
+    # overflow to inf in the forward pass -> non-finite gradient -> rejected
+    big = np.full((1, 4), 3e38, np.float32)
+    ctx.loss_grad(big, [1], [1.0], want_grad=False)
+    ctx.apply_rmsprop_dev()
+    t2, g2, _ = m.read()
+    assert np.array_equal(t2, t1) and np.array_equal(g2, g1) and ctx.dev_version() == v0 + 1
