@@ -844,7 +844,7 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
     ctx_t = [_abi.Context(model, max(NA, TB)) for _ in range(args.e2e_trainers)]
     # trainer threads share the GPU like the device step's trainer contexts:
     # the same SM budget rule (e2e 550K -> 574K samples/s for DNN A)
-    e2e_sms = 111 if 2.5 * fwd_flops_per_sample(args.net) < 50e6 else 148
+    e2e_sms = int(os.environ.get("GA3C_E2E_SMS", 0)) or (111 if 2.5 * fwd_flops_per_sample(args.net) < 50e6 else 148)
     for c_ in ctx_t:
         c_.set_sm_budget(e2e_sms)
     store.close()
