@@ -669,8 +669,8 @@ def main():
     traffic, traffic_src = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f).get(f"{probe[0]}[{probe[1]}]" if probe[1] >= 0 else probe[0])
-        if tr and args.net == "dnn_a":
+            tr = json.load(f).get(args.net, {}).get(f"{probe[0]}[{probe[1]}]" if probe[1] >= 0 else probe[0])
+        if tr:
             traffic, traffic_src = tr["bytes_per_launch"], f"{tr['launch']}; {tr['capture']}"
     except (OSError, ValueError, KeyError):
         pass
