@@ -38,3 +38,19 @@ def test_reference_arm_json_contract():
     assert cfg["net"] == "dnn_a" and cfg["updates_per_step"] == 16 and cfg["params"] == 677943
     # the GPU arm resolves the same automatic budgets
     assert cfg["trainer_sm_budget"] == 111 and cfg["predictor_sm_budget"] == 64
+
+
+def test_reference_arm_under_torchrun_prints_one_line():
+    """N > 1: the driver launches the reference arm with torchrun; rank 0
+    alone runs the CPU path and prints, the other ranks exit 0."""
+    if not os.path.exists(os.path.join(ROOT, "oracle", "libga3c_oracle.so")):
+        pytest.skip("oracle not built (run __graft_entry__.build())")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29541", "bench.py", "--impl", "reference",
+           "--gpus", "2", "--steps", "1", "--warmup", "0"]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
