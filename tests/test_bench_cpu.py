@@ -54,3 +54,14 @@ def test_reference_arm_under_torchrun_prints_one_line():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+def test_ncu_traffic_entries_per_net():
+    """roofline.traffic comes from profiles/ncu_traffic.json, keyed by net and
+    probed kernel class (DRAM read + write bytes of one ncu --set full launch)."""
+    d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+    for net in ("dnn_a", "large1"):
+        e = d[net]["conv_fwd[0]"]
+        assert e["bytes_per_launch"] == e["read"] + e["write"] > 0
+        assert e["algorithmic_bytes"] > 0 and e["capture"].startswith("profiles/")
+        assert os.path.exists(os.path.join(ROOT, e["capture"].split(" ")[0]))
