@@ -794,6 +794,7 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
             if grad_view is not None:
                 with torch.cuda.stream(stream):
                     dist.all_reduce(grad_view)
+                ctx.check_grad()  # reject on the summed gradient, identically on every rank
                 ctx.clip_grad()
             ctx.apply_rmsprop()
         prev_term = term_h[s].astype(np.uint8)

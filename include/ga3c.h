@@ -149,7 +149,10 @@ int ga3c_loss_grad_u8(ga3c_ctx* c, int slot, const uint8_t* frames, const int32_
 int ga3c_loss_grad_f32(ga3c_ctx* c, int slot, const float* states, const int32_t* actions,
                        const double* returns, int B, int apply_clip, float* dtheta,
                        double* scalars);
-/* Device-resident variant (async); all pointers are device memory. */
+/* Device-resident variant (async); all pointers are device memory.  Actions
+ * are not validated on the host: a sample whose action is outside
+ * [0, n_actions) makes the gradient non-finite, so the following apply
+ * rejects the step (the reference throws, nnet.cpp:227-228). */
 int ga3c_loss_grad_dev(ga3c_ctx* c, int slot, const void* d_states, int states_are_u8,
                        long long state_stride, const int32_t* d_actions, const double* d_returns,
                        int B, int apply_clip);
@@ -182,6 +185,11 @@ int ga3c_ctx_read_grad(ga3c_ctx* c, float* dtheta, double* scalars);
 /* Optional global-norm clip of the context gradient (nnet.cpp:281-289). */
 int ga3c_clip_grad(ga3c_ctx* c);
 
+/* Recompute the context gradient's non-finite flag (reset + scan of all P
+ * values) on the context stream: after an in-place data-parallel all-reduce
+ * the flag must describe the SUMMED gradient, so that every replica rejects
+ * or applies the same step (nnet.cpp:299-301). */
+int ga3c_check_grad(ga3c_ctx* c);
 /* ------------------------------------------------------------ rmsprop */
 /* SharedModel::apply pipeline.cpp:37-63 -> nnet::rmsprop_update
  * nnet.cpp:293-312: one non-centred RMSProp step on the LATEST parameters,
@@ -191,6 +199,12 @@ int ga3c_clip_grad(ga3c_ctx* c);
  * non-finite; nothing changes then.  applied_on (nullable) = the version the
  * step was applied on top of. */
 int ga3c_apply_rmsprop(ga3c_ctx* c, const float* dtheta, int* applied, uint64_t* applied_on);
+/* nnet::rmsprop_update nnet.cpp:293-312 on a raw parameter vector of any
+ * length n (no network layout): theta and g (host, n floats) are updated in
+ * place on `device`; a non-finite dtheta leaves them unchanged and returns
+ * GA3C_NOT_APPLIED with applied = 0.  Blocking. */
+int ga3c_rmsprop_flat(const ga3c_hyper* hp, int device, size_t n, float* theta, float* g, const float* dtheta,
+                      int* applied);
 /* Stream-ordered device loop variant: updates the latest slot IN PLACE from
  * the context gradient, gated by the on-device non-finite flag; no host
  * synchronisation.  Only valid while no other thread reads the model. */

@@ -135,6 +135,8 @@ _SIGS = {
     "ga3c_ctx_last_values": (_P, [_P]),
     "ga3c_ctx_read_grad": (C.c_int, [_P, _P, _P]),
     "ga3c_clip_grad": (C.c_int, [_P]),
+    "ga3c_check_grad": (C.c_int, [_P]),
+    "ga3c_rmsprop_flat": (C.c_int, [C.POINTER(HyperC), C.c_int, C.c_size_t, _P, _P, _P, C.POINTER(C.c_int)]),
     "ga3c_apply_rmsprop": (C.c_int, [_P, _P, C.POINTER(C.c_int), C.POINTER(C.c_uint64)]),
     "ga3c_apply_rmsprop_dev": (C.c_int, [_P]),
     "ga3c_ctx_read_dev_version": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
@@ -435,6 +437,10 @@ class Context:
 
     def clip_grad(self):
         check(lib.ga3c_clip_grad(self.h), self.model.error())
+
+    def check_grad(self):
+        """Recompute the non-finite flag of the (all-reduced) gradient."""
+        check(lib.ga3c_check_grad(self.h), self.model.error())
 
     def time_kernel(self, tag, layer=-1):
         check(lib.ga3c_ctx_time_kernel(self.h, K_TAGS[tag] if isinstance(tag, str) else tag, layer))

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -66,6 +67,32 @@ struct Slot {
   bool pending = false;
 };
 
+// Fixed-capacity slot storage: a Slot never moves once published, so a
+// thread holding a slot index may read its immutable fields (theta, g) while
+// another thread appends a slot.  Appends happen under update_m + read_m; the
+// count is published with release order after the slot is fully written.
+// Mutable fields (version, refs, pending, ready) are read under read_m.
+constexpr int kMaxSlots = 64;
+class SlotTable {
+ public:
+  int size() const { return n_.load(std::memory_order_acquire); }
+  Slot& operator[](int i) { return s_[i]; }
+  // false when the table is full (the caller reports GA3C_OUT_OF_MEMORY)
+  bool push_back(const Slot& x) {
+    const int k = n_.load(std::memory_order_relaxed);
+    if (k >= kMaxSlots) return false;
+    s_[k] = x;
+    n_.store(k + 1, std::memory_order_release);
+    return true;
+  }
+  Slot* begin() { return s_; }
+  Slot* end() { return s_ + size(); }
+
+ private:
+  Slot s_[kMaxSlots];
+  std::atomic<int> n_{0};
+};
+
 }  // namespace
 
 struct ga3c_model {
@@ -75,7 +102,7 @@ struct ga3c_model {
   int device = 0;
   std::mutex read_m;    // guards slots[].refs / version / cur  (pipeline.cpp:22-25)
   std::mutex update_m;  // serializes writers                   (pipeline.cpp:40)
-  std::vector<Slot> slots;
+  SlotTable slots;
   int cur = 0;
   // completion of the last asynchronous apply: the next writer orders after it
   cudaEvent_t apply_done = nullptr;
@@ -308,14 +335,21 @@ int ring_cap(const ga3c_ctx* c, int n, long long ctas) {
   return (ctas > kNumSMs || split_sms(c) < kNumSMs) ? 1 : 0;
 }
 
-// Raise a kernel's dynamic shared memory limit once per instantiation.  The
-// static's initialisation is thread-safe: predictor and trainer threads may
-// make their first launches concurrently.
-#define GA3C_SMEM_ONCE(kern, bytes)                                                                         \
-  static const bool smem_once_ = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                                       bytes),                                              \
-                                  true);                                                                    \
-  (void)smem_once_
+// Raise a kernel's dynamic shared memory limit once per instantiation and
+// device (the attribute is per device; a process may drive models on several
+// devices).  Concurrent first launches may both set it, which is harmless;
+// the bit is published only after the attribute is set.
+void smem_once(std::atomic<unsigned long long>& done, const void* kern, int bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done.fetch_or(bit, std::memory_order_acq_rel);
+}
+#define GA3C_SMEM_ONCE(kern, bytes)                         \
+  static std::atomic<unsigned long long> smem_done_{0};     \
+  smem_once(smem_done_, reinterpret_cast<const void*>(kern), static_cast<int>(bytes))
 
 #define GA3C_CAP_SWITCH(cap, F) \
   switch (cap) {                \
@@ -1210,15 +1244,22 @@ int set_device(ga3c_model* m) {
   return GA3C_OK;
 }
 
+// The apply-in-flight state of slot s, read under read_m.
+cudaEvent_t pending_event(ga3c_model* m, int s) {
+  std::lock_guard<std::mutex> lk(m->read_m);
+  const Slot& sl = m->slots[s];
+  return sl.pending ? sl.ready : nullptr;
+}
+
 // Orders c's stream after an asynchronous apply still writing slot s.
 void wait_slot(ga3c_ctx* c, int s) {
-  const Slot& sl = c->m->slots[s];
-  if (sl.pending && !c->capturing) cudaStreamWaitEvent(c->stream, sl.ready, 0);
+  if (c->capturing) return;
+  if (cudaEvent_t e = pending_event(c->m, s)) cudaStreamWaitEvent(c->stream, e, 0);
 }
 
 // Host side: waits until slot s is written.
 void sync_slot(ga3c_model* m, int s) {
-  if (m->slots[s].pending) cudaEventSynchronize(m->slots[s].ready);
+  if (cudaEvent_t e = pending_event(m, s)) cudaEventSynchronize(e);
 }
 
 // Allocates (or reuses) a slot with no readers that is not the current one.
@@ -1233,7 +1274,11 @@ int free_slot_locked(ga3c_model* m) {
     cudaFree(s.theta);
     return -1;
   }
-  m->slots.push_back(s);
+  if (!m->slots.push_back(s)) {
+    cudaFree(s.theta);
+    cudaFree(s.g);
+    return -1;
+  }
   return (int)m->slots.size() - 1;
 }
 
@@ -1736,6 +1781,62 @@ int ga3c_clip_grad(ga3c_ctx* c) {
   return GA3C_OK;
 }
 
+int ga3c_check_grad(ga3c_ctx* c) {
+  if (!c) return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  GA3C_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int), c->cur));
+  {
+    Launch l(c, GA3C_K_OTHER, -1);
+    pdl_launch(c->cur, check_finite_kernel, dim3(kNumSMs), dim3(256), 0, (const float*)c->grad, m->lo.total, c->flag);
+  }
+  c->grad_flag = -1;
+  GA3C_CUDA(cudaGetLastError());
+  return GA3C_OK;
+}
+
+int ga3c_rmsprop_flat(const ga3c_hyper* hp, int device, size_t n, float* theta, float* g, const float* dtheta,
+                      int* applied) {
+  if (!hp || !theta || !g || !dtheta || validate_hyper(*hp) != GA3C_OK) return GA3C_INVALID_ARGUMENT;
+  if (applied) *applied = 0;
+  if (n == 0) {
+    if (applied) *applied = 1;
+    return GA3C_OK;
+  }
+  auto set_err = [&](const std::string& e) { g_tls_error = e; };
+  GA3C_CUDA(cudaSetDevice(device));
+  float* d = nullptr;
+  int* flag = nullptr;
+  const std::size_t bytes = n * sizeof(float);
+  GA3C_CUDA(cudaMalloc(&d, 3 * bytes + 16 + sizeof(int)));
+  float* th = d;
+  float* gg = d + n;
+  float* dt = d + 2 * n;
+  flag = reinterpret_cast<int*>(d + 3 * n + 4);
+  int h_flag = 1;
+  cudaError_t e = cudaMemcpy(th, theta, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(gg, g, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dt, dtheta, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(flag, 0, sizeof(int));
+  if (e == cudaSuccess) {
+    check_finite_kernel<<<kNumSMs, 256>>>(dt, n, flag);
+    const std::size_t n4 = (n + 3) / 4;
+    const unsigned blocks = (unsigned)std::max<std::size_t>(1, std::min<std::size_t>((n4 + 255) / 256, 8 * kNumSMs));
+    rmsprop_kernel<<<blocks, 256>>>(th, gg, dt, th, gg, n, flag, nullptr, static_cast<float>(hp->alpha),
+                                    static_cast<float>(1.0 - hp->alpha), static_cast<float>(hp->eta),
+                                    static_cast<float>(hp->eps_rms));
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(&h_flag, flag, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && !h_flag) e = cudaMemcpy(theta, th, bytes, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && !h_flag) e = cudaMemcpy(g, gg, bytes, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  GA3C_CUDA(e);
+  if (h_flag) return GA3C_NOT_APPLIED;
+  if (applied) *applied = 1;
+  return GA3C_OK;
+}
+
 int ga3c_apply_rmsprop(ga3c_ctx* c, const float* dtheta, int* applied, uint64_t* applied_on) {
   if (!c) return GA3C_INVALID_ARGUMENT;
   ga3c_model* m = c->m;
@@ -1861,7 +1962,12 @@ int ga3c_model_ring(ga3c_model* m, int n, int* slots_out) {
     GA3C_CUDA(cudaMemcpy(s.g, latest.g, bytes, cudaMemcpyDeviceToDevice));
     s.version = latest.version;
     s.refs = 1;  // owned by the caller's device loop: never recycled
-    m->slots.push_back(s);
+    if (!m->slots.push_back(s)) {
+      cudaFree(s.theta);
+      cudaFree(s.g);
+      set_err("ga3c_model_ring: slot table full");
+      return GA3C_OUT_OF_MEMORY;
+    }
     slots_out[i] = static_cast<int>(m->slots.size()) - 1;
   }
   return GA3C_OK;

@@ -266,7 +266,12 @@ heads_loss_kernel(const float* __restrict__ part, int n_split, const float* __re
   softmax64(logit_sh, A, e_sh, p_sh);
   HTRACE(5);
   if (tid < 32) {
-    const double adv = ret_b - static_cast<double>(val_sh);
+    // an action outside [0, A) (the reference throws, nnet.cpp:214-216) makes
+    // the sample's advantage NaN, so every gradient it touches is non-finite
+    // and the step is rejected by the flag the gradient writers raise
+    const bool bad_a = static_cast<unsigned>(a) >= static_cast<unsigned>(A);
+    const double adv = bad_a ? __longlong_as_double(0x7ff8000000000000ULL) : ret_b - static_cast<double>(val_sh);
+    const int ac = bad_a ? 0 : a;
     for (int k = lane; k < A; k += 32) {
       const double p = p_sh[k];
       pi64[static_cast<std::size_t>(b) * A + k] = p;
@@ -281,7 +286,7 @@ heads_loss_kernel(const float* __restrict__ part, int n_split, const float* __re
       double H = 0.0, dot = 0.0;
       for (int k = 0; k < A; ++k) H -= p_sh[k] * lg_sh[k];
       for (int k = 0; k < A; ++k) dot += dp_sh[k] * p_sh[k];
-      scal[3 * b + 0] = -lg_sh[a] * adv - beta * H;
+      scal[3 * b + 0] = -lg_sh[ac] * adv - beta * H;
       scal[3 * b + 1] = adv * adv;
       scal[3 * b + 2] = H;
       e_sh[0] = dot;

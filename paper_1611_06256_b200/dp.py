@@ -61,6 +61,10 @@ def dp_update(ctx, d_states, u8, d_actions, d_returns, B_local, slot, gview, str
     ctx.loss_grad_dev(d_states, u8, d_actions, d_returns, B_local, slot, apply_clip=world == 1)
     if world > 1:
         allreduce_sum_(gview, stream)
+        # the reject decision must see the SUMMED gradient on every rank
+        # (nnet.cpp:299-301): a rank whose own shard was finite would
+        # otherwise apply a non-finite sum the others reject
+        ctx.check_grad()
         ctx.clip_grad()
     ctx.apply_rmsprop_dev()
 
