@@ -128,6 +128,14 @@ int ga3c_forward_u8(ga3c_ctx* c, int slot, const uint8_t* frames, int B, float* 
                     uint64_t* version_used);
 int ga3c_forward_f32(ga3c_ctx* c, int slot, const float* states, int B, float* pi, float* v,
                      uint64_t* version_used);
+/* The same with the policy as the device's fp64 softmax (the reference's
+ * ForwardResult.policies type, nnet.hpp:55-58): pi rows sum to 1 within fp64
+ * rounding, and qac::sample_index (util.hpp:46-54) on them draws exactly the
+ * action ga3c_sample_actions_dev draws on the device.  v = V widened to fp64. */
+int ga3c_forward64_u8(ga3c_ctx* c, int slot, const uint8_t* frames, int B, double* pi, double* v,
+                      uint64_t* version_used);
+int ga3c_forward64_f32(ga3c_ctx* c, int slot, const float* states, int B, double* pi, double* v,
+                       uint64_t* version_used);
 /* Device-resident variant: all pointers are device memory; asynchronous on
  * the context stream; `slot` must be pinned by the caller.  state_stride =
  * elements between consecutive states (0 = dense), so a batch can be read

@@ -5,8 +5,11 @@
 // (include/qac/returns.hpp:13-32), implemented over the C ABI
 // (include/ga3c.h).  A caller written against the reference --
 // predictor_loop, trainer_main, SharedModel::apply, train_sync, the pybind
-// module -- switches by including this header and compiling with
-// QAC_B200_AS_QAC (which aliases namespace qac to qac_b200).
+// module -- switches with an include path: include/qac/nnet.hpp and
+// include/qac/returns.hpp shadow the reference headers of the same names and
+// alias qac::nnet / qac::returns to the namespaces below, so the reference's
+// own sources compile unmodified against this library (INTEGRATION.md §2,
+// oracle/Makefile target `dropin`).
 //
 // Semantics kept:
 //   * pure value semantics: every call takes theta by const& and returns new
@@ -130,7 +133,3 @@ void set_device(int device);
 
 }  // namespace nnet
 }  // namespace qac_b200
-
-#ifdef QAC_B200_AS_QAC
-namespace qac = qac_b200;
-#endif

@@ -123,6 +123,8 @@ _SIGS = {
     "ga3c_ctx_launches": (C.c_uint64, [_P]),
     "ga3c_forward_u8": (C.c_int, [_P, C.c_int, _P, C.c_int, _P, _P, C.POINTER(C.c_uint64)]),
     "ga3c_forward_f32": (C.c_int, [_P, C.c_int, _P, C.c_int, _P, _P, C.POINTER(C.c_uint64)]),
+    "ga3c_forward64_u8": (C.c_int, [_P, C.c_int, _P, C.c_int, _P, _P, C.POINTER(C.c_uint64)]),
+    "ga3c_forward64_f32": (C.c_int, [_P, C.c_int, _P, C.c_int, _P, _P, C.POINTER(C.c_uint64)]),
     "ga3c_forward_dev": (C.c_int, [_P, C.c_int, _P, C.c_int, C.c_longlong, C.c_int, _P, _P]),
     "ga3c_loss_grad_u8": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, C.c_int, _P, _P]),
     "ga3c_loss_grad_f32": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, C.c_int, _P, _P]),

@@ -1624,9 +1624,12 @@ int ga3c_forward_dev(ga3c_ctx* c, int slot, const void* d_states, int states_are
   return GA3C_OK;
 }
 
+// pi/v receive fp32 copies, pi64/v64 the fp64 softmax and widened V (either
+// pair may be null, not both).
 static int forward_host(ga3c_ctx* c, int slot, const void* states, bool u8, int B, float* pi,
-                        float* v, uint64_t* version_used) {
-  if (!c || B < 0 || B > c->max_batch || (B > 0 && (!states || !pi || !v))) return GA3C_INVALID_ARGUMENT;
+                        float* v, uint64_t* version_used, double* pi64 = nullptr, double* v64 = nullptr) {
+  if (!c || B < 0 || B > c->max_batch || (B > 0 && (!states || (!(pi && v) && !(pi64 && v64)))))
+    return GA3C_INVALID_ARGUMENT;
   ga3c_model* m = c->m;
   auto set_err = [&](const std::string& e) { m->set_error(e); };
   const std::size_t dim = m->lo.in_dim;
@@ -1652,9 +1655,14 @@ static int forward_host(ga3c_ctx* c, int slot, const void* states, bool u8, int 
       run_forward(c, m->slots[s].theta, c->d_in, u8, B);
     }
     const int A = m->lo.n_actions;
-    if (!rc && cudaMemcpyAsync(pi, c->pi32, sizeof(float) * B * A, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+    if (!rc && pi && cudaMemcpyAsync(pi, c->pi32, sizeof(float) * B * A, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
       rc = GA3C_CUDA_ERROR;
-    if (!rc && cudaMemcpyAsync(v, c->v, sizeof(float) * B, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+    if (!rc && v && cudaMemcpyAsync(v, c->v, sizeof(float) * B, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+      rc = GA3C_CUDA_ERROR;
+    if (!rc && pi64 &&
+        cudaMemcpyAsync(pi64, c->pi64, sizeof(double) * B * A, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+      rc = GA3C_CUDA_ERROR;
+    if (!rc && v64 && cudaMemcpyAsync(v64, c->v64, sizeof(double) * B, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
       rc = GA3C_CUDA_ERROR;
     cudaError_t e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) {
@@ -1675,6 +1683,16 @@ int ga3c_forward_u8(ga3c_ctx* c, int slot, const uint8_t* frames, int B, float* 
 int ga3c_forward_f32(ga3c_ctx* c, int slot, const float* states, int B, float* pi, float* v,
                      uint64_t* version_used) {
   return forward_host(c, slot, states, false, B, pi, v, version_used);
+}
+
+int ga3c_forward64_u8(ga3c_ctx* c, int slot, const uint8_t* frames, int B, double* pi, double* v,
+                      uint64_t* version_used) {
+  return forward_host(c, slot, frames, true, B, nullptr, nullptr, version_used, pi, v);
+}
+
+int ga3c_forward64_f32(ga3c_ctx* c, int slot, const float* states, int B, double* pi, double* v,
+                       uint64_t* version_used) {
+  return forward_host(c, slot, states, false, B, nullptr, nullptr, version_used, pi, v);
 }
 
 int ga3c_loss_grad_dev(ga3c_ctx* c, int slot, const void* d_states, int states_are_u8,

@@ -34,17 +34,17 @@ std::uint64_t derive_seed(std::uint64_t base, std::initializer_list<std::uint64_
 
 double next_uniform(std::mt19937_64& rng) { return static_cast<double>(rng() >> 11) * 0x1.0p-53; }
 
-int sample_index(const float* probs, int n, std::mt19937_64& rng) {
+int sample_index(const double* probs, int n, std::mt19937_64& rng) {
   const double u = next_uniform(rng);
   double acc = 0.0;
   for (int i = 0; i < n; ++i) {
-    acc += static_cast<double>(probs[i]);
+    acc += probs[i];
     if (u < acc) return i;
   }
   return n - 1;
 }
 
-int argmax_index(const float* v, int n) {
+int argmax_index(const double* v, int n) {
   int best = 0;
   for (int i = 1; i < n; ++i)
     if (v[i] > v[best]) best = i;

@@ -38,8 +38,8 @@ inline constexpr std::uint64_t kSeedAgentRng = 0x6167656e74ULL;   // util.hpp:35
 inline constexpr std::uint64_t kSeedEnvEpisode = 0x656e76ULL;     // util.hpp:36
 inline constexpr std::uint64_t kSeedAnneal = 0x616e6e65616cULL;   // pipeline.cpp:13
 double next_uniform(std::mt19937_64& rng);                         // util.hpp:41-43
-int sample_index(const float* probs, int n, std::mt19937_64& rng);  // util.hpp:46-54 (fp64 CDF)
-int argmax_index(const float* values, int n);                      // util.hpp:57-63
+int sample_index(const double* probs, int n, std::mt19937_64& rng);  // util.hpp:46-54 (fp64 CDF)
+int argmax_index(const double* values, int n);                     // util.hpp:57-63
 void busy_wait_us(std::int64_t us);
 
 // ------------------------------------------------------------- envs.hpp
@@ -126,7 +126,7 @@ struct PredictionRequest {
 };
 
 struct PredictionResponse {
-  std::vector<float> policy;
+  std::vector<double> policy;  // the device's fp64 softmax (ga3c_forward64_*)
   double value = 0.0;
   std::uint64_t model_version = 0;
 };

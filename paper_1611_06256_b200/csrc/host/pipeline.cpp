@@ -159,7 +159,7 @@ void predictor_loop(BoundedChannel<PredictionRequest>& requests,
                     const std::atomic<bool>& stop) {
   std::vector<PredictionRequest> got;
   HostBatch hb;
-  std::vector<float> pi, v;
+  std::vector<double> pi, v;
   while (!stop.load(std::memory_order_relaxed)) {
     auto first = requests.pop(&stop);  // block for the first (pipeline.cpp:72)
     if (!first) break;
@@ -179,8 +179,8 @@ void predictor_loop(BoundedChannel<PredictionRequest>& requests,
     pi.resize(static_cast<std::size_t>(B) * A);
     v.resize(B);
     std::uint64_t ver = 0;
-    const int st = hb.u8 ? ga3c_forward_u8(ctx, snap->slot, hb.b8.data(), B, pi.data(), v.data(), &ver)
-                         : ga3c_forward_f32(ctx, snap->slot, hb.bf.data(), B, pi.data(), v.data(), &ver);
+    const int st = hb.u8 ? ga3c_forward64_u8(ctx, snap->slot, hb.b8.data(), B, pi.data(), v.data(), &ver)
+                         : ga3c_forward64_f32(ctx, snap->slot, hb.bf.data(), B, pi.data(), v.data(), &ver);
     check(st, model.handle(), "forward");
     for (int i = 0; i < B; ++i) {
       PredictionResponse resp;
@@ -723,8 +723,8 @@ RunReport train_sync(const PipelineOptions& opt) {
   std::vector<double> rew, boot;
   std::vector<std::uint8_t> term;
   const int A = o.net.n_actions;
-  std::vector<float> pi(A);
-  float v = 0.f;
+  std::vector<double> pi(A);
+  double v = 0.0;
   int turn = 0;
   while (rep.total_updates < *o.stop.max_updates) {
     Slot& a = agents[turn];
@@ -736,8 +736,8 @@ RunReport train_sync(const PipelineOptions& opt) {
       const auto snap = model.snapshot();
       std::uint64_t ver = 0;
       const bool u8 = !a.obs.u8.empty();
-      const int st = u8 ? ga3c_forward_u8(ctx.c, snap->slot, a.obs.u8.data(), 1, pi.data(), &v, &ver)
-                        : ga3c_forward_f32(ctx.c, snap->slot, a.obs.f32.data(), 1, pi.data(), &v, &ver);
+      const int st = u8 ? ga3c_forward64_u8(ctx.c, snap->slot, a.obs.u8.data(), 1, pi.data(), &v, &ver)
+                        : ga3c_forward64_f32(ctx.c, snap->slot, a.obs.f32.data(), 1, pi.data(), &v, &ver);
       check(st, model.handle(), "forward");
       rep.total_predictions += 1;
       const int action = o.greedy ? argmax_index(pi.data(), A) : sample_index(pi.data(), A, a.rng);

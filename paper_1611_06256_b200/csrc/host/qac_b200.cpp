@@ -242,8 +242,10 @@ ForwardResult forward(const ModelState& model, const NetworkSpec& spec,
   load(e, model.theta, nullptr, model.version);
   const std::vector<float> x = pack_states(states, spec.input_dim);
   const int A = spec.n_actions;
-  std::vector<float> pi(static_cast<std::size_t>(B) * A), v(B);
-  check(ga3c_forward_f32(e.c, -1, x.data(), B, pi.data(), v.data(), nullptr), "forward");
+  // the device's fp64 softmax: rows sum to 1 in fp64 and sample_index on
+  // them matches the on-device sampler (util.hpp:46-54)
+  std::vector<double> pi(static_cast<std::size_t>(B) * A), v(B);
+  check(ga3c_forward64_f32(e.c, -1, x.data(), B, pi.data(), v.data(), nullptr), "forward");
   out.policies.resize(B);
   out.values.resize(B);
   for (int b = 0; b < B; ++b) {
@@ -303,35 +305,23 @@ UpdateResult rmsprop_update(const ModelState& model, const RmsState& rms, const 
     throw std::invalid_argument("rmsprop_update: size mismatch");
   for (double g : grads.dtheta)
     if (!std::isfinite(g)) return UpdateResult{model, rms, false};
-  // RMSProp is elementwise over the flat vector, so it runs on a conv-free
-  // stand-in model with the same hyperparameters and >= P parameters
-  // (3 * (in + 1) for a 2-action, no-hidden MLP); the zero padding is inert.
+  // RMSProp is elementwise over the flat vector: no network layout needed
   const std::size_t P = model.theta.size();
   if (P == 0) return UpdateResult{model, rms, true};
-  ga3c_net_spec flat{};
-  flat.in_h = 1;
-  flat.in_w = 1;
-  flat.n_actions = 2;
-  flat.in_c = static_cast<int>(std::max<std::size_t>(1, (P + 2) / 3 - 1));
-  while (ga3c_param_count(&flat) < P) ++flat.in_c;
-  const std::size_t Pf = ga3c_param_count(&flat);
-  Entry& e = entry(flat, to_c(hp), 1);
-  std::vector<float> t32(Pf, 0.0f), g32(Pf, 0.0f), d32(Pf, 0.0f);
+  const ga3c_hyper h = to_c(hp);
+  std::vector<float> t32(P), g32(P), d32(P);
   for (std::size_t i = 0; i < P; ++i) {
     t32[i] = static_cast<float>(model.theta[i]);
     g32[i] = static_cast<float>(rms.g[i]);
     d32[i] = static_cast<float>(grads.dtheta[i]);
   }
-  check(ga3c_model_load(e.m, t32.data(), g32.data(), model.version), "rmsprop_update: load");
   int applied = 0;
-  const int st = ga3c_apply_rmsprop(e.c, d32.data(), &applied, nullptr);
+  const int st = ga3c_rmsprop_flat(&h, t_device, P, t32.data(), g32.data(), d32.data(), &applied);
   if (st == GA3C_NOT_APPLIED || !applied) return UpdateResult{model, rms, false};
   check(st, "rmsprop_update");
-  std::uint64_t ver = 0;
-  check(ga3c_model_read(e.m, t32.data(), g32.data(), &ver), "rmsprop_update: read");
   UpdateResult r;
-  r.model.theta.assign(t32.begin(), t32.begin() + static_cast<std::ptrdiff_t>(P));
-  r.rms.g.assign(g32.begin(), g32.begin() + static_cast<std::ptrdiff_t>(P));
+  r.model.theta.assign(t32.begin(), t32.end());
+  r.rms.g.assign(g32.begin(), g32.end());
   r.model.version = model.version + 1;
   r.applied = true;
   return r;

@@ -238,23 +238,19 @@ def rmsprop_update(model: ModelState, rms: RmsState, grads: GradientPacket,
     P = len(model.theta)
     if len(grads.dtheta) != P or len(rms.g) != P:
         raise InvalidArgument(_abi.INVALID_ARGUMENT, "rmsprop_update: size mismatch")
-    # the update is shape-agnostic: any spec with P parameters can host it
-    m, ctx = _engine(spec if spec is not None else _flat_spec_for(P), hyper, 1)
-    m.load(model.theta, rms.g, model.version)
-    applied, _ = ctx.apply_rmsprop(np.ascontiguousarray(grads.dtheta, np.float32))
-    if not applied:
+    # the update is elementwise over the flat vector: no network layout needed
+    th = np.array(model.theta, np.float32)
+    g = np.array(rms.g, np.float32)
+    d = np.ascontiguousarray(grads.dtheta, np.float32)
+    ap = C.c_int(0)
+    h = hyper.to_c()
+    rc = _abi.lib.ga3c_rmsprop_flat(C.byref(h), 0, P, th.ctypes.data, g.ctypes.data, d.ctypes.data,
+                                    C.byref(ap))
+    if rc == _abi.NOT_APPLIED or not ap.value:
         return UpdateResult(ModelState(np.array(model.theta, np.float32), model.version),
-                        RmsState(np.array(rms.g, np.float32)), False)
-    th, g, ver = m.read()
-    return UpdateResult(ModelState(th, ver), RmsState(g), True)
-
-
-def _flat_spec_for(P: int) -> NetworkSpec:
-    """A head-only spec {d, [], A} has P = (d + 1) * (A + 1) parameters."""
-    for A in range(2, 64):
-        if P % (A + 1) == 0 and P // (A + 1) >= 2:
-            return NetworkSpec(P // (A + 1) - 1, [], A)
-    raise InvalidArgument(_abi.INVALID_ARGUMENT, f"no host layout for {P} parameters; pass spec=")
+                            RmsState(np.array(rms.g, np.float32)), False)
+    _abi.check(rc, "rmsprop_update")
+    return UpdateResult(ModelState(th, model.version + 1), RmsState(g), True)
 
 
 def compute_returns(rewards, terminal: bool, bootstrap: float, gamma: float) -> List[float]:

@@ -203,14 +203,14 @@ static void envs_dynamics() {  // test_envs.cpp
 
 static void sampling_matches_util() {  // util.hpp:46-54
   std::mt19937_64 a(1234), b(1234);
-  const float p[4] = {0.1f, 0.2f, 0.3f, 0.4f};
+  const double p[4] = {0.1, 0.2, 0.3, 0.4};
   int counts[4] = {0, 0, 0, 0};
   for (int i = 0; i < 40000; ++i) {
     const double u = next_uniform(b);
     double acc = 0.0;
     int want = 3;
     for (int k = 0; k < 4; ++k) {
-      acc += static_cast<double>(p[k]);
+      acc += p[k];
       if (u < acc) {
         want = k;
         break;

@@ -1,12 +1,12 @@
 // test_qac_adapter.cpp -- the reference's own nnet / returns unit tests
 // (proj/tests/test_nnet.cpp, test_returns.cpp) restated against the B200
-// drop-in adapter (csrc/host/qac_b200.hpp), compiled the way a reference
-// caller would be: QAC_B200_AS_QAC makes `qac::nnet::forward` etc. resolve to
-// the device implementation.  Exact fp64 expectations of the reference become
+// drop-in adapter (include/qac_b200.hpp), compiled the way a reference
+// caller is: `#include "qac/nnet.hpp"` resolves to the shim in include/qac/,
+// so `qac::nnet::forward` etc. are the device implementation.  Exact fp64 expectations of the reference become
 // fp32 tolerances; returns stay bitwise.  Needs a GPU; built
 // and run by tests/test_qac_adapter_gpu.py.
-#define QAC_B200_AS_QAC 1
-#include "qac_b200.hpp"
+#include "qac/nnet.hpp"
+#include "qac/returns.hpp"
 
 #include <cmath>
 #include <cstdio>

@@ -1,6 +1,6 @@
 """The reference's nnet/returns unit tests (test_nnet.cpp, test_returns.cpp)
-restated in C++ against the drop-in adapter csrc/host/qac_b200.hpp, which a
-reference caller includes instead of qac/nnet.hpp.  Compiling and linking is
+restated in C++ against the drop-in headers include/qac/{nnet,returns}.hpp,
+which shadow the reference headers of the same names.  Compiling and linking is
 checked on CPU; running needs the GPU."""
 import os
 import subprocess
@@ -13,7 +13,7 @@ PKG = os.path.join(ROOT, "paper_1611_06256_b200")
 
 def _build(out):
     subprocess.run(["g++", "-std=c++20", "-O1", "-pthread", "-Wall", "-Wextra", "-ffp-contract=off",
-                    "-I", os.path.join(PKG, "csrc", "host"), "-I", os.path.join(ROOT, "include"),
+                    "-I", os.path.join(ROOT, "include"),
                     os.path.join(ROOT, "tests", "cpp", "test_qac_adapter.cpp"),
                     "-L", PKG, "-lga3c_b200", "-Wl,-rpath," + PKG, "-o", str(out)], check=True)
 
