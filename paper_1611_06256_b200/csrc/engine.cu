@@ -1826,11 +1826,13 @@ int ga3c_rmsprop_flat(const ga3c_hyper* hp, int device, size_t n, float* theta, 
   float* d = nullptr;
   int* flag = nullptr;
   const std::size_t bytes = n * sizeof(float);
-  GA3C_CUDA(cudaMalloc(&d, 3 * bytes + 16 + sizeof(int)));
+  // the kernel moves float4s: every sub-buffer starts 256-byte aligned
+  const std::size_t np = (n + 63) / 64 * 64;
+  GA3C_CUDA(cudaMalloc(&d, (3 * np + 64) * sizeof(float)));
   float* th = d;
-  float* gg = d + n;
-  float* dt = d + 2 * n;
-  flag = reinterpret_cast<int*>(d + 3 * n + 4);
+  float* gg = d + np;
+  float* dt = d + 2 * np;
+  flag = reinterpret_cast<int*>(d + 3 * np);
   int h_flag = 1;
   cudaError_t e = cudaMemcpy(th, theta, bytes, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(gg, g, bytes, cudaMemcpyHostToDevice);
