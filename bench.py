@@ -350,7 +350,6 @@ def main():
     th = np.zeros(P, np.float32)
     _abi.check(_abi.lib.ga3c_init_params(spec, 1 + rank * 0, None, th.ctypes.data))  # identical replicas
     model.load(th)
-    slot, _ = model.acquire()
 
     # ---- synthetic inputs resident in HBM (agent-major frame rings) ----
     set_bytes = n * FRAME_BYTES
@@ -363,151 +362,33 @@ def main():
     rewards = (torch.rand((sets, NA, T), dtype=torch.float64, device="cuda", generator=g) - 0.5) * 2
     terminal = (torch.rand((sets, NA), device="cuda", generator=g) < T / 64.0).to(torch.uint8)
     offsets = torch.arange(0, n + 1, T, dtype=torch.int32, device="cuda")
-    # double-buffered experience (actions, n-step returns): with several
-    # trainers in flight the predictor phase of step i overlaps the trainer
-    # phase, which consumes step i-1's experiences (GA3C's concurrent
-    # predictor and trainer threads decoupled by the training queue)
-    actions2 = torch.zeros((2, NA, T), dtype=torch.int32, device="cuda")
-    rets2 = torch.zeros((2, NA, T), dtype=torch.float64, device="cuda")
-    actions, rets = actions2[0], rets2[0]
     torch.cuda.synchronize()
     stream = torch.cuda.ExternalStream(ctx.stream)
 
     from paper_1611_06256_b200 import dp
-    grad_view = dp.grad_view(ctx, P, f"cuda:{local}") if world > 1 else None
-
-    fstride = T * FRAME_BYTES
-
-    # N_T trainers in flight (GA3C's trainer threads, pipeline.cpp:241-306):
-    # update u's gradient runs on trainer context u % N_T (its own stream and
-    # workspace) against parameter version u - (N_T - 1), the policy lag GA3C
-    # accepts; the RMSProp steps stay serialized in update order on the main
-    # stream and write out of place into a ring of N_T + 1 device slots, so a
-    # trainer never reads a version that is being overwritten.
+    from paper_1611_06256_b200.loop import GMAX, DeviceLoop, mean_policy_lag
     NT = args.trainers
-    GMAX = 8  # steps one CUDA graph may chain
-    assert hyper.grad_clip_norm == 0.0 or NT == 1, "clipping with several trainers in flight is not wired here"
-    # ring of R >= N_T + 1 slots; R divides the updates per step so every
-    # step starts from slot 0 (one captured graph per input set)
-    ring_sizes = [r for r in range(NT + 1, updates + 1) if updates % r == 0]
-    assert NT == 1 or ring_sizes, "N_T must be below the updates per step"
-    overlap = NT > 1 and not args.no_overlap
-    if NT > 1:
-        R = ring_sizes[0]
-        ring = model.ring(R + 1)  # + the predictor's slot, never written by a trainer
-        pred_slot = ring[R]
-        tctx = [_abi.Context(model, TB) for _ in range(NT)]
-        tstream = [torch.cuda.ExternalStream(c.stream) for c in tctx]
-        tgrad = [dp.grad_view(c, P, f"cuda:{local}") for c in tctx] if world > 1 else None
-        # events per update of a multi-step graph (update index continuous
-        # across the steps one graph captures, see `step`)
-        ev_g = [torch.cuda.Event() for _ in range(updates * GMAX)]
-        ev_a = [torch.cuda.Event() for _ in range(updates * GMAX)]
-        ev_r = torch.cuda.Event()
-        ev_p = [torch.cuda.Event() for _ in range(GMAX)]
-        ev_end = [torch.cuda.Event() for _ in range(GMAX)]
-        for c in tctx:
-            c.set_sm_budget(args.trainer_sms)
+    loop = DeviceLoop(model, ctx, NA, T, TB, NT, frames, uni, rewards, terminal, trainer_sms=args.trainer_sms,
+                      pred_sms=args.pred_sms, overlap=not args.no_overlap, world=world, device=f"cuda:{local}",
+                      hyper=hyper)
+    grad_view = loop.grad_view
     fused = None
-    if world > 1 and NT > 1 and args.dp == "fused":
-        try:
-            fused = dp.FusedUpdate(model, tctx, ring[:R], rank, world)
-            if not fused.self_check(ctx, 0, P, f"cuda:{local}", ring[0], ring[1], ring[2]):
-                raise RuntimeError("self-check against NCCL all-reduce + RMSProp failed")
-        except Exception as e:  # IPC unavailable or a mismatch: fall back to NCCL, and say so
-            print(f"[bench] fused DP update unavailable ({e}); using NCCL all-reduce", file=sys.stderr)
-            fused = None
-            args.dp = "nccl"
-    pctx = _abi.Context(model, NA) if overlap else ctx
-    if overlap:
-        pctx.set_sm_budget(args.pred_sms)
-    pstream = torch.cuda.ExternalStream(pctx.stream) if overlap else stream
-    lv = pctx.last_values_ptr()
-
-    def predict(i, b):
-        """t_max predictor batches of N_A agents, sampling, n-step returns -> buffer b."""
-        s = i % sets
-        fr = frames[s].data_ptr()
-        pslot = pred_slot if NT > 1 else slot
-        acts, rts = actions2[b], rets2[b]
-        for t in range(T):
-            pctx.forward_dev(fr + t * FRAME_BYTES, NA, True, slot=pslot, stride=fstride)
-            pctx.sample_dev(uni[s, t].data_ptr(), NA, acts.data_ptr() + 4 * t, stride=T)
-        pctx.compute_returns_dev(rewards[s].data_ptr(), offsets.data_ptr(), NA, terminal[s].data_ptr(), lv,
-                                 hyper.gamma, rts.data_ptr())
-
-    def step(i, pos=0):
-        if NT == 1:
-            predict(i, 0)
-            fr = frames[i % sets].data_ptr()
-            for u in range(updates):  # data parallel: summed local gradient -> all-reduce -> RMSProp
-                dp.dp_update(ctx, fr + u * TB * FRAME_BYTES, True, actions.data_ptr() + 4 * u * TB,
-                             rets.data_ptr() + 8 * u * TB, TB, slot, grad_view, stream, world)
-            return
-        # pos: position of this step inside a multi-step graph (0 = first,
-        # or eager).  Update U = pos * updates + u is continuous across the
-        # chained steps, so trainer U waits only for apply U - N_T and the
-        # first updates of step pos + 1 overlap the last ones of step pos.
-        base = pos * updates
-        if overlap:
-            # predictor branch (own context and stream) || trainers on the
-            # previous step's experiences.  The predictor of a chained step
-            # waits for the previous step's end (its slot was refreshed and
-            # the experience buffer it overwrites was consumed).
-            if pos == 0:
-                ev_r.record(stream)
-                ev_r.wait(pstream)
-            else:
-                ev_end[pos - 1].wait(pstream)
-            predict(i, i % 2)
-            ev_p[pos].record(pstream)
-            ti, b = i - 1, (i - 1) % 2
-            ready = ev_r if pos == 0 else ev_p[pos - 1]  # this step's experiences exist
+    if world > 1 and NT > 1:
+        if args.dp == "fused":
+            try:
+                fused = dp.FusedUpdate(model, loop.tctx, loop.ring[:loop.R], rank, world)
+                fused.self_check(ctx, 0, P, f"cuda:{local}", loop.ring[0], loop.ring[1], loop.ring[2])
+            except Exception as e:  # loud: the line records the fallback and why
+                print(f"[bench] FUSED DP UPDATE UNAVAILABLE, falling back to NCCL: {e}", file=sys.stderr)
+                fused = None
+                args.dp = "nccl"
+                args.dp_fallback = str(e)
+        if fused is not None:
+            loop.dp_update = lambda lp, j, U: fused.apply(ctx, j, lp.ring[U % lp.R], lp.ring[(U + 1) % lp.R])
         else:
-            predict(i, 0)
-            ev_r.record(stream)
-            ti, b = i, 0
-            ready = ev_r
-        fr = frames[ti % sets].data_ptr()
-        acts, rts = actions2[b], rets2[b]
-        for u in range(updates):
-            U = base + u
-            j = U % NT
-            if u < NT:
-                ready.wait(tstream[j])
-            if U >= NT:
-                ev_a[U - NT].wait(tstream[j])  # version U - N_T + 1 exists; context j's last gradient was applied
-            tctx[j].loss_grad_dev(fr + u * TB * FRAME_BYTES, True, acts.data_ptr() + 4 * u * TB,
-                                  rts.data_ptr() + 8 * u * TB, TB, ring[(U - NT + 1) % R], apply_clip=world == 1)
-            ev_g[U].record(tstream[j])
-            ev_g[U].wait(stream)
-            if fused is not None:  # reduce-scatter + RMSProp + all-gather in one kernel
-                fused.apply(ctx, j, ring[U % R], ring[(U + 1) % R])
-            else:
-                if world > 1:  # default hyper: no clip, so nothing to do after the sum
-                    dp.allreduce_sum_(tgrad[j], stream)
-                ctx.apply_slots_dev(tctx[j], ring[U % R], ring[(U + 1) % R])
-            ev_a[U].record(stream)
-        if overlap:
-            ev_p[pos].wait(stream)  # the predictor is done reading its slot
-        ctx.copy_slot_dev(ring[updates % R], pred_slot)
-        ev_end[pos].record(stream)
-
-    contexts = [ctx] + (tctx if NT > 1 else []) + ([pctx] if overlap else [])
-
-    def time_kernel(tag, li=-1):
-        for c in contexts:
-            c.time_kernel(tag, li)
-
-    def kernel_time():
-        ms = cnt = 0
-        for c in contexts:
-            a, b = c.kernel_time()
-            ms, cnt = ms + a, cnt + b
-        return ms, cnt
-
-    def launches_all():
-        return sum(c.launches() for c in contexts)
+            loop.dp_update = dp.nccl_update
+    step = loop.step
+    time_kernel, kernel_time, launches_all = loop.time_kernel, loop.kernel_time, loop.launches
 
     def busy():
         # Park the stream behind a ~4 ms spin so the host can enqueue a whole
@@ -560,20 +441,23 @@ def main():
     graphs = None
     G = args.graph_steps or next(g for g in range(GMAX, 0, -1) if args.steps % g == 0)  # steps chained per graph
     assert 1 <= G <= GMAX and args.steps % G == 0, "--graph-steps must divide --steps (and be <= 8)"
-    # graphs on every rank when the data-parallel exchange is the fused
-    # kernel (a plain launch, capturable; every rank replays the same
-    # sequence); the NCCL fallback runs eagerly
-    if not args.no_graph and (world == 1 or fused is not None):
+    graph_note = None
+    if not args.no_graph:
         # one CUDA graph per input set: the whole GA3C iteration replays as a
-        # single launch (kernel timing probes are captured as event nodes)
-        graphs = []
-        l_cap = launches_all()
-        for s in range(sets):
-            ctx.graph_begin()
-            for pos in range(G):
-                step(s * G + pos, pos)
-            graphs.append(ctx.graph_end())
-        launches_per_step = (launches_all() - l_cap) // (sets * G)
+        # single launch (kernel timing probes are captured as event nodes).
+        # The data-parallel exchange is captured too on every rank: the fused
+        # kernel is a plain launch and NCCL collectives are capturable.  If
+        # the NCCL capture fails, say so and run eagerly.
+        try:
+            graphs, launches_per_step = loop.capture(G)
+        except Exception as e:
+            if world == 1 or fused is not None:
+                raise
+            print(f"[bench] NCCL CAPTURE FAILED, running eagerly: {e}", file=sys.stderr)
+            graph_note = f"nccl capture failed: {e}"
+            graphs = None
+            torch.cuda.synchronize()
+    if graphs is not None:
         if not args.no_graph_warm:
             for s in range(sets):  # warm the instantiated graphs
                 ctx.graph_launch(graphs[s])
@@ -611,13 +495,10 @@ def main():
     # fingerprint of the parameters the timed steps produced (every update
     # reads a fixed version, so this is schedule-independent: equal across
     # --graph-steps settings and runs unless a dependency is missing)
-    th_now = torch.zeros(P, dtype=torch.float32, device="cuda")
+    theta_fingerprint = None
     if NT > 1:
-        class _V:
-            __cuda_array_interface__ = {"shape": (P,), "typestr": "<f4", "version": 3, "strides": None,
-                                        "data": (_abi.slot_theta_ptr(model, ring[0]), False)}
-        th_now = torch.as_tensor(_V(), device="cuda")
-    theta_fingerprint = float(th_now.double().abs().sum().item()) if NT > 1 else None
+        th_now, _ = model.read_slot(loop.latest_slot())
+        theta_fingerprint = float(np.abs(th_now.astype(np.float64)).sum())
     probe_steps = args.steps
     if graphs is not None:
         # the probed kernel timed inside the real step: one more G-step graph,
@@ -708,6 +589,7 @@ def main():
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "ga3c_loop": loop, "gpu_launches": launches,
             "clocks": clk, "kernel_breakdown_ms_per_step": breakdown,
             "cuda_graph": graphs is not None, "steps_per_graph": G if graphs is not None else None,
+            "graph_note": graph_note, "dp_fallback": getattr(args, "dp_fallback", None),
             "theta_fingerprint": theta_fingerprint,
         }
         print(json.dumps(out), flush=True)

@@ -98,6 +98,9 @@ void ga3c_model_destroy(ga3c_model* m);
 /* Install theta (fp32, P values), g (nullable = zeros, init_rms nnet.cpp:170)
  * and version as a new snapshot. */
 int ga3c_model_load(ga3c_model* m, const float* theta, const float* g, uint64_t version);
+/* Copy parameter slot `slot` (theta and/or g, nullable) to the host after
+ * every write to it in flight on any stream (device synchronise). */
+int ga3c_model_read_slot(ga3c_model* m, int slot, float* theta, float* g);
 /* Copy the latest snapshot out (ModelState/RmsState nnet.hpp:35-44). */
 int ga3c_model_read(ga3c_model* m, float* theta, float* g, uint64_t* version);
 /* SharedModel::version pipeline.hpp:98 */
@@ -193,11 +196,11 @@ int ga3c_ctx_read_grad(ga3c_ctx* c, float* dtheta, double* scalars);
 /* Optional global-norm clip of the context gradient (nnet.cpp:281-289). */
 int ga3c_clip_grad(ga3c_ctx* c);
 
-/* Recompute the context gradient's non-finite flag (reset + scan of all P
- * values) on the context stream: after an in-place data-parallel all-reduce
- * the flag must describe the SUMMED gradient, so that every replica rejects
- * or applies the same step (nnet.cpp:299-301). */
-int ga3c_check_grad(ga3c_ctx* c);
+/* Recompute the non-finite flag of grad_from's gradient (NULL = c; reset +
+ * scan of all P values) on c's stream: after an in-place data-parallel
+ * all-reduce the flag must describe the SUMMED gradient, so that every
+ * replica rejects or applies the same step (nnet.cpp:299-301). */
+int ga3c_check_grad(ga3c_ctx* c, ga3c_ctx* grad_from);
 /* ------------------------------------------------------------ rmsprop */
 /* SharedModel::apply pipeline.cpp:37-63 -> nnet::rmsprop_update
  * nnet.cpp:293-312: one non-centred RMSProp step on the LATEST parameters,

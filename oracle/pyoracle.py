@@ -207,6 +207,39 @@ def loss_and_gradients(spec, hyper, theta, states, actions, returns):
     return d, sc
 
 
+def _chunks(B, threads):
+    k = max(1, min(threads, B))
+    edges = np.linspace(0, B, k + 1).astype(int)
+    return [(a, b) for a, b in zip(edges[:-1], edges[1:]) if b > a]
+
+
+def forward_mt(spec, theta, states, threads=None):
+    """forward over row chunks on `threads` host threads (ctypes releases
+    the GIL); rows are independent, so the result equals forward()."""
+    from concurrent.futures import ThreadPoolExecutor
+    states = np.ascontiguousarray(states, np.float64).reshape(-1, input_dim(spec))
+    parts = _chunks(states.shape[0], threads or os.cpu_count() or 1)
+    with ThreadPoolExecutor(len(parts)) as ex:
+        res = list(ex.map(lambda ab: forward(spec, theta, states[ab[0]:ab[1]]), parts))
+    return np.concatenate([r[0] for r in res]), np.concatenate([r[1] for r in res])
+
+
+def loss_and_gradients_mt(spec, hyper, theta, states, actions, returns, threads=None):
+    """loss_and_gradients as a sum of per-chunk sums on host threads (the
+    batch sum is associative up to fp64 rounding, far below the fp32 parity
+    tolerances this is checked against).  No clip (grad_clip_norm must be 0)."""
+    from concurrent.futures import ThreadPoolExecutor
+    assert hyper.grad_clip_norm == 0.0
+    states = np.ascontiguousarray(states, np.float64).reshape(-1, input_dim(spec))
+    actions = np.ascontiguousarray(actions, np.int32)
+    returns = np.ascontiguousarray(returns, np.float64)
+    parts = _chunks(states.shape[0], threads or os.cpu_count() or 1)
+    with ThreadPoolExecutor(len(parts)) as ex:
+        res = list(ex.map(lambda ab: loss_and_gradients(spec, hyper, theta, states[ab[0]:ab[1]],
+                                                        actions[ab[0]:ab[1]], returns[ab[0]:ab[1]]), parts))
+    return sum(r[0] for r in res), sum(r[1] for r in res)
+
+
 def rmsprop_update(hyper, theta, g, dtheta):
     P = len(theta)
     to, go = np.zeros(P), np.zeros(P)

@@ -137,7 +137,8 @@ _SIGS = {
     "ga3c_ctx_last_values": (_P, [_P]),
     "ga3c_ctx_read_grad": (C.c_int, [_P, _P, _P]),
     "ga3c_clip_grad": (C.c_int, [_P]),
-    "ga3c_check_grad": (C.c_int, [_P]),
+    "ga3c_check_grad": (C.c_int, [_P, _P]),
+    "ga3c_model_read_slot": (C.c_int, [_P, C.c_int, _P, _P]),
     "ga3c_rmsprop_flat": (C.c_int, [C.POINTER(HyperC), C.c_int, C.c_size_t, _P, _P, _P, C.POINTER(C.c_int)]),
     "ga3c_apply_rmsprop": (C.c_int, [_P, _P, C.POINTER(C.c_int), C.POINTER(C.c_uint64)]),
     "ga3c_apply_rmsprop_dev": (C.c_int, [_P]),
@@ -268,6 +269,13 @@ class Model:
         v = C.c_uint64(0)
         check(lib.ga3c_model_read(self.h, ptr(th), ptr(g), C.byref(v)), self.error())
         return th, g, v.value
+
+    def read_slot(self, slot):
+        """theta and g of one parameter slot (after all in-flight writes)."""
+        th = np.zeros(self.P, np.float32)
+        g = np.zeros(self.P, np.float32)
+        check(lib.ga3c_model_read_slot(self.h, slot, ptr(th), ptr(g)), self.error())
+        return th, g
 
     def version(self):
         return int(lib.ga3c_model_version(self.h))
@@ -440,9 +448,10 @@ class Context:
     def clip_grad(self):
         check(lib.ga3c_clip_grad(self.h), self.model.error())
 
-    def check_grad(self):
-        """Recompute the non-finite flag of the (all-reduced) gradient."""
-        check(lib.ga3c_check_grad(self.h), self.model.error())
+    def check_grad(self, grad_from=None):
+        """Recompute the non-finite flag of the (all-reduced) gradient of
+        grad_from (default: this context), on this context's stream."""
+        check(lib.ga3c_check_grad(self.h, grad_from.h if grad_from is not None else None), self.model.error())
 
     def time_kernel(self, tag, layer=-1):
         check(lib.ga3c_ctx_time_kernel(self.h, K_TAGS[tag] if isinstance(tag, str) else tag, layer))

@@ -1450,6 +1450,17 @@ int ga3c_model_read(ga3c_model* m, float* theta, float* g, uint64_t* version) {
   return rc;
 }
 
+int ga3c_model_read_slot(ga3c_model* m, int slot, float* theta, float* g) {
+  if (!m || slot < 0 || slot >= m->slots.size()) return GA3C_INVALID_ARGUMENT;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  if (set_device(m)) return GA3C_CUDA_ERROR;
+  GA3C_CUDA(cudaDeviceSynchronize());
+  const std::size_t bytes = m->lo.total * sizeof(float);
+  if (theta) GA3C_CUDA(cudaMemcpy(theta, m->slots[slot].theta, bytes, cudaMemcpyDeviceToHost));
+  if (g) GA3C_CUDA(cudaMemcpy(g, m->slots[slot].g, bytes, cudaMemcpyDeviceToHost));
+  return GA3C_OK;
+}
+
 uint64_t ga3c_model_version(ga3c_model* m) {
   std::lock_guard<std::mutex> lk(m->read_m);
   return m->slots[m->cur].version;
@@ -1799,16 +1810,17 @@ int ga3c_clip_grad(ga3c_ctx* c) {
   return GA3C_OK;
 }
 
-int ga3c_check_grad(ga3c_ctx* c) {
-  if (!c) return GA3C_INVALID_ARGUMENT;
+int ga3c_check_grad(ga3c_ctx* c, ga3c_ctx* grad_from) {
+  if (!c || (grad_from && grad_from->m != c->m)) return GA3C_INVALID_ARGUMENT;
+  ga3c_ctx* g = grad_from ? grad_from : c;
   ga3c_model* m = c->m;
   auto set_err = [&](const std::string& e) { m->set_error(e); };
-  GA3C_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int), c->cur));
+  GA3C_CUDA(cudaMemsetAsync(g->flag, 0, sizeof(int), c->cur));
   {
     Launch l(c, GA3C_K_OTHER, -1);
-    pdl_launch(c->cur, check_finite_kernel, dim3(kNumSMs), dim3(256), 0, (const float*)c->grad, m->lo.total, c->flag);
+    pdl_launch(c->cur, check_finite_kernel, dim3(kNumSMs), dim3(256), 0, (const float*)g->grad, m->lo.total, g->flag);
   }
-  c->grad_flag = -1;
+  g->grad_flag = -1;
   GA3C_CUDA(cudaGetLastError());
   return GA3C_OK;
 }

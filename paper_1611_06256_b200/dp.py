@@ -69,6 +69,17 @@ def dp_update(ctx, d_states, u8, d_actions, d_returns, B_local, slot, gview, str
     ctx.apply_rmsprop_dev()
 
 
+def nccl_update(lp, j, U):
+    """DeviceLoop data-parallel exchange over NCCL for update U (trainer
+    context j): all-reduce(sum) of the gradient on the loop's main stream,
+    the non-finite flag recomputed on the SUMMED gradient (so every replica
+    rejects or applies the same step, nnet.cpp:299-301), then the identical
+    RMSProp step on every replica.  All on one stream: capturable."""
+    allreduce_sum_(lp.tgrad[j], lp.stream)
+    lp.ctx.check_grad(lp.tctx[j])
+    lp.ctx.apply_slots_dev(lp.tctx[j], lp.ring[U % lp.R], lp.ring[(U + 1) % lp.R])
+
+
 def peer_lists(local, gathered, rank, opener):
     """Per-rank pointer lists from every rank's {name: [pointers or handles]}:
     this rank's own pointers as they are, the peers' opened with `opener`."""
@@ -113,21 +124,22 @@ class FusedUpdate:
         self.dp.apply(ctx, self.ctxs[j], src_slot, dst_slot, self.peers["grad"][j], self.peers["theta"][dst],
                       self.peers["sig"][0])
 
-    def self_check(self, ctx, j, P, device, src, dst_fused, dst_ref, stream=None):
-        """One fused update against NCCL all-reduce + ga3c_apply_rmsprop_slots_dev
-        on the same synthetic gradients (bitwise, on every rank); the two
-        destination slots are restored from src afterwards.  Returns True
-        when every rank agrees; on False the caller uses the NCCL path."""
+    def self_check(self, ctx, j, P, device, src, dst_fused, dst_ref):
+        """One fused update against its definition, bitwise on every rank:
+        all-gather every rank's gradient, sum it in rank order in fp32 (the
+        order the fused kernel reduces in -- NCCL's ring/NVLS order is not
+        rank order, so NCCL is not the reference here), load the sum into
+        context j's gradient and run the single-GPU RMSProp kernel
+        (ga3c_apply_rmsprop_slots_dev) from the same source slot.  Raises
+        RuntimeError (naming the rank and the first mismatching index) if any
+        rank differs; the destination slots are restored from src."""
         import torch
         import torch.distributed as dist
 
-        rank = dist.get_rank()
+        rank, world = dist.get_rank(), dist.get_world_size()
         gv = grad_view(self.ctxs[j], P, device)
-
-        def fill():
-            i = torch.arange(P, device=device, dtype=torch.int64)
-            gv.copy_((((i * 7 + rank * 13) % 101) - 50).to(torch.float32) * 1e-4)
-
+        i = torch.arange(P, device=device, dtype=torch.int64)
+        mine = ((((i * 7 + rank * 13) % 101) - 50).to(torch.float32) * 1e-4 * (1 + rank)).contiguous()
         from . import _abi
 
         def theta(slot):
@@ -136,27 +148,35 @@ class FusedUpdate:
                                             "data": (_abi.slot_theta_ptr(self.dp.model, slot), False)}
             return torch.as_tensor(_V(), device=device)
 
-        ok = True
+        err = ""
         try:  # no collectives in here: a failure must not desynchronise the ranks
-            fill()
+            gv.copy_(mine)
             torch.cuda.synchronize()
             self.apply(ctx, j, src, dst_fused)
             self.dp.check()
-        except Exception:
-            ok = False
-        fill()
-        torch.cuda.synchronize()
-        allreduce_sum_(gv)  # every rank, exactly once
+        except Exception as e:
+            err = f"fused apply failed: {e}"
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine)  # every rank, exactly once
+        acc = parts[0].clone()
+        for q in range(1, world):
+            acc = acc + parts[q]  # fp32, rank order
+        gv.copy_(acc)
         torch.cuda.synchronize()
         ctx.apply_slots_dev(self.ctxs[j], src, dst_ref)
         ctx.sync()
-        ok = ok and bool(torch.equal(theta(dst_fused), theta(dst_ref)))
+        a, b = theta(dst_fused), theta(dst_ref)
+        if not err and not torch.equal(a, b):
+            k = int(torch.nonzero(a != b)[0].item())
+            err = f"theta'[{k}] fused {a[k].item()!r} != rank-order reference {b[k].item()!r}"
         ctx.copy_slot_dev(src, dst_fused)
         ctx.copy_slot_dev(src, dst_ref)
         ctx.sync()
-        flag = torch.tensor([1 if ok else 0], device=device)
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        return bool(flag.item())
+        flag = torch.tensor([1 if err else 0], device=device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+        if flag.item():
+            raise RuntimeError(f"fused DP self-check failed (rank {rank}: {err or 'ok'}; another rank failed)")
+        return True
 
     def close(self):
         from . import _abi

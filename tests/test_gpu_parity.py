@@ -171,6 +171,30 @@ def test_large_dnn_stride1():
     check_grad(spec, th, fr, st, acts, rets)
 
 
+@pytest.mark.parametrize("sms", [0, 111])
+def test_large1_bench_batches(sms):
+    """large s1 at the batch sizes its bench line runs: predictor forward at
+    B = 128 (the persistent int8 conv1 path) and loss/backward at B = 40,
+    against the oracle (threaded over the batch); whole-GPU plans (the
+    large-net default) and the shared 111-SM trainer plan."""
+    spec = O.dnn_large(1)
+    th = theta32(spec, O.derive_seed(1, [O.SEED_MODEL_INIT]))
+    m, ctx = make(spec, max_batch=128)
+    m.load(th)
+    ctx.set_sm_budget(sms)
+    fr = O.synthetic_frames(11, 128)
+    st = O.frames_to_states(fr)
+    pi, v, _ = ctx.forward(fr)
+    rpi, rv = O.forward_mt(spec, th.astype(np.float64), st)
+    assert np.max(np.abs(pi - rpi)) <= 2e-6, np.max(np.abs(pi - rpi))
+    assert np.max(np.abs(v - rv)) <= 1e-5 * max(1.0, np.max(np.abs(rv)))
+    acts, rets = O.synthetic_batch(11, 40, 6)
+    d, sc = ctx.loss_grad(fr[:40], acts, rets)
+    rd, rsc = O.loss_and_gradients_mt(spec, HYPER, th.astype(np.float64), st[:40], acts, rets)
+    grad_close(d, rd)
+    assert np.allclose(sc, rsc, rtol=1e-5, atol=1e-6), (sc, rsc)
+
+
 def test_conv_small_golden(golden):
     g = golden("conv_small")
     spec = O.make_spec((12, 12, 2), [(4, 4, 2), (6, 3, 1)], [16], 3)
