@@ -21,8 +21,9 @@ Checked:
   * the step-0 n-step returns within 1e-5 of the oracle's (returns.cpp:8-26,
     bootstrapped with the oracle's own V);
   * theta and the RMSProp accumulator g after 32 updates against the
-    oracle's fp64 trajectory: max |dtheta| <= 5e-5 and <= 2e-3 of the total
-    parameter movement ||theta_32 - theta_0||_inf; g relative to max g <= 1e-3.
+    oracle's fp64 trajectory: max |dtheta| <= 1e-5 and <= 1e-3 of the total
+    parameter movement ||theta_32 - theta_0||_inf; g relative to max g <= 2e-4
+    (measured on B200: 2.5e-7, 1.2e-5 of the movement, g 1.4e-5).
     (fp32 device arithmetic with 3xTF32 GEMMs; RMSProp's normalised steps
     carry the gradient's ~1e-6 relative error into theta at ~eta per update.)
 """
@@ -119,5 +120,5 @@ def test_headline_schedule_matches_oracle():
     gerr = np.max(np.abs(g_dev.astype(np.float64) - g)) / np.max(np.abs(g))
     print(f"theta after 32 updates: max |dev - oracle| {err:.3e}, movement {move:.3e} (ratio {err / move:.2e}); "
           f"g rel {gerr:.2e}")
-    assert err <= 5e-5 and err <= 2e-3 * move, (err, move)
-    assert gerr <= 1e-3, gerr
+    assert err <= 1e-5 and err <= 1e-3 * move, (err, move)
+    assert gerr <= 2e-4, gerr
