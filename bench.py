@@ -74,8 +74,10 @@ def parse():
     p.add_argument("--trainers", type=int, default=3,
                    help="trainer contexts in flight in the device step (N_T, policy lag N_T - 1 updates)")
     p.add_argument("--cpu-seconds", type=float, default=6.0)
-    p.add_argument("--probe", default="conv_fwd:0",
-                   help="kernel class[:layer] for the roofline probe (auto = largest eager share)")
+    p.add_argument("--probe", default="auto",
+                   help="kernel class[:layer] for the headline roofline (auto = the largest in-step share)")
+    p.add_argument("--no-large", action="store_true",
+                   help="skip the large1 sub-line of the default (dnn_a, 1 GPU) run")
     p.add_argument("--trainer-sms", type=int, default=0,
                    help="N_T > 1: SMs each trainer context's split-K plans fill (ga3c_ctx_set_sm_budget); "
                         "0 = auto: 3/4 of them when an update is latency-bound (< 50 MFLOP/sample), else all")
@@ -151,11 +153,21 @@ def work_per_step(net, agents, tmax, tb):
 
 
 def bytes_per_step(net, agents, tmax, tb):
-    """Algorithmic HBM bytes per step of each forward-layer class: the layer's
-    input (u8 frames for conv1, fp32 activations otherwise) and its fp32
-    output, read/written once per launch (weights are negligible)."""
+    """Algorithmic HBM bytes per step of each kernel class, every operand
+    moved once per launch:
+      conv_fwd / fc_fwd[l]  layer input (u8 frames for layer 0, fp32
+                            activations otherwise) + fp32 output, per
+                            forwarded state (predictor + trainer recompute);
+      wgrad[l]              layer input + fp32 output gradient per trained
+                            sample, + the fp32 weight gradient per update;
+      dgrad[l]              fp32 output gradient in + fp32 input gradient out
+                            per trained sample (+ the weights per update);
+      rmsprop               theta, g, dtheta read + theta', g' written = 20 B
+                            per parameter per update."""
     layers, _ = layer_geometry(net)
-    n_fwd = agents * tmax + agents * tmax  # predictor + trainer recompute
+    n_train = agents * tmax
+    n_fwd = 2 * n_train  # predictor + trainer recompute
+    updates = n_train // tb
     b = {}
     h, w, c = FRAME
     in_bytes = h * w * c  # u8 state
@@ -163,8 +175,92 @@ def bytes_per_step(net, agents, tmax, tb):
         out = l["N"] * l["P"] * 4
         key = "conv_fwd" if l["kind"] == "conv" else "fc_fwd"
         b[(key, li)] = float(in_bytes + out) * n_fwd
+        b[("wgrad", li)] = float(in_bytes + out) * n_train + 4.0 * l["params"] * updates
+        if li > 0:
+            b[("dgrad", li)] = float(out + in_bytes) * n_train + 4.0 * l["params"] * updates
         in_bytes = out
+    b[("rmsprop", -1)] = 20.0 * param_count(net) * updates
     return b
+
+
+# Tensor-core work each kernel class issues per algorithmic FLOP, and the MMA
+# kind: 3xTF32 = A_hi*[B_hi|B_lo] + A_lo*B_hi (3 MMA FLOPs per
+# FLOP) with the exact-u8 operand skipping A_lo (2); conv1 forward runs the
+# exact int8 digits kernel (4 s8 digit MMAs) for predictor batches and the
+# 3-piece bf16 kernel for trainer batches -- mixed, charged here as int8.
+def issued(key):
+    tag, li = key
+    if tag == "conv_fwd" and li == 0:
+        return "i8", 4.0
+    if tag == "wgrad" and li == 0:
+        return "tf32", 2.0
+    if tag in ("conv_fwd", "fc_fwd", "wgrad", "dgrad"):
+        return "tf32", 3.0
+    return None, 0.0
+
+
+def tc_peaks():
+    """Dense tcgen05 peaks measured on the box by tools/tc_peak.cu
+    (profiles/r2_tc_peaks.json): tf32 / bf16 TFLOP/s and i8 TOP/s."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_tc_peaks.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def kernel_roofline(args, key, ms, launches, steps, ms_step, tc):
+    """One kernel class against its own roofline from in-step timings: the
+    lower of the measured HBM bandwidth x arithmetic intensity and the
+    measured bf16 tensor peak decides the bound; the tensor fraction against
+    the peak of the MMA kind the kernel actually issues is reported beside."""
+    hbm, bf16, bf16_sus, peak_src = measured_peaks()
+    NA, T, TB = args.agents, args.tmax, args.train_batch
+    flops = work_per_step(args.net, NA, T, TB)[key] * steps
+    byts = bytes_per_step(args.net, NA, T, TB).get(key, 0.0) * steps
+    sec = max(ms, 1e-9) / 1e3
+    r = {"kernel": f"{key[0]}[layer {key[1]}]", "launches": launches, "avg_launch_us": 1e3 * ms / max(1, launches),
+         "share_of_step": ms / (ms_step * steps), "algorithmic_bytes_per_launch": byts / max(1, launches)}
+    if key[0] == "rmsprop":
+        r.update({"bound": "hbm", "achieved": flops / sec / 1e9, "peak": hbm, "unit": "GB/s"})
+    else:
+        ai = flops / byts
+        r["arithmetic_intensity_flop_per_byte"] = ai
+        r["ridge_flop_per_byte"] = bf16 * 1e3 / hbm
+        r["tflops_achieved"] = flops / sec / 1e12
+        r["tflops_frac_of_bf16_peak"] = r["tflops_achieved"] / bf16
+        if ai < bf16 * 1e3 / hbm:
+            r.update({"bound": "hbm", "achieved": byts / sec / 1e9, "peak": hbm, "unit": "GB/s"})
+        else:
+            r.update({"bound": "tensor", "achieved": r["tflops_achieved"], "peak": bf16, "unit": "TFLOP/s"})
+        kind, mult = issued(key)
+        pk = {"tf32": tc.get("tf32_tflops"), "i8": tc.get("i8_tops"), "bf16": tc.get("bf16_tflops")}.get(kind)
+        if kind and pk:
+            r["issued_mma"] = kind
+            r["issued_tensor_frac"] = r["tflops_achieved"] * mult / pk
+    r["frac"] = r["achieved"] / r["peak"]
+    r["peak_source"] = f"{peak_src} ({'HBM copy' if r['bound'] == 'hbm' else 'cuBLAS bf16 burst'})"
+    traffic, src = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get(args.net, {}).get(f"{key[0]}[{key[1]}]" if key[1] >= 0 else key[0])
+        if tr:
+            traffic, src = tr["bytes_per_launch"], f"{tr['launch']}; {tr['capture']}"
+    except (OSError, ValueError, KeyError):
+        pass
+    r["traffic"], r["traffic_source"] = traffic, src
+    return r
+
+
+def sample_rows(pi, u):
+    """qac::sample_index (util.hpp:46-54) per row: the first a with
+    u < sum_{<=a} pi accumulated left to right in fp64, else the last action.
+    pi is the device's fp64 softmax (ga3c_*64 calls), so this draws exactly
+    the action the on-device sampler draws."""
+    hit = u[:, None] < np.cumsum(pi, 1)
+    a = hit.argmax(1)
+    a[~hit.any(1)] = pi.shape[1] - 1
+    return a
 
 
 def fwd_flops_per_sample(net):
@@ -231,81 +327,108 @@ def measured_peaks():
 
 # ------------------------------------------------------------- CPU oracle
 
-def cpu_leg(net, agents, tmax, tb, seconds):
-    """The reference CPU path (fp64 oracle restatement) on all host threads:
-    the same GA3C iteration's forward, loss_and_gradients and RMSProp work."""
+def cpu_iteration(net, agents, tmax, tb, max_steps, budget_s, warmup=1):
+    """The reference's CPU path EXECUTING the same GA3C iteration (not a
+    model of it): the fp64 oracle restatement of nnet.cpp / returns.cpp /
+    util.hpp (oracle/libga3c_oracle.so, the reference's own code has no conv
+    layers) runs t_max predictor forwards of N_A states + sample_index +
+    per-agent compute_returns, then N_A*t_max/min_train_batch updates of
+    loss_and_gradients + rmsprop_update, with every host thread working on
+    each call (rows split across threads: an upper bound on the reference's
+    own N_P/N_T thread parallelism).  Steps run until max_steps or budget_s;
+    the value is N_A*t_max samples over the median step time."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as O
     convs, hidden = NETS[net]
     spec = O.make_spec(FRAME, convs, hidden, N_ACTIONS)
     hp = O.Hyper()
     th = O.init_model(spec, O.derive_seed(1, [O.SEED_MODEL_INIT])).astype(np.float32).astype(np.float64)
+    g = np.zeros_like(th)
     threads = os.cpu_count() or 1
-    fb = min(agents, 8)
-    frames = O.synthetic_frames(3, fb)
-    st = O.frames_to_states(frames)
-    acts, rets = O.synthetic_batch(3, fb, N_ACTIONS)
-    fwd_rate, n_fwd = O.throughput(spec, hp, th, st, acts, rets, 0, threads, seconds / 2)
-    tr_rate, n_tr = O.throughput(spec, hp, th, st, acts, rets, 1, threads, seconds / 2)
-    P = th.size
-    g = np.zeros(P)
-    d = np.full(P, 1e-3)
-    t0 = time.perf_counter()
-    reps = 0
-    while time.perf_counter() - t0 < min(1.0, seconds / 6) or reps < 1:
-        O.rmsprop_update(hp, th, g, d)
-        reps += 1
-    t_rms = (time.perf_counter() - t0) / reps
+    rng = np.random.default_rng(1234)
     n = agents * tmax
     updates = n // tb
-    t_step = n / fwd_rate + n / tr_rate + updates * t_rms  # rmsprop is serialized (pipeline.cpp:40)
-    return dict(value=n / t_step, fwd_rate=fwd_rate, train_rate=tr_rate, t_rms=t_rms, threads=threads,
-                sample=(f"{net}: {n_fwd} forwards + {n_tr} loss_and_gradients (batch {fb}/thread) on "
-                        f"{threads} threads over {seconds:.0f}s, {reps} single-thread rmsprop_update; "
-                        f"step = {n} predictions + {n} trained samples + {updates} updates"))
+    states = rng.integers(0, 256, (agents, tmax) + FRAME, dtype=np.uint8).reshape(agents, tmax, -1) / 256.0
+    uni = rng.random((tmax, agents))
+    rewards = rng.random((agents, tmax)) * 2 - 1
+    terminal = rng.random(agents) < tmax / 64.0
+
+    def one():
+        nonlocal th, g
+        acts = np.zeros((agents, tmax), np.int32)
+        v = None
+        for t in range(tmax):
+            pi, v = O.forward_mt(spec, th, states[:, t], threads)
+            acts[:, t] = sample_rows(pi, uni[t])
+        rets = np.stack([O.compute_returns(rewards[a], bool(terminal[a]), 0.0 if terminal[a] else v[a], hp.gamma)
+                         for a in range(agents)])
+        X, A, R = states.reshape(n, -1), acts.reshape(-1), rets.reshape(-1)
+        for u in range(updates):
+            sl = slice(u * tb, (u + 1) * tb)
+            d, _ = O.loss_and_gradients_mt(spec, hp, th, X[sl], A[sl], R[sl], threads)
+            th, g, _ = O.rmsprop_update(hp, th, g, d)
+
+    for _ in range(warmup):
+        one()
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max(1, max_steps) and (not times or time.perf_counter() - t_start < budget_s):
+        t0 = time.perf_counter()
+        one()
+        times.append(time.perf_counter() - t0)
+    med = float(np.median(times))
+    return dict(value=n / med, threads=threads, steps=len(times), s_per_step=med,
+                sample=(f"{net}: {len(times)} executed GA3C iterations ({tmax} x {agents} forwards + sampling + "
+                        f"returns, {updates} x (loss_and_gradients on {tb} + rmsprop_update)) on {threads} "
+                        f"threads, {med:.2f} s median per step, after {warmup} warm-up step(s)"))
 
 
 def run_reference(args, rank):
     if rank != 0:
         return
-    # bounded: one short warm-up sample, then up to 3 step samples of a few
-    # seconds of CPU work each (the whole arm stays within ~a minute)
-    seconds = max(1.0, args.cpu_seconds / 2)
-    cpu_leg(args.net, args.agents, args.tmax, args.train_batch, 0.5)
-    vals = []
-    for _ in range(max(1, min(args.steps, 3))):
-        r = cpu_leg(args.net, args.agents, args.tmax, args.train_batch, seconds)
-        vals.append(r["value"])
-    v = float(np.median(vals))
+    # bounded: one warm-up step, then up to --steps executed steps within
+    # ~60 s of CPU work (the whole arm ends within a few minutes)
+    r = cpu_iteration(args.net, args.agents, args.tmax, args.train_batch, args.steps, 60.0,
+                      warmup=min(1, args.warmup))
+    v = r["value"]
     n = args.agents * args.tmax
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * n / v,
+        "steps": r["steps"], "warmup": args.warmup, "ms_per_step": 1e3 * n / v,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_of(args, 1),
+        "data": "synthetic", "config": config_of(args, int(os.environ.get("WORLD_SIZE", "1"))),
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": r["threads"], "kind": "port",
-                         "sample": r["sample"] + f"; median of {len(vals)} step samples"},
+                         "sample": r["sample"]},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
-def config_of(args, world, sets=None):
+def config_of(args, world):
+    """The workload, identical for both arms (no run-specific keys)."""
+    from paper_1611_06256_b200.loop import mean_policy_lag
     n = args.agents * args.tmax
+    updates = n // args.train_batch
+    overlap = args.trainers > 1 and not args.no_overlap
     return {"workload": f"GA3C iteration ({args.net}): {args.tmax} predictor batches of {args.agents} "
-                        f"agents + n-step returns + {n // args.train_batch} trainer updates of "
+                        f"agents + n-step returns + {updates} trainer updates of "
                         f"{args.train_batch} samples (loss/backward + RMSProp) per GPU",
             "net": args.net, "agents_per_gpu": args.agents, "t_max": args.tmax,
             "predictor_batch": args.agents, "min_train_batch": args.train_batch,
-            "global_train_batch": args.train_batch * world, "updates_per_step": n // args.train_batch,
+            "global_train_batch": args.train_batch * world, "updates_per_step": updates,
             "params": param_count(args.net), "parallelism": f"dp{world}",
-            "trainers_in_flight": args.trainers, "policy_lag_updates": args.trainers - 1,
-            "predictor_trainer_overlap": args.trainers > 1 and not args.no_overlap,
+            "trainers_in_flight": args.trainers,
+            # gradient computed on version U - (N_T - 1), applied on version U
+            "gradient_staleness_updates": args.trainers - 1,
+            # the reference's lag metric, applied_on - produced_version
+            # (pipeline.cpp:289-291), averaged over the step's experiences
+            # (paper_1611_06256_b200/loop.py)
+            "mean_policy_lag_updates": mean_policy_lag(updates, overlap) if args.trainers > 1
+            else (updates - 1) / 2,
+            "predictor_trainer_overlap": overlap,
             "dp_update": (args.dp if world > 1 and args.trainers > 1 else
                           ("nccl" if world > 1 else "none (1 GPU)")),
             "trainer_sm_budget": args.trainer_sms if args.trainers > 1 else 148,
-            "predictor_sm_budget": (args.pred_sms if args.trainers > 1 and not args.no_overlap else None),
-            "l2": (f"inputs cycled over {sets} sets = {sets * n * FRAME_BYTES / 1e6:.0f} MB > 126 MB L2"
-                   if sets else "n/a")}
+            "predictor_sm_budget": (args.pred_sms if overlap else None)}
 
 
 # ----------------------------------------------------------------- GPU arm
@@ -431,7 +554,7 @@ def main():
             for tag, li, sid, a, b in tl:
                 f.write(f"{a:9.4f} {b:9.4f} {1e3 * (b - a):8.2f}  s{sid}  {tag}[{li}]\n")
     work = work_per_step(args.net, NA, T, TB)
-    if args.probe == "auto":
+    if args.probe == "auto":  # eager guess; re-chosen from the in-step timings below
         cand = [(breakdown.get(f"{t}[{l}]" if l >= 0 else t, 0.0), (t, l)) for (t, l) in work]
         probe = max(cand)[1]
     else:
@@ -499,25 +622,6 @@ def main():
     if NT > 1:
         th_now, _ = model.read_slot(loop.latest_slot())
         theta_fingerprint = float(np.abs(th_now.astype(np.float64)).sum())
-    probe_steps = args.steps
-    if graphs is not None:
-        # the probed kernel timed inside the real step: one more G-step graph,
-        # captured with event-record nodes around every launch of the probed
-        # kernel class (on the stream it runs on), replayed once after the
-        # timed region
-        time_kernel(probe[0], probe[1])
-        ctx.graph_begin()
-        for pos in range(G):
-            step(pos, pos)
-        pg = ctx.graph_end()
-        ctx.graph_launch(pg)
-        ctx.sync()
-        torch.cuda.synchronize()
-        probe_steps = G
-    probe_ms, probe_n = kernel_time()
-    time_kernel("none")
-    probe_pass = ("one extra replay of a graph of the timed steps with event nodes around the probed "
-                  "kernel's launches" if graphs is not None else "inside the timed region")
     if world > 1:
         t = torch.tensor([ms_total], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -526,41 +630,38 @@ def main():
     ms_step = ms_total / args.steps
     value = world * n / (ms_step / 1e3)
 
-    hbm, bf16, bf16_sus, peak_src = measured_peaks()
-    probed_steps = probe_steps
-    w = work[probe] * probed_steps
-    # the kernel's bound is the lower roofline: below the ridge (measured bf16
-    # peak / measured HBM bandwidth) its arithmetic intensity makes it HBM-bound
-    byts = bytes_per_step(args.net, NA, T, TB).get(probe)
-    ai = work[probe] / byts if byts else None
-    if probe[0] == "rmsprop":
-        achieved = w / (probe_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s"}
-    elif ai is not None and ai < bf16 * 1e3 / hbm:
-        achieved = byts * probed_steps / (probe_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "arithmetic_intensity_flop_per_byte": ai, "ridge_flop_per_byte": bf16 * 1e3 / hbm,
-                "tflops_achieved": w / (probe_ms / 1e3) / 1e12, "tflops_frac_of_bf16_peak":
-                w / (probe_ms / 1e3) / 1e12 / bf16}
+    # ---- every kernel class timed INSIDE the real step ----
+    # One more G-step graph per class, captured with event-record nodes
+    # around every launch of that class (on the stream it runs on) and
+    # replayed once after the timed region; eager (no graphs): the probe
+    # brackets ran inside the timed region for the headline class only.
+    per_class = {}
+    if graphs is not None:
+        for key in sorted(work):
+            time_kernel(key[0], key[1])
+            ctx.graph_begin()
+            for pos in range(G):
+                step(pos, pos)
+            pg = ctx.graph_end()
+            ctx.graph_launch(pg)
+            ctx.sync()
+            torch.cuda.synchronize()
+            per_class[key] = kernel_time() + (G,)
+            time_kernel("none")
+        if args.probe == "auto":
+            probe = max(per_class, key=lambda k: per_class[k][0])
     else:
-        achieved = w / (probe_ms / 1e3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s"}
-        if ai is not None:
-            roof.update({"arithmetic_intensity_flop_per_byte": ai, "ridge_flop_per_byte": bf16 * 1e3 / hbm})
-    traffic, traffic_src = None, None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f).get(args.net, {}).get(f"{probe[0]}[{probe[1]}]" if probe[1] >= 0 else probe[0])
-        if tr:
-            traffic, traffic_src = tr["bytes_per_launch"], f"{tr['launch']}; {tr['capture']}"
-    except (OSError, ValueError, KeyError):
-        pass
-    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": traffic, "traffic_source": traffic_src,
-                 "kernel": f"{probe[0]}[layer {probe[1]}]", "launches": probe_n,
-                 "avg_launch_us": 1e3 * probe_ms / max(1, probe_n),
-                 "share_of_step": probe_ms / (ms_step * probed_steps),
-                 "probe_pass": probe_pass,
-                 "peak_source": f"{peak_src} ({'HBM copy' if probe[0] == 'rmsprop' else 'cuBLAS bf16 burst'})"})
+        per_class[probe] = kernel_time() + (args.steps,)
+        time_kernel("none")
+    probe_pass = ("one extra replay of a graph of the timed steps with event nodes around the class's "
+                  "launches" if graphs is not None else "inside the timed region")
+    tc = tc_peaks()
+    rbk = {f"{k[0]}[{k[1]}]" if k[1] >= 0 else k[0]: kernel_roofline(args, k, *per_class[k], ms_step, tc)
+           for k in per_class}
+    roof = dict(rbk[f"{probe[0]}[{probe[1]}]" if probe[1] >= 0 else probe[0]])
+    roof["probe_pass"] = probe_pass
+    roof["selection"] = ("auto: the largest in-step share of the step time" if args.probe == "auto"
+                         else f"--probe {args.probe}")
 
     # ---- end to end through the C ABI with host buffers ----
     e2e = None
@@ -568,33 +669,62 @@ def main():
         e2e = e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world, grad_view,
                       stream, dist)
 
-    loop = None
+    loop_line = None
     if rank == 0 and world == 1 and not args.no_loop and args.net == "dnn_a":
-        loop = loop_leg(args)
+        loop_line = loop_leg(args)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        r = cpu_leg(args.net, NA, T, TB, args.cpu_seconds)
+        r = cpu_iteration(args.net, NA, T, TB, 1000, args.cpu_seconds)
         cpu = {"value": r["value"], "unit": "samples/s", "cores": r["threads"], "kind": "port",
                "sample": r["sample"]}
+
+    large = None
+    if rank == 0 and world == 1 and args.net == "dnn_a" and not args.no_large:
+        large = large_leg(args)
 
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (u8 84x84x4 frames, seeded weights)",
-            "config": config_of(args, world, sets),
+            "config": config_of(args, world),
+            "l2_flush": f"inputs cycled over {sets} sets = {sets * n * FRAME_BYTES / 1e6:.0f} MB > 126 MB L2",
             "pps": value, "tps_updates_per_s": updates / (ms_step / 1e3),
             "fwd_mflop_per_prediction": fwd_flops_per_sample(args.net) / 1e6,
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "ga3c_loop": loop, "gpu_launches": launches,
+            "roofline": roof, "roofline_by_kernel": rbk, "tc_peaks_measured": tc or None,
+            "cpu_baseline": cpu, "e2e": e2e, "ga3c_loop": loop_line, "gpu_launches": launches,
             "clocks": clk, "kernel_breakdown_ms_per_step": breakdown,
             "cuda_graph": graphs is not None, "steps_per_graph": G if graphs is not None else None,
             "graph_note": graph_note, "dp_fallback": getattr(args, "dp_fallback", None),
             "theta_fingerprint": theta_fingerprint,
+            "large1": large,
         }
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def large_leg(args):
+    """BASELINE configs[2] (the paper's larger DNN at stride 1) measured in the
+    same bench invocation: bench.py --net large1 in a child process on this
+    GPU, its line embedded (value, e2e, roofline, cpu_baseline, clocks)."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--net", "large1", "--steps", "64", "--warmup", "4",
+           "--no-loop", "--no-large", "--e2e-steps", "40"]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        if r.returncode != 0 or not line:
+            return {"error": f"rc {r.returncode}: {r.stderr[-400:]}"}
+        d = json.loads(line[-1])
+    except (OSError, subprocess.TimeoutExpired, ValueError) as e:
+        return {"error": str(e)}
+    keep = ("metric", "value", "unit", "ms_per_step", "steps", "warmup", "config", "l2_flush", "pps",
+            "tps_updates_per_s", "roofline", "roofline_by_kernel", "cpu_baseline", "e2e", "gpu_launches", "clocks",
+            "cuda_graph", "steps_per_graph", "theta_fingerprint")
+    d = {k: d.get(k) for k in keep}
+    d["command"] = " ".join(cmd[1:])
+    return d
 
 
 def loop_leg(args):
@@ -660,14 +790,11 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
         slots = np.zeros((NA, T), np.int32)
         v = None
         for t in range(T):
-            pi, v, sl, _ = _abi.predict_frames(ctx, store, newf[s][t], agents, prev_term if t == 0 else None)
+            pi, v, sl, _ = _abi.predict_frames(ctx, store, newf[s][t], agents, prev_term if t == 0 else None,
+                                               fp64=True)
             slots[:, t] = sl
-            cdf = np.cumsum(pi.astype(np.float64), 1)
-            hit = u_h[s, t][:, None] < cdf
-            a = hit.argmax(1)
-            a[~hit.any(1)] = N_ACTIONS - 1
-            acts[:, t] = a
-        boot = v.astype(np.float64)
+            acts[:, t] = sample_rows(pi, u_h[s, t])
+        boot = v
         for u in range(updates):
             sl = slice(u * per_upd, (u + 1) * per_upd)
             _abi.train_frames(ctx, store, np.repeat(agents[sl], T), slots[sl].reshape(-1), acts[sl].reshape(-1),
@@ -681,17 +808,16 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
             ctx.apply_rmsprop()
         prev_term = term_h[s].astype(np.uint8)
         h2d = (T * NA * (px + 4 * 4) + NA + updates * (TB * (4 + 4 + 4 + 8) + 4 * (per_upd + 1) + per_upd * 9))
-        d2h = T * NA * (N_ACTIONS + 1 + 1) * 4 + updates * (3 * 8 + TB * 8 + 4)
+        d2h = T * NA * (8 * N_ACTIONS + 8 + 4) + updates * (3 * 8 + TB * 8 + 4)  # fp64 pi + V, state slot
 
     def full_state_step(i):
         s = i % hs
         acts = np.zeros((NA, T), np.int32)
         v = None
         for t in range(T):
-            pi, v, _ = ctx.forward(fr_time[s][t])
-            acts[:, t] = np.minimum((u_h[s, t][:, None] < np.cumsum(pi.astype(np.float64), 1)).argmax(1),
-                                    N_ACTIONS - 1)
-        rets = ctx.compute_returns(r_h[s].reshape(-1), off, term_h[s], v.astype(np.float64), hyper.gamma)
+            pi, v, _ = ctx.forward(fr_time[s][t], fp64=True)
+            acts[:, t] = sample_rows(pi, u_h[s, t])
+        rets = ctx.compute_returns(r_h[s].reshape(-1), off, term_h[s], v, hyper.gamma)
         for u in range(updates):
             sl = slice(u * TB // T, (u + 1) * TB // T)
             ctx.loss_grad(fr_agent[s][sl].reshape(TB, -1), acts[sl].reshape(-1), rets[u * TB:(u + 1) * TB],
@@ -767,13 +893,9 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
         gs = groups[g]
         for t in range(T):
             pi, v, sl, _ = _abi.predict_frames(ctx_p[g], store, newf[s][t][gs], agents[gs],
-                                               pt[gs] if t == 0 else None)
+                                               pt[gs] if t == 0 else None, fp64=True)
             slots[gs, t] = sl
-            cdf = np.cumsum(pi.astype(np.float64), 1)
-            hit = u_h[s, t][gs, None] < cdf
-            a = hit.argmax(1)
-            a[~hit.any(1)] = N_ACTIONS - 1
-            acts[gs, t] = a
+            acts[gs, t] = sample_rows(pi, u_h[s, t][gs])
         vout[gs] = v
 
     def predict_step(i, pt):

@@ -310,6 +310,12 @@ void ga3c_frames_destroy(ga3c_frames* f);
 int ga3c_predict_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* new_frames,
                         const int32_t* agents, const uint8_t* resets, int n, int32_t* state_slots,
                         float* pi, float* v, uint64_t* version_used);
+/* The same with pi as the device's fp64 softmax and V widened to fp64 (see
+ * ga3c_forward64_u8): host-side qac::sample_index on these rows draws the
+ * action the on-device sampler draws. */
+int ga3c_predict_frames64(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* new_frames,
+                          const int32_t* agents, const uint8_t* resets, int n, int32_t* state_slots, double* pi,
+                          double* v, uint64_t* version_used);
 /* Trainer call: as ga3c_loss_grad_segments_u8, with sample b's state read
  * from the store at (agents[b], state_slots[b]) on the device. */
 int ga3c_train_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const int32_t* agents,

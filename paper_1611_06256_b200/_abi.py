@@ -163,6 +163,8 @@ _SIGS = {
     "ga3c_frames_destroy": (None, [_P]),
     "ga3c_predict_frames": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_int, _P, _P, _P,
                                       C.POINTER(C.c_uint64)]),
+    "ga3c_predict_frames64": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_int, _P, _P, _P,
+                                        C.POINTER(C.c_uint64)]),
     "ga3c_train_frames": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, _P, _P, _P, C.c_int, _P, _P, C.c_double,
                                     C.c_int, _P, _P]),
     "ga3c_frames_read": (C.c_int, [_P, C.c_int, C.c_int, _P]),
@@ -327,18 +329,22 @@ class Context:
         return int(lib.ga3c_ctx_launches(self.h))
 
     # --- host-buffer calls (blocking) -------------------------------------
-    def forward(self, states, slot=-1):
-        """states: (B, H*W*C) or (B,H,W,C) uint8 frames or float32 states."""
+    def forward(self, states, slot=-1, fp64=False):
+        """states: (B, H*W*C) or (B,H,W,C) uint8 frames or float32 states.
+        fp64: pi as the device's fp64 softmax, V widened (ga3c_forward64_*)."""
         states = np.ascontiguousarray(states)
         B = states.shape[0]
-        pi = np.zeros((B, self.A), np.float32)
-        v = np.zeros(B, np.float32)
+        dt = np.float64 if fp64 else np.float32
+        pi = np.zeros((B, self.A), dt)
+        v = np.zeros(B, dt)
         ver = C.c_uint64(0)
         if states.dtype == np.uint8:
-            rc = lib.ga3c_forward_u8(self.h, slot, ptr(states), B, ptr(pi), ptr(v), C.byref(ver))
+            fn = lib.ga3c_forward64_u8 if fp64 else lib.ga3c_forward_u8
+            rc = fn(self.h, slot, ptr(states), B, ptr(pi), ptr(v), C.byref(ver))
         else:
             states = np.ascontiguousarray(states, np.float32)
-            rc = lib.ga3c_forward_f32(self.h, slot, ptr(states), B, ptr(pi), ptr(v), C.byref(ver))
+            fn = lib.ga3c_forward64_f32 if fp64 else lib.ga3c_forward_f32
+            rc = fn(self.h, slot, ptr(states), B, ptr(pi), ptr(v), C.byref(ver))
         check(rc, self.model.error())
         return pi, v, ver.value
 
@@ -519,18 +525,21 @@ class Frames:
         return out
 
 
-def predict_frames(ctx: "Context", frames: Frames, new_frames, agents, resets=None, slot=-1):
-    """-> (pi [n][A], v [n], state_slots [n], version)."""
+def predict_frames(ctx: "Context", frames: Frames, new_frames, agents, resets=None, slot=-1, fp64=False):
+    """-> (pi [n][A], v [n], state_slots [n], version); fp64 = the device's
+    fp64 softmax and V (ga3c_predict_frames64)."""
     import numpy as np
     nf = np.ascontiguousarray(new_frames, np.uint8)
     ag = np.ascontiguousarray(agents, np.int32)
     n = len(ag)
     rs = None if resets is None else np.ascontiguousarray(resets, np.uint8)
-    pi = np.empty((n, ctx.model.n_actions), np.float32)
-    v = np.empty(n, np.float32)
+    dt = np.float64 if fp64 else np.float32
+    pi = np.empty((n, ctx.model.n_actions), dt)
+    v = np.empty(n, dt)
     slots = np.empty(n, np.int32)
     ver = C.c_uint64(0)
-    check(lib.ga3c_predict_frames(ctx.h, slot, frames.h, nf.ctypes.data, ag.ctypes.data,
+    fn = lib.ga3c_predict_frames64 if fp64 else lib.ga3c_predict_frames
+    check(fn(ctx.h, slot, frames.h, nf.ctypes.data, ag.ctypes.data,
                                   None if rs is None else rs.ctypes.data, n, slots.ctypes.data, pi.ctypes.data,
                                   v.ctypes.data, C.byref(ver)), ctx.model.error())
     return pi, v, slots, ver.value

@@ -27,6 +27,7 @@
 #include <functional>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "ga3c.h"
@@ -2449,9 +2450,15 @@ int ga3c_loss_grad_segments_u8(ga3c_ctx* c, int slot, const uint8_t* frames, int
 // states on the device, so the predictor reads its batch and the trainer
 // gathers its experiences without another host->device copy.
 
-int ga3c_predict_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* new_frames,
-                        const int32_t* agents, const uint8_t* resets, int n, int32_t* state_slots, float* pi,
-                        float* v, uint64_t* version_used) {
+}  // extern "C"
+
+// pi / v as fp32 (ga3c_predict_frames) or as the fp64 softmax and widened V
+// (ga3c_predict_frames64)
+template <typename OutT>
+static int predict_frames_impl(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* new_frames,
+                               const int32_t* agents, const uint8_t* resets, int n, int32_t* state_slots, OutT* pi,
+                               OutT* v, uint64_t* version_used) {
+  constexpr bool f64 = std::is_same<OutT, double>::value;
   if (!c || !f || f->m != c->m || n < 0 || n > c->max_batch || (n > 0 && (!new_frames || !agents || !pi || !v)))
     return GA3C_INVALID_ARGUMENT;
   ga3c_model* m = c->m;
@@ -2494,8 +2501,8 @@ int ga3c_predict_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* ne
     const int A = m->lo.n_actions;
     Stager sg{c};
     const int32_t* d_idx = sg.put(idx.data(), idx.size());
-    float* h_pi = sg.take<float>(static_cast<std::size_t>(n) * A);
-    float* h_v = sg.take<float>(n);
+    OutT* h_pi = sg.take<OutT>(static_cast<std::size_t>(n) * A);
+    OutT* h_v = sg.take<OutT>(n);
     if (!d_idx || !h_pi || !h_v) rc = GA3C_INVALID_ARGUMENT;
     if (!rc && (cudaMemcpyAsync(newf, new_frames, f->frame_px * n, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
                 !sg.flush()))
@@ -2509,8 +2516,10 @@ int ga3c_predict_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* ne
       }
       wait_slot(c, s);
       run_forward(c, m->slots[s].theta, dense, true, n);
-      if (cudaMemcpyAsync(h_pi, c->pi32, sizeof(float) * n * A, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
-          cudaMemcpyAsync(h_v, c->v, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+      const void* d_pi = f64 ? static_cast<const void*>(c->pi64) : static_cast<const void*>(c->pi32);
+      const void* d_v = f64 ? static_cast<const void*>(c->v64) : static_cast<const void*>(c->v);
+      if (cudaMemcpyAsync(h_pi, d_pi, sizeof(OutT) * n * A, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+          cudaMemcpyAsync(h_v, d_v, sizeof(OutT) * n, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
         rc = GA3C_CUDA_ERROR;
     }
     cudaError_t e = cudaStreamSynchronize(c->stream);
@@ -2519,13 +2528,27 @@ int ga3c_predict_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* ne
       set_err(std::string("predict_frames: ") + cudaGetErrorString(e));
     }
     if (!rc) {
-      std::memcpy(pi, h_pi, sizeof(float) * n * A);
-      std::memcpy(v, h_v, sizeof(float) * n);
+      std::memcpy(pi, h_pi, sizeof(OutT) * n * A);
+      std::memcpy(v, h_v, sizeof(OutT) * n);
     }
   }
   if (pinned_here) ga3c_snapshot_release(m, s);
   if (version_used) *version_used = ver;
   return rc;
+}
+
+extern "C" {
+
+int ga3c_predict_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* new_frames,
+                        const int32_t* agents, const uint8_t* resets, int n, int32_t* state_slots, float* pi,
+                        float* v, uint64_t* version_used) {
+  return predict_frames_impl(c, slot, f, new_frames, agents, resets, n, state_slots, pi, v, version_used);
+}
+
+int ga3c_predict_frames64(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* new_frames,
+                          const int32_t* agents, const uint8_t* resets, int n, int32_t* state_slots, double* pi,
+                          double* v, uint64_t* version_used) {
+  return predict_frames_impl(c, slot, f, new_frames, agents, resets, n, state_slots, pi, v, version_used);
 }
 
 int ga3c_train_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const int32_t* agents, const int32_t* state_slots,

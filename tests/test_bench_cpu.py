@@ -36,8 +36,25 @@ def test_reference_arm_json_contract():
     assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["value"] == d["value"]
     cfg = d["config"]
     assert cfg["net"] == "dnn_a" and cfg["updates_per_step"] == 16 and cfg["params"] == 677943
-    # the GPU arm resolves the same automatic budgets
+    # the GPU arm resolves the same automatic budgets and prints the same
+    # dict (config_of has no run-specific keys: the L2 note is top-level)
     assert cfg["trainer_sm_budget"] == 111 and cfg["predictor_sm_budget"] == 64
+    assert "l2" not in cfg
+    # the reference's lag metric (pipeline.cpp:289-291) for the overlapped
+    # N_T = 3 step: 16 + 15/2 updates
+    assert cfg["mean_policy_lag_updates"] == 23.5 and cfg["gradient_staleness_updates"] == 2
+    assert "executed GA3C iterations" in cb["sample"]
+
+
+def test_algorithmic_bytes_and_issued_work():
+    w = bench.work_per_step("dnn_a", 128, 5, 40)
+    b = bench.bytes_per_step("dnn_a", 128, 5, 40)
+    # every timed class has both its FLOPs and its bytes
+    assert set(w) <= set(b) | {k for k in w if k[0] == "rmsprop"}
+    assert b[("rmsprop", -1)] == 20.0 * 677943 * 16 == w[("rmsprop", -1)]
+    # conv1 weight gradient: u8 frame + fp32 output gradient per sample
+    assert b[("wgrad", 0)] == (28224 + 20 * 20 * 16 * 4) * 640 + 4 * (16 * 8 * 8 * 4 + 16) * 16
+    assert bench.issued(("wgrad", 0)) == ("tf32", 2.0) and bench.issued(("dgrad", 1)) == ("tf32", 3.0)
 
 
 def test_reference_arm_under_torchrun_prints_one_line():
