@@ -658,6 +658,12 @@ def main():
     tc = tc_peaks()
     rbk = {f"{k[0]}[{k[1]}]" if k[1] >= 0 else k[0]: kernel_roofline(args, k, *per_class[k], ms_step, tc)
            for k in per_class}
+    # concurrent streams overlap the brackets (each includes the contention
+    # of the kernels beside it), so shares of the STEP sum above 1; the share
+    # of the summed kernel time is what ncu's serialised launch list compares to
+    tot = sum(v[0] for v in per_class.values()) or 1.0
+    for k, v in per_class.items():
+        rbk[f"{k[0]}[{k[1]}]" if k[1] >= 0 else k[0]]["share_of_kernel_time"] = v[0] / tot
     roof = dict(rbk[f"{probe[0]}[{probe[1]}]" if probe[1] >= 0 else probe[0]])
     roof["probe_pass"] = probe_pass
     roof["selection"] = ("auto: the largest in-step share of the step time" if args.probe == "auto"

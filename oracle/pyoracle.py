@@ -213,14 +213,25 @@ def _chunks(B, threads):
     return [(a, b) for a, b in zip(edges[:-1], edges[1:]) if b > a]
 
 
+_POOL = None
+
+
+def _pool():
+    """One persistent host thread pool for the *_mt helpers (ctypes releases
+    the GIL, so the chunks run in parallel)."""
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(os.cpu_count() or 1)
+    return _POOL
+
+
 def forward_mt(spec, theta, states, threads=None):
-    """forward over row chunks on `threads` host threads (ctypes releases
-    the GIL); rows are independent, so the result equals forward()."""
-    from concurrent.futures import ThreadPoolExecutor
+    """forward over row chunks on `threads` host threads; rows are
+    independent, so the result equals forward()."""
     states = np.ascontiguousarray(states, np.float64).reshape(-1, input_dim(spec))
     parts = _chunks(states.shape[0], threads or os.cpu_count() or 1)
-    with ThreadPoolExecutor(len(parts)) as ex:
-        res = list(ex.map(lambda ab: forward(spec, theta, states[ab[0]:ab[1]]), parts))
+    res = list(_pool().map(lambda ab: forward(spec, theta, states[ab[0]:ab[1]]), parts))
     return np.concatenate([r[0] for r in res]), np.concatenate([r[1] for r in res])
 
 
@@ -228,15 +239,13 @@ def loss_and_gradients_mt(spec, hyper, theta, states, actions, returns, threads=
     """loss_and_gradients as a sum of per-chunk sums on host threads (the
     batch sum is associative up to fp64 rounding, far below the fp32 parity
     tolerances this is checked against).  No clip (grad_clip_norm must be 0)."""
-    from concurrent.futures import ThreadPoolExecutor
     assert hyper.grad_clip_norm == 0.0
     states = np.ascontiguousarray(states, np.float64).reshape(-1, input_dim(spec))
     actions = np.ascontiguousarray(actions, np.int32)
     returns = np.ascontiguousarray(returns, np.float64)
     parts = _chunks(states.shape[0], threads or os.cpu_count() or 1)
-    with ThreadPoolExecutor(len(parts)) as ex:
-        res = list(ex.map(lambda ab: loss_and_gradients(spec, hyper, theta, states[ab[0]:ab[1]],
-                                                        actions[ab[0]:ab[1]], returns[ab[0]:ab[1]]), parts))
+    res = list(_pool().map(lambda ab: loss_and_gradients(spec, hyper, theta, states[ab[0]:ab[1]],
+                                                         actions[ab[0]:ab[1]], returns[ab[0]:ab[1]]), parts))
     return sum(r[0] for r in res), sum(r[1] for r in res)
 
 
