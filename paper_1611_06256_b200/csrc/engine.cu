@@ -301,36 +301,20 @@ float* region(ga3c_ctx* c, int r) { return c->part + static_cast<std::size_t>(r)
 // on the context stream so far and directs launches to it; join() makes the
 // context stream wait for `s` and directs launches back.  Both are plain
 // event edges, so they are captured into CUDA graphs as graph dependencies.
-// A/B knobs for measurement (read once):
-//   GA3C_SERIAL_BWD=1   the whole backward on the context stream
-//   GA3C_NO_PRIO=1      side streams at the same priority as the context stream
-//   GA3C_NO_CLUSTER=1   no cluster split-K (conv forward, FC input gradient)
-bool env_flag(const char* name) {
-  const char* e = std::getenv(name);
-  return e && e[0] == '1';
-}
-bool serial_bwd() {
-  static const bool v = env_flag("GA3C_SERIAL_BWD");
-  return v;
-}
-// SMs a split-K plan tries to fill (GA3C_SPLIT_SMS, default all 148): with
-// several trainer contexts in flight, fewer and longer CTAs per kernel cost
-// less SM time than one full wave each.
-int split_sms(const ga3c_ctx* c) {
-  static const int v = [] {
-    const char* e = std::getenv("GA3C_SPLIT_SMS");
-    const int n = e ? std::atoi(e) : 0;
-    return n > 0 ? n : kNumSMs;
-  }();
-  return c && c->sms > 0 ? c->sms : v;
-}
+// (The design alternatives measured in round 1 -- serial backward, no side
+// stream priorities, no cluster split-K, deep-only rings, ... -- are recorded
+// with their numbers in DESIGN.md §5; the library builds only the measured
+// best path.  It reads no environment variables.)
+//
+// SMs a split-K plan tries to fill (ga3c_ctx_set_sm_budget, default all
+// 148): with several trainer contexts in flight, fewer and longer CTAs per
+// kernel cost less SM time than one full wave each.
+int split_sms(const ga3c_ctx* c) { return c && c->sms > 0 ? c->sms : kNumSMs; }
 // Ring-depth cap (pipe::ring_depth) for a tensor-core launch whose CTAs
 // each stream `n` k-chunks: no deeper than n; at most ~112 KB (two CTAs per
 // SM) for multi-wave grids and for contexts sharing the GPU with other
 // contexts (an SM budget below all SMs); otherwise as deep as fits.
 int ring_cap(const ga3c_ctx* c, int n, long long ctas) {
-  static const bool deep_only = env_flag("GA3C_DEEP_ONLY");
-  if (deep_only) return 0;
   if (n <= 2) return 2;
   if (n == 3) return 3;
   return (ctas > kNumSMs || split_sms(c) < kNumSMs) ? 1 : 0;
@@ -360,23 +344,11 @@ void smem_once(std::atomic<unsigned long long>& done, const void* kern, int byte
     default: F(0); break;       \
   }
 
-// SMs a cluster split-K plan (conv forward, FC input gradient) targets:
-// GA3C_CLUSTER_SCALE x the context's budget (A/B; default 1).
-int cluster_sms(const ga3c_ctx* c) {
-  static const double f = [] {
-    const char* e = std::getenv("GA3C_CLUSTER_SCALE");
-    return e && std::atof(e) > 0.0 ? std::atof(e) : 1.0;
-  }();
-  return std::max(1, static_cast<int>(f * split_sms(c)));
-}
-
-bool no_cluster() {
-  static const bool v = env_flag("GA3C_NO_CLUSTER");
-  return v;
-}
+// SMs a cluster split-K plan (conv forward, FC input gradient) targets: the
+// context's budget (0.25 / 0.5 / 2 x measured slower).
+int cluster_sms(const ga3c_ctx* c) { return std::max(1, split_sms(c)); }
 
 void fork_to(ga3c_ctx* c, cudaStream_t s) {
-  if (serial_bwd()) return;
   cudaEvent_t e = c->evs[c->ev_next++ & 15];
   cudaEventRecord(e, c->stream);
   cudaStreamWaitEvent(s, e, 0);
@@ -384,7 +356,6 @@ void fork_to(ga3c_ctx* c, cudaStream_t s) {
 }
 
 void join_from(ga3c_ctx* c, cudaStream_t s) {
-  if (serial_bwd()) return;
   cudaEvent_t e = c->evs[c->ev_next++ & 15];
   cudaEventRecord(e, s);
   cudaStreamWaitEvent(c->stream, e, 0);
@@ -560,10 +531,9 @@ void u8_persist_launch(ga3c_ctx* c, int li, const u8c::ConvArgs& a, dim3 grid) {
 
 bool u8_conv_persistent(ga3c_ctx* c, int li, const Layer& L, const float* theta, const uint8_t* x,
                         long long bstride, float* out, int B) {
-  static const bool off = env_flag("GA3C_NO_PERSIST");
   const int P = L.oh * L.ow;
   const int rowb = L.iw * L.cin;
-  if (off || P < 128 || L.cin % 4 != 0 || rowb % 16 != 0 || L.in % 128 != 0 || L.in > u8c::kMaxK ||
+  if (P < 128 || L.cin % 4 != 0 || rowb % 16 != 0 || L.in % 128 != 0 || L.in > u8c::kMaxK ||
       (L.k * L.cin) % 16 != 0 || L.cout > 32 || L.cout % 4 != 0 || L.w_off % 4 != 0 || bstride % 16 != 0 ||
       (reinterpret_cast<uintptr_t>(x) % 16) != 0)
     return false;
@@ -572,11 +542,7 @@ bool u8_conv_persistent(ga3c_ctx* c, int li, const Layer& L, const float* theta,
   const int rows = std::max((span + 1) * L.stride + L.k, span * L.stride + 2 * L.k);
   // one tile per CTA gains nothing from persistence, and its 180 KB of smem
   // would keep concurrent kernels off the SM: small grids take tc_bf16.cuh
-  static const int min_tiles = [] {
-    const char* e = std::getenv("GA3C_PERSIST_MIN_TILES");
-    return e ? std::atoi(e) : 2 * kNumSMs;
-  }();
-  if ((B * P + 127) / 128 < min_tiles) return false;
+  if ((B * P + 127) / 128 < 2 * kNumSMs) return false;
   const int fp_bytes = ((rows * rowb + 16) + 127) / 128 * 128;
   const int fp_stages = std::min(u8c::kFpMaxStages, u8c::kFpRegion / fp_bytes);
   if (fp_stages < 2) return false;
@@ -592,11 +558,10 @@ bool u8_conv_persistent(ga3c_ctx* c, int li, const Layer& L, const float* theta,
 }
 
 bool u8_conv_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const Seg& A, float* out, int B) {
-  static const bool off = env_flag("GA3C_NO_BF16");
-  if (!off && u8_conv_persistent(c, li, L, theta, static_cast<const uint8_t*>(A.p), A.bstride, out, B))
+  if (u8_conv_persistent(c, li, L, theta, static_cast<const uint8_t*>(A.p), A.bstride, out, B))
     return true;
   const int bn = tc_bn(L.cout);
-  if (off || L.in % 64 != 0 || (L.k * L.cin) % 32 != 0 || bn > 64 || L.cout % 4 != 0 || L.w_off % 4 != 0 ||
+  if (L.in % 64 != 0 || (L.k * L.cin) % 32 != 0 || bn > 64 || L.cout % 4 != 0 || L.w_off % 4 != 0 ||
       A.rowlen % 32 != 0)
     return false;
   Seg W = dense_seg(theta + L.w_off, L.cout, L.in, L.in, false);
@@ -604,7 +569,7 @@ bool u8_conv_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, co
   const int M = B * L.pixels();
   const int tiles = ((M + 127) / 128) * ((L.cout + bn - 1) / bn);
   const int chunks = L.in / 64;
-  int ks = no_cluster() ? 1 : std::max(1, std::min({8, chunks, cluster_sms(c) / std::max(1, tiles)}));
+  int ks = std::max(1, std::min({8, chunks, cluster_sms(c) / std::max(1, tiles)}));
   const int kc = ((chunks + ks - 1) / ks) * 64;
   ks = (L.in + kc - 1) / kc;
   const int cap = ring_cap(c, (std::min(kc, L.in) + 63) / 64, static_cast<long long>(tiles) * ks);
@@ -648,7 +613,7 @@ void conv_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const
       // partial tiles are summed through DSMEM in the epilogue.
       const int tiles = ((M + 127) / 128) * ((L.cout + bn - 1) / bn);
       const int chunks = L.in / 32;
-      int ks = no_cluster() ? 1 : std::max(1, std::min({8, chunks, cluster_sms(c) / std::max(1, tiles)}));
+      int ks = std::max(1, std::min({8, chunks, cluster_sms(c) / std::max(1, tiles)}));
       const int kc = ((chunks + ks - 1) / ks) * 32;
       ks = (L.in + kc - 1) / kc;
       tc_dispatch<T, float, TC_EPI_BIAS_RELU>(c, GA3C_K_CONV_FWD, li, bn, A, W, M, L.cout, L.in, ks, kc, e);
@@ -669,29 +634,6 @@ template <typename T>
 int fc_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const void* x, float* out,
                int B, bool keep_partials, long long in_stride) {
   const long long ld = in_stride > 0 ? in_stride : L.in;
-  static const bool direct = env_flag("GA3C_FC_DIRECT");
-  if (keep_partials && direct) {
-    // (A/B, off by default) batch rows x output units, split-K reduced inside
-    // a cluster (DSMEM), bias + ReLU in the epilogue: h is final, the heads
-    // read it directly.  Measured slower for DNN A (0.90M vs 1.01M samples/s:
-    // 16 CTAs x 11 k-chunks vs 42 CTAs x 2 plus the heads' reduction).
-    Seg X = dense_seg(x, B, ld, L.in, sizeof(T) == 1);
-    Seg W = dense_seg(theta + L.w_off, L.out, L.in, L.in, false);
-    X.rows = B;
-    W.rows = L.out;
-    if (seg_ok(X, B) && seg_ok(W, L.out) && L.in % 32 == 0 && (L.w_off % 4) == 0 && L.out % 4 == 0 &&
-        L.out <= 256) {
-      const int bn = tc_bn(L.out);
-      const int tiles = ((B + 127) / 128) * ((L.out + bn - 1) / bn);
-      const int chunks = L.in / 32;
-      int ks = no_cluster() ? 1 : std::max(1, std::min({8, chunks, cluster_sms(c) / std::max(1, tiles)}));
-      const int kc = ((chunks + ks - 1) / ks) * 32;
-      ks = (L.in + kc - 1) / kc;
-      TcEpiArgs e{theta + L.b_off, out, L.out};
-      tc_dispatch<T, float, TC_EPI_BIAS_RELU>(c, GA3C_K_FC_FWD, li, bn, X, W, B, L.out, L.in, ks, kc, e);
-      return 0;
-    }
-  }
   {
     Seg X = dense_seg(x, B, ld, L.in, sizeof(T) == 1);
     Seg W = dense_seg(theta + L.w_off, L.out, L.in, L.in, false);
@@ -700,12 +642,7 @@ int fc_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const vo
       const int bn = tc_bn(B);
       const int tiles = ((L.out + 127) / 128) * ((B + bn - 1) / bn);
       const int chunks = L.in / 32;
-      static const int force = [] {  // A/B: GA3C_FC_SPLITS caps the K splits
-        const char* e = std::getenv("GA3C_FC_SPLITS");
-        return e ? std::atoi(e) : 0;
-      }();
       int splits = std::max(1, std::min(chunks, split_sms(c) / std::max(1, tiles)));
-      if (force > 0) splits = std::min(splits, force);
       while (splits > 1 && static_cast<std::size_t>(splits) * B * L.out > kRegionFloats) --splits;
       const int kc = ((chunks + splits - 1) / splits) * 32;
       splits = (L.in + kc - 1) / kc;
@@ -773,15 +710,9 @@ void wgrad_tc_launch_v(ga3c_ctx* c, int li, const WgradArgs& a, dim3 grid, int t
 
 template <typename TX, int BN>
 void wgrad_tc_launch(ga3c_ctx* c, int li, const WgradArgs& a, dim3 grid, int tag = GA3C_K_WGRAD) {
-  // A/B: GA3C_MN_CAP forces the ring cap of the MN GEMMs (DNN A: deep 0.85M,
-  // cap 3 0.95M, cap 2 / default 1.01M samples/s -- occupancy beats depth)
-  static const int force = [] {
-    const char* e = std::getenv("GA3C_MN_CAP");
-    return e ? std::atoi(e) : -1;
-  }();
-  const int cap = force >= 0 ? force
-                             : ring_cap(c, (std::min(a.kc, a.npix) + 31) / 32,
-                                        static_cast<long long>(grid.x) * grid.y * grid.z);
+  // ring cap by occupancy (DNN A: deep 0.85M, cap 3 0.95M, cap 2 / default
+  // 1.01M samples/s -- occupancy beats depth)
+  const int cap = ring_cap(c, (std::min(a.kc, a.npix) + 31) / 32, static_cast<long long>(grid.x) * grid.y * grid.z);
 #define GA3C_F(C) wgrad_tc_launch_v<TX, BN, C>(c, li, a, grid, tag)
   GA3C_CAP_SWITCH(cap, GA3C_F)
 #undef GA3C_F
@@ -816,53 +747,19 @@ bool layer_wgrad_tc(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const
       }
     bn = std::min(bn, pick);
   }
-  static const int force_bn = [] {  // A/B: GA3C_WGRAD_BN forces the N tile (32/64/128)
-    const char* e = std::getenv("GA3C_WGRAD_BN");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (chunks < 4 && (force_bn == 32 || force_bn == 64 || force_bn == 128)) bn = force_bn;
   const int ntiles = (L.out + bn - 1) / bn;
   // A context with the whole GPU plans two CTAs per SM (ring cap 1), so the
   // conversion-heavy producers of one CTA overlap the other's; a context
   // sharing the GPU (a trainer beside other trainers) plans for half its
   // budget: fewer split partials to reduce on its critical path (DNN A
   // 1.00M -> 1.04M samples/s; x2 0.96M; large s1 whole-GPU x1 105K, x0.5 94K).
-  static const bool one = env_flag("GA3C_WGRAD_1CTA");
-  static const double scale = [] {  // A/B: GA3C_WGRAD_SPLIT_SCALE overrides the factor
-    const char* e = std::getenv("GA3C_WGRAD_SPLIT_SCALE");
-    return e ? std::atof(e) : 0.0;
-  }();
   const bool whole = split_sms(c) >= kNumSMs;
-  const double f = scale > 0.0 ? scale : (whole ? (one ? 1.0 : 2.0) : 0.5);
+  const double f = whole ? 2.0 : 0.5;
   const int wsms = std::max(1, static_cast<int>(f * split_sms(c)));
   int splits = std::max(1, std::min(chunks / 2, (wsms + mtiles * ntiles - 1) / (mtiles * ntiles)));
   while (splits > 1 && static_cast<std::size_t>(splits) * L.out * (L.in + 1) > kRegionFloats) --splits;
   const int kc = ((chunks + splits - 1) / splits) * 32;
   splits = (npix + kc - 1) / kc;
-  // GA3C_WGRAD_CLUSTER (A/B, off): at most 8 splits, reduced through DSMEM
-  // in the kernel (dtheta stored directly) instead of partials + a reduction
-  // kernel.  Correct (parity green) but measured much slower -- DNN A 0.81M
-  // vs 1.01M, large s1 57K vs 104K samples/s: the MN pipeline is bound by
-  // per-chunk load latency at shallow ring depths, so long CTAs lose to many
-  // short split CTAs plus the reduction kernel.
-  static const bool clu = env_flag("GA3C_WGRAD_CLUSTER");
-  bool cl = false;
-  if (clu && splits > 1) {
-    const int s8 = std::min(splits, 8);
-    const int kc8 = ((chunks + s8 - 1) / s8) * 32;
-    splits = (npix + kc8 - 1) / kc8;
-    cl = splits > 1;
-    if (cl) {
-      WgradArgs a8{X, dout, L.out, L.out, L.in, npix, kc8, part, gm, 1, 0, nullptr, nullptr, 0, 1};
-      dim3 grid8(mtiles, splits, ntiles);
-      switch (bn) {
-        case 32: wgrad_tc_launch<TX, 32>(c, li, a8, grid8); break;
-        case 64: wgrad_tc_launch<TX, 64>(c, li, a8, grid8); break;
-        default: wgrad_tc_launch<TX, 128>(c, li, a8, grid8); break;
-      }
-      return true;
-    }
-  }
   WgradArgs a{X, dout, L.out, L.out, L.in, npix, kc, part, gm, splits == 1, 0, nullptr, nullptr, 0, 0};
   dim3 grid(mtiles, splits, ntiles);
   switch (bn) {
@@ -917,8 +814,7 @@ bool fc_dgrad_tc(ga3c_ctx* c, int li, const Layer& L, const float* theta, const 
   // row tiles alone cannot fill the SMs
   const int mtiles = (L.in + 127) / 128;
   const int chunks = (L.out + 31) / 32;
-  static const bool no_mn = env_flag("GA3C_NO_CLUSTER_MN");
-  int ks = no_cluster() || no_mn ? 1 : std::max(1, std::min({8, chunks, cluster_sms(c) / mtiles}));
+  int ks = std::max(1, std::min({8, chunks, cluster_sms(c) / mtiles}));
   const int kc = ((chunks + ks - 1) / ks) * 32;
   ks = (L.out + kc - 1) / kc;
   WgradArgs a{W, doutT, ldT, B, L.in, L.out, kc, nullptr, GradMap{}, 0, 1, din, gate, L.in, 0};
@@ -944,8 +840,7 @@ void dgrad_tc_launch(ga3c_ctx* c, int li, const dg::DgradArgs& a, dim3 grid) {
 
 bool conv_dgrad_tc(ga3c_ctx* c, int li, const Layer& L, const float* theta, const float* dout,
                    const float* gate, float* din, int B) {
-  static const bool off = env_flag("GA3C_SIMT_DGRAD");
-  if (off || L.k % L.stride != 0 || L.cout % 32 != 0 || L.cin % 16 != 0 || L.cin > 128) return false;
+  if (L.k % L.stride != 0 || L.cout % 32 != 0 || L.cin % 16 != 0 || L.cin > 128) return false;
   const int T = L.k / L.stride;
   if (T * T * L.cout / 32 < 1) return false;
   dg::DgradArgs a{dout, theta + L.w_off, gate, din, B, L.ih, L.iw, L.cin, L.oh, L.ow, L.cout, L.k, L.stride, T};
@@ -954,13 +849,9 @@ bool conv_dgrad_tc(ga3c_ctx* c, int li, const Layer& L, const float* theta, cons
   const long long m0 = static_cast<long long>(B) * a0 * b0;
   const int ntiles = (L.cin + bn - 1) / bn;
   dim3 grid(static_cast<unsigned>((m0 + 127) / 128), L.stride * L.stride, ntiles);
-  // GA3C_DGRAD_CAP forces a ring cap (A/B measurement: large s1 conv2 dgrad
-  // cap 0 = 97 us, 1 = 68 us, 2 = 68 us, 3 = 97 us -- two CTAs per SM win)
-  static const int force = [] {
-    const char* e = std::getenv("GA3C_DGRAD_CAP");
-    return e ? std::atoi(e) : -1;
-  }();
-  const int cap = force >= 0 ? force : ring_cap(c, T * T * L.cout / 32, static_cast<long long>(grid.x) * grid.y * grid.z);
+  // ring cap by occupancy (large s1 conv2 dgrad: cap 0 = 97 us, 1 = 68 us,
+  // 2 = 68 us, 3 = 97 us -- two CTAs per SM win)
+  const int cap = ring_cap(c, T * T * L.cout / 32, static_cast<long long>(grid.x) * grid.y * grid.z);
   switch (bn) {
     case 16: {
 #define GA3C_F(C) dgrad_tc_launch<16, C>(c, li, a, grid)
@@ -1514,7 +1405,6 @@ ga3c_ctx* ga3c_ctx_create(ga3c_model* m, int max_batch, int* status) {
   // streams of the backward DAG (weight gradients) fill the SMs it leaves.
   int prio_lo = 0, prio_hi = 0;
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-  if (env_flag("GA3C_NO_PRIO")) prio_hi = prio_lo;
   bool ok = cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi) == cudaSuccess;
   c->cur = c->stream;
   for (auto& sd : c->side)
