@@ -509,7 +509,10 @@ def main():
         if fused is not None:
             loop.dp_update = lambda lp, j, U: fused.apply(ctx, j, lp.ring[U % lp.R], lp.ring[(U + 1) % lp.R])
         else:
+            loop.nccl = dp.NcclComm(rank, world, local)  # the library's own NCCL entry (ga3c_allreduce_grads)
             loop.dp_update = dp.nccl_update
+    elif world > 1:
+        loop.nccl = dp.NcclComm(rank, world, local)
     step = loop.step
     time_kernel, kernel_time, launches_all = loop.time_kernel, loop.kernel_time, loop.launches
 

@@ -277,6 +277,24 @@ int ga3c_ipc_close(void* dev_ptr);
 /* On-device update counter of ga3c_apply_rmsprop_dev (blocking read). */
 int ga3c_ctx_read_dev_version(ga3c_ctx* c, uint64_t* version);
 
+/* ------------------------------------ data parallel through NCCL (§8e) */
+/* in-place ncclAllReduce(sum) of
+ * grad_from's gradient (NULL = c) over `nccl_comm` (an ncclComm_t) on c's
+ * stream, then the non-finite flag recomputed on the sum (ga3c_check_grad),
+ * so every replica applies or rejects the same step and stays bit-identical.
+ * Follow with ga3c_clip_grad (if clipping) and the apply.  NCCL is loaded at
+ * run time (libnccl.so.2; the copy already in the process if any):
+ * GA3C_NCCL_ERROR when it is unavailable.  Capturable. */
+int ga3c_allreduce_grads(ga3c_ctx* c, ga3c_ctx* grad_from, void* nccl_comm);
+/* Communicator plumbing for callers without their own NCCL binding: rank 0
+ * draws the 128-byte id, the caller broadcasts it, every rank inits. */
+int ga3c_nccl_unique_id(void* id128);
+int ga3c_nccl_comm_init(int world, const void* id128, int rank, int device, void** comm);
+int ga3c_nccl_comm_destroy(void* comm);
+int ga3c_nccl_version(int* version);
+/* The model a context belongs to. */
+ga3c_model* ga3c_ctx_model(ga3c_ctx* c);
+
 /* ------------------------------------------------------------ returns */
 /* returns::compute_returns returns.hpp:31 / returns.cpp:8-26, batched over
  * n_seg segments: segment s covers rewards[seg_offsets[s] .. seg_offsets[s+1]).

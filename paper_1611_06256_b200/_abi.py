@@ -138,6 +138,12 @@ _SIGS = {
     "ga3c_ctx_read_grad": (C.c_int, [_P, _P, _P]),
     "ga3c_clip_grad": (C.c_int, [_P]),
     "ga3c_check_grad": (C.c_int, [_P, _P]),
+    "ga3c_allreduce_grads": (C.c_int, [_P, _P, _P]),
+    "ga3c_nccl_unique_id": (C.c_int, [_P]),
+    "ga3c_nccl_comm_init": (C.c_int, [C.c_int, _P, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "ga3c_nccl_comm_destroy": (C.c_int, [_P]),
+    "ga3c_nccl_version": (C.c_int, [C.POINTER(C.c_int)]),
+    "ga3c_ctx_model": (_P, [_P]),
     "ga3c_model_read_slot": (C.c_int, [_P, C.c_int, _P, _P]),
     "ga3c_rmsprop_flat": (C.c_int, [C.POINTER(HyperC), C.c_int, C.c_size_t, _P, _P, _P, C.POINTER(C.c_int)]),
     "ga3c_apply_rmsprop": (C.c_int, [_P, _P, C.POINTER(C.c_int), C.POINTER(C.c_uint64)]),

@@ -1670,6 +1670,8 @@ int ga3c_loss_grad_f32(ga3c_ctx* c, int slot, const float* states, const int32_t
 
 float* ga3c_ctx_grad(ga3c_ctx* c) { return c ? c->grad : nullptr; }
 
+ga3c_model* ga3c_ctx_model(ga3c_ctx* c) { return c ? c->m : nullptr; }
+
 const double* ga3c_ctx_last_values(ga3c_ctx* c) { return c ? c->v64 : nullptr; }
 
 int ga3c_ctx_read_grad(ga3c_ctx* c, float* dtheta, double* scalars) {

@@ -55,11 +55,15 @@ def allreduce_sum_(t, stream=None):
     return t
 
 
-def dp_update(ctx, d_states, u8, d_actions, d_returns, B_local, slot, gview, stream, world):
+def dp_update(ctx, d_states, u8, d_actions, d_returns, B_local, slot, gview, stream, world, comm=None):
     """One data-parallel update on this rank's shard: local summed gradient,
-    all-reduce(sum), clip on the reduced gradient, identical RMSProp."""
+    all-reduce(sum) (the library's NCCL entry when `comm` is a NcclComm, else
+    torch.distributed), clip on the reduced gradient, identical RMSProp."""
     ctx.loss_grad_dev(d_states, u8, d_actions, d_returns, B_local, slot, apply_clip=world == 1)
-    if world > 1:
+    if world > 1 and comm is not None:
+        comm.allreduce(ctx)
+        ctx.clip_grad()
+    elif world > 1:
         allreduce_sum_(gview, stream)
         # the reject decision must see the SUMMED gradient on every rank
         # (nnet.cpp:299-301): a rank whose own shard was finite would
@@ -69,14 +73,47 @@ def dp_update(ctx, d_states, u8, d_actions, d_returns, B_local, slot, gview, str
     ctx.apply_rmsprop_dev()
 
 
+class NcclComm:
+    """An NCCL communicator of the library's own entry points
+    (ga3c_nccl_comm_init / ga3c_allreduce_grads): rank 0
+    draws the id and the torch process group broadcasts it."""
+
+    def __init__(self, rank, world, device):
+        import ctypes as C
+
+        from . import _abi
+        self._abi = _abi
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            _abi.check(_abi.lib.ga3c_nccl_unique_id(uid), "ga3c_nccl_unique_id")
+        if world > 1:
+            import torch.distributed as dist
+            box = [bytes(uid)]
+            dist.broadcast_object_list(box, src=0)
+            C.memmove(uid, box[0], 128)
+        comm = C.c_void_p(0)
+        _abi.check(_abi.lib.ga3c_nccl_comm_init(world, uid, rank, device, C.byref(comm)), "ga3c_nccl_comm_init")
+        self.comm = comm
+
+    def allreduce(self, ctx, grad_from=None):
+        """Sum grad_from's gradient (default ctx's) over the ranks on ctx's
+        stream and recompute its non-finite flag on the sum."""
+        self._abi.check(self._abi.lib.ga3c_allreduce_grads(ctx.h, grad_from.h if grad_from is not None else None,
+                                                           self.comm), "ga3c_allreduce_grads")
+
+    def close(self):
+        if self.comm:
+            self._abi.lib.ga3c_nccl_comm_destroy(self.comm)
+            self.comm = None
+
+
 def nccl_update(lp, j, U):
     """DeviceLoop data-parallel exchange over NCCL for update U (trainer
-    context j): all-reduce(sum) of the gradient on the loop's main stream,
-    the non-finite flag recomputed on the SUMMED gradient (so every replica
+    context j): ga3c_allreduce_grads sums the gradient on the loop's main
+    stream and recomputes the non-finite flag on the SUM (so every replica
     rejects or applies the same step, nnet.cpp:299-301), then the identical
-    RMSProp step on every replica.  All on one stream: capturable."""
-    allreduce_sum_(lp.tgrad[j], lp.stream)
-    lp.ctx.check_grad(lp.tctx[j])
+    RMSProp step runs on every replica.  All on one stream: capturable."""
+    lp.nccl.allreduce(lp.ctx, lp.tctx[j])
     lp.ctx.apply_slots_dev(lp.tctx[j], lp.ring[U % lp.R], lp.ring[(U + 1) % lp.R])
 
 

@@ -91,6 +91,7 @@ class DeviceLoop:
         self.overlap = NT > 1 and overlap
         self.grad_view = dp.grad_view(ctx, self.P, device) if world > 1 else None
         self.dp_update = dp_update  # data-parallel exchange for NT > 1 (fused kernel or NCCL), or None
+        self.nccl = None  # dp.NcclComm for the NCCL exchange (dp.nccl_update, and NT == 1)
         if NT > 1:
             self.R = ring_size(NT, self.updates)
             self.ring = model.ring(self.R + 1)  # + the predictor's slot, never written by a trainer
@@ -101,7 +102,6 @@ class DeviceLoop:
             n_ev = self.updates * GMAX
             self.ev_g = [torch.cuda.Event() for _ in range(n_ev)]
             self.ev_a = [torch.cuda.Event() for _ in range(n_ev)]
-            self.ev_c = [torch.cuda.Event() for _ in range(n_ev)]
             self.ev_r = torch.cuda.Event()
             self.ev_p = [torch.cuda.Event() for _ in range(GMAX)]
             self.ev_end = [torch.cuda.Event() for _ in range(GMAX)]
@@ -141,7 +141,7 @@ class DeviceLoop:
             for u in range(self.updates):
                 self.dp.dp_update(self.ctx, fr + u * TB * FRAME_BYTES, True, self.actions2[0].data_ptr() + 4 * u * TB,
                                   self.rets2[0].data_ptr() + 8 * u * TB, TB, self.slot, self.grad_view, self.stream,
-                                  self.world)
+                                  self.world, self.nccl)
             return
         base = pos * self.updates
         stream, tstream = self.stream, self.tstream
