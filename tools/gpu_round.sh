@@ -12,5 +12,5 @@ timeout 900 python bench.py --net large1 --steps 60 > gpurun_out/${TAG}_bench_la
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${TAG}_bench_reference.json 2> gpurun_out/${TAG}_bench_reference.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches_dnn_a.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches_large1.csv python bench.py --net large1 --steps 2 --warmup 1 --no-cpu --no-e2e > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"u8conv|tc_u8_fwd|rmsprop" -s 6 -c 6 -o gpurun_out/${TAG}_full_dnn_a python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e --trainers 1 --no-graph > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"u8conv|tc_u8_fwd|rmsprop|tc_mn_ws|heads|splitk" -s 10 -c 14 -o gpurun_out/${TAG}_full_dnn_a python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e --trainers 1 --no-graph > /dev/null 2>&1
 ls -la gpurun_out | tail -20

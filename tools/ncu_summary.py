@@ -39,10 +39,11 @@ def launches(path, out):
 def full(rep, out):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(raw.splitlines()))
-    hdr, rows = r[0], r[2:]
+    hdr, units, rows = r[0], r[1], r[2:]
     with open(out, "w", newline="") as f:
         w = csv.writer(f)
         w.writerow(["kernel"] + FULL_METRICS)
+        w.writerow(["(unit)"] + [units[hdr.index(m)] if m in hdr else "" for m in FULL_METRICS])
         for row in rows:
             w.writerow([row[hdr.index("Kernel Name")][:80]] +
                        [row[hdr.index(m)] if m in hdr else "" for m in FULL_METRICS])
