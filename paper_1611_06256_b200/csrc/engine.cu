@@ -143,7 +143,7 @@ struct ga3c_ctx {
   int32_t* d_actions = nullptr;
   double* d_rets = nullptr;
   float* grad = nullptr;
-  int* flag = nullptr;
+  int* flag = nullptr;  // control words: [0] non-finite flag, [1] heads-kernel ticket
   unsigned long long* dev_version = nullptr;
   float* part = nullptr;
   double* clip_part = nullptr;
@@ -1022,20 +1022,37 @@ int run_loss_grad(ga3c_ctx* c, const float* theta, const void* d_in, bool u8, co
   // so they run on side streams as soon as it exists.  Every branch writes
   // disjoint dtheta ranges and its own split-K region, so the result is the
   // same bit for bit as the serial order.
+  const bool heads_contig = lo.policy.b_off == lo.policy.w_off + static_cast<std::size_t>(A) * D &&
+                            lo.value.w_off == lo.policy.b_off + A && lo.value.b_off == lo.value.w_off + D;
+  bool used[2] = {true, false};
   fork_to(c, c->side[0]);
-  {
+  if (heads_contig && A + 1 <= 32) {
+    // heads weight gradient [A+1][D+1] = dhead^T [h | 1], sample order
+    GradFinal f{};
+    f.heads = 1;
+    f.dhead = c->dhead;
+    f.h = h;
+    f.B = B;
+    f.A = A;
+    f.D = D;
+    f.wp_off = lo.policy.w_off;
+    f.bp_off = lo.policy.b_off;
+    f.wv_off = lo.value.w_off;
+    f.bv_off = lo.value.b_off;
+    f.scal = c->scal;
+    f.scal_sum = c->scal_sum;
+    Launch l(c, GA3C_K_WGRAD, -1);
+    pdl_launch(c->cur, final_grad_kernel, dim3((D + 1 + 31) / 32), dim3(256), 0, f, c->grad, c->flag);
+  } else {
     // heads weight gradient: [A+1][D+1] = dhead^T [h | 1]
     GradMap gm{c->grad, c->flag, lo.policy.w_off, lo.policy.b_off, lo.value.w_off, lo.value.b_off, A, D};
     DenseT a{c->dhead, A + 1};
     WithOnes<DenseT> b{DenseT{h, D}, D};
     wgrad_gemm(c, -1, a, b, gm, A + 1, D + 1, B, region(c, kRegions - 1));
-  }
-  {
     Launch l(c, GA3C_K_OTHER, -1);
     pdl_launch(c->cur, scalars_kernel, dim3(1), dim3(32), 0, c->scal, B, c->scal_sum);
   }
   c->cur = c->stream;
-  bool used[2] = {true, false};
   for (int li = lo.n_trunk - 1; li >= 0; --li) {
     const Layer& L = lo.trunk[li];
     const void* x_in = li == 0 ? d_in : c->act[li - 1];

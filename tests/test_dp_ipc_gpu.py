@@ -7,6 +7,7 @@ restatement.  (Kernels of different processes are time-sliced on one GPU,
 so the cross-rank barriers complete through preemption rather than true
 concurrency; on a multi-GPU box they run concurrently over NVLink.)"""
 import json
+import re
 import os
 import subprocess
 import sys
@@ -22,7 +23,8 @@ def test_two_process_ipc_fused_update():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29571", os.path.join(ROOT, "tests", "dp_ipc_worker.py")]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=300)
-    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    # the two ranks share one stdout pipe: their lines may interleave
+    lines = [json.loads(x) for x in re.findall(r"\{[^{}]*\}", r.stdout)]
     print(lines)
     assert r.returncode == 0, r.stderr[-3000:]
     assert len(lines) == 2

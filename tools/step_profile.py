@@ -65,6 +65,19 @@ def main(net="dnn_a", tb=40, na=128):
     ctx.loss_grad_dev(fr.data_ptr(), True, acts.data_ptr(), rets.data_ptr(), tb, slot)
     print("kernels per loss_grad:", ctx.launches() - n0)
     ctx.sync()
+    # per-launch timeline of one eager update queued behind a spin (serial
+    # latency view: every launch's start/end relative to the first)
+    for rep in range(2):
+        ctx.time_kernel("all")
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(int(4e6))
+        ctx.loss_grad_dev(fr.data_ptr(), True, acts.data_ptr(), rets.data_ptr(), tb, slot)
+        ctx.apply_rmsprop_dev()
+        tl = ctx.timeline()
+        ctx.time_kernel("none")
+    print("# one eager update (B=%d): start_ms end_ms dur_us stream kernel[layer]" % tb)
+    for tag, li, sid, a, b in tl:
+        print(f"{a:9.4f} {b:9.4f} {1e3 * (b - a):8.2f}  s{sid}  {tag}[{li}]")
 
 
 if __name__ == "__main__":
