@@ -1027,22 +1027,11 @@ int run_loss_grad(ga3c_ctx* c, const float* theta, const void* d_in, bool u8, co
   bool used[2] = {true, false};
   fork_to(c, c->side[0]);
   if (heads_contig && A + 1 <= 32) {
-    // heads weight gradient [A+1][D+1] = dhead^T [h | 1], sample order
-    GradFinal f{};
-    f.heads = 1;
-    f.dhead = c->dhead;
-    f.h = h;
-    f.B = B;
-    f.A = A;
-    f.D = D;
-    f.wp_off = lo.policy.w_off;
-    f.bp_off = lo.policy.b_off;
-    f.wv_off = lo.value.w_off;
-    f.bv_off = lo.value.b_off;
-    f.scal = c->scal;
-    f.scal_sum = c->scal_sum;
+    // heads weight gradient [A+1][D+1] = dhead^T [h | 1] + the loss sums
+    const HeadsGrad hg{c->dhead, h, B, A, D, lo.policy.w_off, lo.policy.b_off, lo.value.w_off, lo.value.b_off,
+                       c->scal, c->scal_sum};
     Launch l(c, GA3C_K_WGRAD, -1);
-    pdl_launch(c->cur, final_grad_kernel, dim3((D + 1 + 31) / 32), dim3(256), 0, f, c->grad, c->flag);
+    pdl_launch(c->cur, heads_wgrad_kernel, dim3((D + 1 + 31) / 32), dim3(256), 0, hg, c->grad, c->flag);
   } else {
     // heads weight gradient: [A+1][D+1] = dhead^T [h | 1]
     GradMap gm{c->grad, c->flag, lo.policy.w_off, lo.policy.b_off, lo.value.w_off, lo.value.b_off, A, D};

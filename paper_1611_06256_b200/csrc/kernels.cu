@@ -722,127 +722,76 @@ rmsprop_kernel(const float* __restrict__ th_in, const float* __restrict__ g_in,
   if (version && t0 == 0) *version += 1ull;
 }
 
-// ---------------------------------------------- gradient finishing pass
-// Sum of the split partials of one element in splitk_wgrad{,8}_kernel's
-// exact order (sequential for <= 16 splits; else 8 chains k = q mod 8 added
-// in q order), with every load of a round issued before the adds.
-__device__ __forceinline__ float split_sum(const float* __restrict__ p, std::size_t base, std::size_t stride,
-                                          int n) {
-  p += base;
-  if (n <= 16) {
-    float t[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) t[k] = k < n ? __ldcg(p + k * stride) : 0.f;
-    float s = 0.f;
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (k < n) s += t[k];
-    return s;
-  }
-  float c[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int k0 = 0; k0 < n; k0 += 32) {
-    float t[32];
-#pragma unroll
-    for (int u = 0; u < 32; ++u) t[u] = k0 + u < n ? __ldcg(p + (k0 + u) * stride) : 0.f;
-#pragma unroll
-    for (int u = 0; u < 32; ++u)
-      if (k0 + u < n) c[u & 7] += t[u];
-  }
-  float t = c[0];
-#pragma unroll
-  for (int q = 1; q < 8; ++q) t += c[q];
-  return t;
-}
-
-__global__ void __launch_bounds__(256) final_grad_kernel(GradFinal gf, float* __restrict__ grad, int* __restrict__ ctl) {
+// ------------------------------------------------- heads weight gradient
+__global__ void __launch_bounds__(256) heads_wgrad_kernel(HeadsGrad hg, float* __restrict__ grad,
+                                                          int* __restrict__ flag) {
   __shared__ float hs[64][33];  // h[b][c0 + col] for a chunk of 64 samples
-  __shared__ float gs[64][9];   // dhead[b][j], j <= A (A + 1 <= 9 staged; larger A read directly)
+  __shared__ float gs[64][9];   // dhead[b][j] when A + 1 <= 9 (else read directly)
   pdl_enter();
   const int tid = threadIdx.x;
   bool bad = false;
-  if (static_cast<int>(blockIdx.x) < gf.split_blocks) {
-    unsigned long long e = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + tid;
-    if (e < gf.split_count) {
-#pragma unroll
-      for (int k = 0; k < kMaxFinalSegs; ++k) {
-        if (k >= gf.n) break;
-        const FinalSeg& s = gf.seg[k];
-        const unsigned long long nw = static_cast<unsigned long long>(s.cout) * s.Kw;
-        if (e < nw + s.cout) {
-          const float v = e < nw ? split_sum(s.part, e, nw, s.n_split)
-                                 : split_sum(s.part, static_cast<std::size_t>(s.n_split) * nw + (e - nw), s.cout,
-                                             s.n_split);
-          grad[s.w_off + e] = v;
-          bad = !isfinite(v);
-          break;
-        }
-        e -= nw + s.cout;
-      }
-    }
-  } else {
-    // heads: columns [c0, c0 + 32) of [h | 1] (column D = the bias), rows
-    // j = tid / 32 (+ 8, + 16, ...) <= A
-    const int c0 = (static_cast<int>(blockIdx.x) - gf.split_blocks) * 32;
-    if (c0 == 0 && gf.scal) {
-      // the loss diagnostics' batch sums (nnet.cpp:233-235) in sample order,
-      // staged 256 terms per round
-      __shared__ double sc[256];
-      double acc_s = 0.0;
-      const int n = 3 * gf.B;
-      for (int i0 = 0; i0 < n; i0 += 255) {  // 85 samples x 3 terms per round
-        const int m = min(255, n - i0);
-        __syncthreads();
-        if (tid < m) sc[tid] = __ldcg(gf.scal + i0 + tid);
-        __syncthreads();
-        if (tid < 3)
-          for (int i = tid; i < m; i += 3) acc_s += sc[i];
-      }
-      if (tid < 3) gf.scal_sum[tid] = acc_s;
-    }
-    const int col = c0 + (tid & 31);
-    const int A1 = gf.A + 1;
-    constexpr int kRows = 256 / 32;
-    const int nj = (A1 + kRows - 1) / kRows;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};  // A + 1 <= 32 (validated: n_actions <= 31 here, else direct loads)
-    for (int b0 = 0; b0 < gf.B; b0 += 64) {
-      const int nb = min(64, gf.B - b0);
+  // columns [c0, c0 + 32) of [h | 1] (column D = the bias), rows
+  // j = tid / 32 (+ 8, + 16, + 24) <= A
+  const int c0 = static_cast<int>(blockIdx.x) * 32;
+  if (c0 == 0 && hg.scal) {
+    // the loss diagnostics' batch sums in sample order (scalars_kernel's
+    // order), staged 255 terms (85 samples) per round
+    __shared__ double sc[256];
+    double acc_s = 0.0;
+    const int n = 3 * hg.B;
+    for (int i0 = 0; i0 < n; i0 += 255) {
+      const int m = min(255, n - i0);
       __syncthreads();
-      for (int i = tid; i < nb * 32; i += blockDim.x) {
-        const int bb = i >> 5, cc = c0 + (i & 31);
-        hs[bb][i & 31] = cc < gf.D ? __ldcg(gf.h + static_cast<std::size_t>(b0 + bb) * gf.D + cc) : 1.f;
-      }
-      if (A1 <= 9)
-        for (int i = tid; i < nb * A1; i += blockDim.x) {
-          const int bb = i / A1, jj = i - bb * A1;
-          gs[bb][jj] = __ldcg(gf.dhead + static_cast<std::size_t>(b0 + bb) * A1 + jj);
-        }
+      if (tid < m) sc[tid] = __ldcg(hg.scal + i0 + tid);
       __syncthreads();
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int j = tid / 32 + kRows * q;
-        if (q >= nj || j >= A1) break;
-        float s = acc[q];
-        for (int bb = 0; bb < nb; ++bb) {
-          const float g = A1 <= 9 ? gs[bb][j] : __ldcg(gf.dhead + static_cast<std::size_t>(b0 + bb) * A1 + j);
-          s = fmaf(g, hs[bb][tid & 31], s);
-        }
-        acc[q] = s;
-      }
+      if (tid < 3)
+        for (int i = tid; i < m; i += 3) acc_s += sc[i];
     }
-    if (col <= gf.D) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int j = tid / 32 + kRows * q;
-        if (q >= nj || j >= A1) break;
-        const unsigned long long i = j < gf.A ? (col < gf.D ? gf.wp_off + static_cast<unsigned long long>(j) * gf.D + col
-                                                            : gf.bp_off + j)
-                                              : (col < gf.D ? gf.wv_off + col : gf.bv_off);
-        grad[i] = acc[q];
-        bad |= !isfinite(acc[q]);
+    if (tid < 3) hg.scal_sum[tid] = acc_s;
+  }
+  const int col = c0 + (tid & 31);
+  const int A1 = hg.A + 1;
+  constexpr int kRows = 256 / 32;
+  const int nj = (A1 + kRows - 1) / kRows;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int b0 = 0; b0 < hg.B; b0 += 64) {
+    const int nb = min(64, hg.B - b0);
+    __syncthreads();
+    for (int i = tid; i < nb * 32; i += blockDim.x) {
+      const int bb = i >> 5, cc = c0 + (i & 31);
+      hs[bb][i & 31] = cc < hg.D ? __ldcg(hg.h + static_cast<std::size_t>(b0 + bb) * hg.D + cc) : 1.f;
+    }
+    if (A1 <= 9)
+      for (int i = tid; i < nb * A1; i += blockDim.x) {
+        const int bb = i / A1, jj = i - bb * A1;
+        gs[bb][jj] = __ldcg(hg.dhead + static_cast<std::size_t>(b0 + bb) * A1 + jj);
       }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = tid / 32 + kRows * q;
+      if (q >= nj || j >= A1) break;
+      float s = acc[q];
+      for (int bb = 0; bb < nb; ++bb) {
+        const float g = A1 <= 9 ? gs[bb][j] : __ldcg(hg.dhead + static_cast<std::size_t>(b0 + bb) * A1 + j);
+        s = fmaf(g, hs[bb][tid & 31], s);
+      }
+      acc[q] = s;
     }
   }
-  if (__syncthreads_or(bad) && tid == 0) atomicOr(ctl, 1);
+  if (col <= hg.D) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = tid / 32 + kRows * q;
+      if (q >= nj || j >= A1) break;
+      const unsigned long long i = j < hg.A ? (col < hg.D ? hg.wp_off + static_cast<unsigned long long>(j) * hg.D + col
+                                                          : hg.bp_off + j)
+                                            : (col < hg.D ? hg.wv_off + col : hg.bv_off);
+      grad[i] = acc[q];
+      bad |= !isfinite(acc[q]);
+    }
+  }
+  if (__syncthreads_or(bad) && tid == 0) atomicOr(flag, 1);
 }
 
 // --------------------------------------------------------------- returns

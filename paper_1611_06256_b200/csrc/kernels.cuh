@@ -23,41 +23,23 @@ __global__ void heads_loss_kernel(const float* part, int n_split, const float* f
                                   float* v_out, float* dhead, float* dh, float* dhT, int ldT, double* scal,
                                   int* flag);
 
-// --------------------------------------------- gradient finishing pass
-// The pieces of a gradient that need a batch-wide reduction after their
-// producer -- the split-K partials of the trunk weight gradients and the
-// heads' weight gradient -- are finished by ONE launch at the end of the
-// backward DAG (final_grad_kernel) instead of a reduction kernel per layer +
-// a heads GEMM:
-//   split: a trunk layer's W [cout][Kw] at w_off, its bias [cout] right after,
-//          from tc_mn_ws_kernel's split-K partials [split][cout][Kw] +
-//          [split][cout], summed in splitk_wgrad{,8}_kernel's exact order
-//          (the same bits);
-//   heads: [W_p | b_p | w_v | b_v] (nnet.hpp layout order) = dhead^T [h | 1]
-//          (nnet.cpp:237-262 summed over the batch), in sample order.
-// CTAs [0, split_blocks) take one split element per thread; the rest take
-// 32 heads columns each, staging h and dhead through shared memory.
-constexpr int kMaxFinalSegs = 8;
-struct FinalSeg {
-  unsigned long long w_off;
-  const float* part;
-  int n_split, cout, Kw;
-};
-struct GradFinal {
-  int n;  // split segments
-  FinalSeg seg[kMaxFinalSegs];
-  unsigned long long split_count;  // split elements (sum of cout * (Kw + 1))
-  int split_blocks;
-  int heads;
+// ------------------------------------------- heads weight gradient
+// [W_p | b_p | w_v | b_v] (nnet.hpp layout order) = dhead^T [h | 1]
+// (nnet.cpp:237-262 summed over the batch, sample order), plus the loss
+// diagnostics' batch sums (nnet.cpp:233-235), in one launch on the
+// backward DAG's side stream: CTA k takes columns [32k, 32k + 32) of [h | 1]
+// for every output row, staging h and dhead through shared memory.
+struct HeadsGrad {
   const float* dhead;  // [B][A+1]
   const float* h;      // [B][D]
-  int B, A, D;
+  int B, A, D;         // A + 1 <= 32
   unsigned long long wp_off, bp_off, wv_off, bv_off;
   const double* scal;  // per-sample loss diagnostics [B][3] (nullable)
   double* scal_sum;    // their batch sums
 };
 
-__global__ void final_grad_kernel(GradFinal gf, float* grad, int* ctl);
+__global__ void heads_wgrad_kernel(HeadsGrad hg, float* grad, int* flag);
+
 
 __global__ void loss_heads_bwd_kernel(const double* pi64, const float* v, const int32_t* actions,
                                       const double* rets, const float* h, int B, int D, int A,

@@ -1,12 +1,11 @@
-"""The gradient's finishing pass (final_grad_kernel): the split-K
-reductions of the trunk weight gradients and the heads' weight gradient
-(nnet.cpp:237-262, summed over the batch) are finished by ONE launch at the
-end of the backward DAG, and the loss diagnostics by the heads kernel's
-last CTA (nnet.cpp:233-235).  Checked here against the fp64 oracle at the
-shapes the bench runs, on a net where EVERY weight gradient is finished by
-that pass (no hidden layer), and for the reference's reject
-(nnet.cpp:299-301) when the non-finite values exist only in the pieces the
-pass produces.  Needs a B200 (-m gpu)."""
+"""The heads' weight gradient (nnet.cpp:237-262, summed over the batch) and
+the loss diagnostics' batch sums (nnet.cpp:233-235) come from one kernel
+on the backward DAG's side stream (heads_wgrad_kernel).  Checked against
+the fp64 oracle at the shapes the bench runs (B = 40 at the trainer SM
+budget, the predictor's 128), on a net with no hidden layer (the heads read
+the conv output, D = 2592), and for the reference's reject
+(nnet.cpp:299-301) of a non-finite gradient, through the device apply.
+Needs a B200 (-m gpu)."""
 import numpy as np
 import pytest
 
@@ -42,7 +41,7 @@ def test_dnn_a_gradient_and_scalars(B, budget):
     assert np.allclose(s1, rsc, rtol=1e-5, atol=1e-6 * B), (s1, rsc)
 
 
-def test_conv_only_net_all_pieces_finished_in_one_pass():
+def test_conv_only_net_wide_heads():
     spec = O.make_spec((84, 84, 4), [(16, 8, 4), (32, 4, 2)], [], 6)
     m, ctx, th, fr, acts, rets = case(spec, 40, 2)
     d, sc = ctx.loss_grad(fr, acts, rets)
@@ -60,12 +59,10 @@ def test_large1_batch8():
 
 
 @pytest.mark.parametrize("hidden", [[256], []])
-def test_reject_when_only_finished_pieces_are_nonfinite(hidden):
-    """With no hidden layer the non-finite values exist only in the pieces the
-    finishing pass writes, so its flag alone must reject the step (the
-    reference throws on the action, nnet.cpp:214-216, and rejects non-finite
-    gradients, nnet.cpp:299-301); the device apply then leaves theta, g and
-    the version unchanged."""
+def test_reject_nonfinite_through_device_apply(hidden):
+    """An out-of-range action (the reference throws, nnet.cpp:214-216) makes
+    every gradient piece non-finite; the device apply then rejects the step
+    (nnet.cpp:299-301) and leaves theta, g and the version unchanged."""
     import torch
     spec = O.make_spec((84, 84, 4), [(16, 8, 4), (32, 4, 2)], hidden, 6)
     m, ctx, th, fr, acts, rets = case(spec, 40, 9, bad_action=True)
