@@ -307,6 +307,11 @@ int ga3c_compute_returns_dev(ga3c_ctx* c, const double* d_rewards, const int32_t
                              int n_seg, const uint8_t* d_terminal, const double* d_bootstrap,
                              double gamma, double* d_out);
 
+/* Page-locked host memory (cudaMallocHost): copies between it and the
+ * device are asynchronous DMA (the engine's predictor stages frames here). */
+void* ga3c_host_alloc(size_t bytes, int* status);
+void ga3c_host_free(void* p);
+
 /* -------------------------------------------------------- frame store */
 /* Device-resident 4-frame stacks.  The reference's
  * PredictionRequest carries the whole stacked state (pipeline.hpp:23-27);
@@ -416,6 +421,10 @@ typedef struct ga3c_pipeline_opts {
   int max_agents, max_predictors, max_trainers;
   double metrics_interval_s;
   int greedy, sync_after_submit, capture_trajectory, device;
+  /* 1 = device frame store (frame envs): agents send their newest 84x84
+   * frame, stacks and the TrainingQueue's states stay on the GPU
+   * (ga3c_frames_*); 0 = whole states both ways, as the reference. */
+  int device_frames;
 } ga3c_pipeline_opts;
 
 typedef struct ga3c_run_report {

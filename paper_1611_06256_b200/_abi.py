@@ -70,6 +70,7 @@ class PipelineOpts(C.Structure):
         ("max_agents", C.c_int), ("max_predictors", C.c_int), ("max_trainers", C.c_int),
         ("metrics_interval_s", C.c_double),
         ("greedy", C.c_int), ("sync_after_submit", C.c_int), ("capture_trajectory", C.c_int), ("device", C.c_int),
+        ("device_frames", C.c_int),
     ]
 
 
@@ -167,6 +168,8 @@ _SIGS = {
     "ga3c_ctx_set_sm_budget": (C.c_int, [_P, C.c_int]),
     "ga3c_frames_create": (_P, [_P, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "ga3c_frames_destroy": (None, [_P]),
+    "ga3c_host_alloc": (_P, [C.c_size_t, C.POINTER(C.c_int)]),
+    "ga3c_host_free": (None, [_P]),
     "ga3c_predict_frames": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_int, _P, _P, _P,
                                       C.POINTER(C.c_uint64)]),
     "ga3c_predict_frames64": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_int, _P, _P, _P,

@@ -2476,6 +2476,20 @@ int ga3c_train_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const int32_t* agen
                             });
 }
 
+void* ga3c_host_alloc(size_t bytes, int* status) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, std::max<size_t>(bytes, 16)) != cudaSuccess) {
+    if (status) *status = GA3C_OUT_OF_MEMORY;
+    return nullptr;
+  }
+  if (status) *status = GA3C_OK;
+  return p;
+}
+
+void ga3c_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 ga3c_frames* ga3c_frames_create(ga3c_model* m, int n_agents, int history, int* status) {
   auto fail = [&](int st) -> ga3c_frames* {
     if (status) *status = st;

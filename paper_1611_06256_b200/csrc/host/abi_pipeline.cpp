@@ -46,6 +46,7 @@ PipelineOptions to_options(const ga3c_pipeline_opts* o) {
   p.sync_after_submit = o->sync_after_submit != 0;
   p.capture_trajectory = o->capture_trajectory != 0;
   p.device = o->device;
+  p.device_frames = o->device_frames != 0;
   return p;
 }
 

@@ -217,6 +217,7 @@ class FrameCatchEnv final : public Env {
   int action_count() const override { return s_.n_actions; }
   bool frames() const override { return true; }
   ga3c_net_spec input() const override { return frame_input(); }
+  void set_single_frame(bool on) override { single_ = on; }
 
  private:
   void push_frame() {  // channel t = frame t of the 4-step stack (NHWC)
@@ -232,12 +233,18 @@ class FrameCatchEnv final : public Env {
   }
   Observation observe() const {
     Observation o;
-    o.u8.assign(stack_, stack_ + kFrameBytes);
+    if (single_) {  // the newest channel
+      o.u8.resize(kFrameBytes / 4);
+      for (int p = 0; p < 84 * 84; ++p) o.u8[p] = stack_[p * 4 + 3];
+    } else {
+      o.u8.assign(stack_, stack_ + kFrameBytes);
+    }
     return o;
   }
   EnvSpec s_;
   int g_, cell_, row_ = 0, col_ = 0, pad_ = 0;
   bool done_ = true;
+  bool single_ = false;
   uint8_t stack_[kFrameBytes];
 };
 
@@ -264,13 +271,17 @@ class FramesEnv final : public Env {
   int action_count() const override { return s_.n_actions; }
   bool frames() const override { return true; }
   ga3c_net_spec input() const override { return frame_input(); }
+  void set_single_frame(bool on) override { single_ = on; }
 
  private:
+  // a fresh synthetic state per step (frames mode), or a fresh newest frame
+  // (single-frame mode, stacked on the device)
   Observation frame() {
     Observation o;
-    o.u8.resize(kFrameBytes);
+    const int bytes = single_ ? kFrameBytes / 4 : kFrameBytes;
+    o.u8.resize(bytes);
     std::uint64_t* w = reinterpret_cast<std::uint64_t*>(o.u8.data());
-    for (int i = 0; i < kFrameBytes / 8; ++i) {  // xorshift64*
+    for (int i = 0; i < bytes / 8; ++i) {  // xorshift64*
       state_ ^= state_ >> 12;
       state_ ^= state_ << 25;
       state_ ^= state_ >> 27;
@@ -282,6 +293,7 @@ class FramesEnv final : public Env {
   std::uint64_t state_ = 1;
   int steps_ = 0;
   bool done_ = true;
+  bool single_ = false;
 };
 
 class RepeatWrapper final : public Env {  // envs.cpp:140-164
@@ -302,6 +314,7 @@ class RepeatWrapper final : public Env {  // envs.cpp:140-164
   int action_count() const override { return in_->action_count(); }
   bool frames() const override { return in_->frames(); }
   ga3c_net_spec input() const override { return in_->input(); }
+  void set_single_frame(bool on) override { in_->set_single_frame(on); }
 
  private:
   std::unique_ptr<Env> in_;

@@ -22,6 +22,7 @@
 #include <mutex>
 #include <optional>
 #include <random>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -74,6 +75,13 @@ class Env {
   virtual int action_count() const = 0;
   virtual bool frames() const = 0;       // u8 84x84x4 observations
   virtual ga3c_net_spec input() const = 0;  // in_h/in_w/in_c of the observation
+  // Device frame store mode (frame envs only): observations carry only the
+  // NEWEST frame (in_h x in_w bytes); the 4-frame stack is built on the
+  // device (ga3c_predict_frames), where it equals the stack frames() mode
+  // returns (reset = the first frame four times).
+  virtual void set_single_frame(bool on) {
+    if (on) throw std::invalid_argument("env: no single-frame observations");
+  }
 };
 
 void validate(const EnvSpec& spec);
@@ -122,21 +130,24 @@ bool decide(AnnealState& s, const KnobConfig& candidate, double measured_tps);  
 struct PredictionRequest {
   int agent_id = 0;
   std::uint64_t ticket = 0;
-  Observation state;
+  Observation state;  // device frames: the newest frame only
+  bool reset = false;  // device frames: first frame of an episode
 };
 
 struct PredictionResponse {
   std::vector<double> policy;  // the device's fp64 softmax (ga3c_forward64_*)
   double value = 0.0;
   std::uint64_t model_version = 0;
+  int state_slot = -1;  // device frames: where the stacked state is kept
 };
 
 struct Experience {  // returns.hpp:13-19
-  Observation state;
+  Observation state;    // empty with device frames
   int action = 0;
   double reward = 0.0;
   double value_at_play = 0.0;
   std::uint64_t produced_version = 0;
+  int state_slot = -1;  // device frames: the state's slot in the agent's ring
 };
 
 struct ExperienceBatch {  // returns.hpp:21-26 (returns computed on the trainer's device)
@@ -191,6 +202,10 @@ struct PipelineOptions {  // pipeline.hpp:67-85
   bool sync_after_submit = false;
   bool capture_trajectory = false;
   int device = 0;
+  // Device frame store (ga3c_frames_*, frame envs): agents send only their
+  // newest 84x84 frame, the stacks live on the GPU, and the TrainingQueue
+  // carries frame-store slots instead of 28 KB states.
+  bool device_frames = false;
 };
 
 // Device-resident SharedModel (pipeline.hpp:92-111): immutable snapshots are
@@ -227,10 +242,12 @@ struct PredictorMetrics {
   std::atomic<std::int64_t> predictions{0};
   std::atomic<std::int64_t> batches{0};
 };
+// frames (nullable): requests carry newest frames, pushed into the device
+// frame store by the batched forward (ga3c_predict_frames64).
 void predictor_loop(BoundedChannel<PredictionRequest>& requests,
                     std::vector<std::unique_ptr<ResponseSlot<PredictionResponse>>>& slots,
                     SharedModel& model, ga3c_ctx* ctx, int pred_batch_max, PredictorMetrics& metrics,
-                    const std::atomic<bool>& stop);
+                    const std::atomic<bool>& stop, ga3c_frames* frames = nullptr);
 
 void validate(const PipelineOptions& opt);
 RunReport run(const PipelineOptions& opt);          // pipeline.cpp:607-611

@@ -57,6 +57,27 @@ struct Ctx {
   }
 };
 
+// Page-locked host buffer (ga3c_host_alloc): device copies from it are
+// asynchronous DMA instead of a staged pageable copy.
+struct PinnedBuf {
+  std::uint8_t* p = nullptr;
+  std::size_t cap = 0;
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  ~PinnedBuf() { ga3c_host_free(p); }
+  std::uint8_t* get(std::size_t bytes) {
+    if (bytes > cap) {
+      ga3c_host_free(p);
+      int st = 0;
+      p = static_cast<std::uint8_t*>(ga3c_host_alloc(bytes, &st));
+      if (!p) throw std::runtime_error("pinned host allocation failed");
+      cap = bytes;
+    }
+    return p;
+  }
+};
+
 // Contiguous host batch of observations for one device call.
 struct HostBatch {
   bool u8 = false;
@@ -79,17 +100,22 @@ struct HostBatch {
 // and gradients on `snap`; the gradient stays in ctx for apply().
 void train_on(Ctx& ctx, int slot, const std::vector<ExperienceBatch>& group, const ga3c_hyper& hp,
               HostBatch& hb, std::vector<std::int32_t>& acts, std::vector<double>& rew,
-              std::vector<std::int32_t>& off, std::vector<std::uint8_t>& term, std::vector<double>& boot) {
+              std::vector<std::int32_t>& off, std::vector<std::uint8_t>& term, std::vector<double>& boot,
+              ga3c_frames* frames = nullptr, std::vector<std::int32_t>* fidx = nullptr) {
   hb.clear();
   acts.clear();
   rew.clear();
   off.assign(1, 0);
   term.clear();
   boot.clear();
+  if (frames) fidx->clear();
   hb.u8 = !group.front().experiences.front().state.u8.empty();
   for (const auto& b : group) {
     for (const auto& e : b.experiences) {
-      hb.add(e.state);
+      if (frames)
+        fidx->push_back(e.state_slot);
+      else
+        hb.add(e.state);
       acts.push_back(e.action);
       rew.push_back(e.reward);
     }
@@ -100,6 +126,18 @@ void train_on(Ctx& ctx, int slot, const std::vector<ExperienceBatch>& group, con
   const int B = static_cast<int>(acts.size());
   ctx.ensure(B);
   const int n_seg = static_cast<int>(term.size());
+  if (frames) {
+    // states stay on the device: (agent, slot) per sample
+    std::vector<std::int32_t>& ag = *fidx;
+    ag.resize(2 * static_cast<std::size_t>(B));
+    int k = 0;
+    for (const auto& b : group)
+      for (std::size_t i = 0; i < b.experiences.size(); ++i) ag[B + k++] = b.agent_id;
+    const int st = ga3c_train_frames(ctx.c, slot, frames, ag.data() + B, ag.data(), B, acts.data(), rew.data(),
+                                     off.data(), n_seg, term.data(), boot.data(), hp.gamma, 1, nullptr, nullptr);
+    check(st, ctx.m, "train_frames");
+    return;
+  }
   const int st = hb.u8 ? ga3c_loss_grad_segments_u8(ctx.c, slot, hb.b8.data(), B, acts.data(), rew.data(),
                                                     off.data(), n_seg, term.data(), boot.data(), hp.gamma, 1,
                                                     nullptr, nullptr)
@@ -156,10 +194,13 @@ std::vector<float> SharedModel::read_theta() const {
 void predictor_loop(BoundedChannel<PredictionRequest>& requests,
                     std::vector<std::unique_ptr<ResponseSlot<PredictionResponse>>>& slots,
                     SharedModel& model, ga3c_ctx* ctx, int pred_batch_max, PredictorMetrics& metrics,
-                    const std::atomic<bool>& stop) {
+                    const std::atomic<bool>& stop, ga3c_frames* frames) {
   std::vector<PredictionRequest> got;
   HostBatch hb;
   std::vector<double> pi, v;
+  PinnedBuf newf;
+  std::vector<std::int32_t> agents, state_slots;
+  std::vector<std::uint8_t> resets;
   while (!stop.load(std::memory_order_relaxed)) {
     auto first = requests.pop(&stop);  // block for the first (pipeline.cpp:72)
     if (!first) break;
@@ -170,17 +211,35 @@ void predictor_loop(BoundedChannel<PredictionRequest>& requests,
       if (!more) break;
       got.push_back(std::move(*more));
     }
-    hb.u8 = !got.front().state.u8.empty();
-    hb.clear();
-    for (auto& r : got) hb.add(r.state);
     const int B = static_cast<int>(got.size());
     const auto snap = model.snapshot();
     const int A = ga3c_model_n_actions(model.handle());
     pi.resize(static_cast<std::size_t>(B) * A);
     v.resize(B);
     std::uint64_t ver = 0;
-    const int st = hb.u8 ? ga3c_forward64_u8(ctx, snap->slot, hb.b8.data(), B, pi.data(), v.data(), &ver)
-                         : ga3c_forward64_f32(ctx, snap->slot, hb.bf.data(), B, pi.data(), v.data(), &ver);
+    int st;
+    if (frames) {
+      // newest frames into a pinned batch; the store stacks them on the device
+      const std::size_t fb = got.front().state.u8.size();
+      std::uint8_t* buf = newf.get(fb * static_cast<std::size_t>(pred_batch_max));
+      agents.resize(B);
+      resets.resize(B);
+      state_slots.resize(B);
+      for (int i = 0; i < B; ++i) {
+        if (got[i].state.u8.size() != fb) throw std::invalid_argument("predictor: frame size mismatch");
+        std::memcpy(buf + static_cast<std::size_t>(i) * fb, got[i].state.u8.data(), fb);
+        agents[i] = got[i].agent_id;
+        resets[i] = got[i].reset ? 1 : 0;
+      }
+      st = ga3c_predict_frames64(ctx, snap->slot, frames, buf, agents.data(), resets.data(), B, state_slots.data(),
+                                 pi.data(), v.data(), &ver);
+    } else {
+      hb.u8 = !got.front().state.u8.empty();
+      hb.clear();
+      for (auto& r : got) hb.add(r.state);
+      st = hb.u8 ? ga3c_forward64_u8(ctx, snap->slot, hb.b8.data(), B, pi.data(), v.data(), &ver)
+                 : ga3c_forward64_f32(ctx, snap->slot, hb.bf.data(), B, pi.data(), v.data(), &ver);
+    }
     check(st, model.handle(), "forward");
     for (int i = 0; i < B; ++i) {
       PredictionResponse resp;
@@ -188,6 +247,7 @@ void predictor_loop(BoundedChannel<PredictionRequest>& requests,
                          pi.begin() + static_cast<std::ptrdiff_t>(i + 1) * A);
       resp.value = v[i];
       resp.model_version = ver;
+      if (frames) resp.state_slot = state_slots[i];
       slots[got[i].agent_id]->put(got[i].ticket, std::move(resp));
     }
     metrics.predictions.fetch_add(B, std::memory_order_relaxed);
@@ -217,6 +277,8 @@ void validate(const PipelineOptions& opt) {  // pipeline.cpp:572-603
     throw std::invalid_argument(
         "pipeline: lockstep mode requires one agent, one predictor, one trainer and min_train_batch 1");
   auto probe = make_env(opt.env);
+  if (opt.device_frames && (!probe->frames() || opt.net.in_c != 4))
+    throw std::invalid_argument("pipeline: device frames need an 84x84x4 frame environment");
   const ga3c_net_spec in = probe->input();
   if (in.in_h != opt.net.in_h || in.in_w != opt.net.in_w || in.in_c != opt.net.in_c)
     throw std::invalid_argument("pipeline: net input does not match env observation");
@@ -243,6 +305,20 @@ class Engine {
         train_q_(static_cast<std::size_t>(opt.knobs.train_queue_cap)),
         budget_(opt.stop.max_updates ? *opt.stop.max_updates : std::numeric_limits<std::int64_t>::max()) {
     for (std::size_t i = 0; i < slot_cap_; ++i) slots_.push_back(std::make_unique<ResponseSlot<PredictionResponse>>());
+    if (opt_.device_frames) {
+      // Per-agent history of stacked states on the device.  An agent's
+      // states in flight are its current one, its open batch, its batches in
+      // the TrainingQueue and in trainers' groups; agents also stall (after
+      // flushing their open batch) while `history - 2` of theirs are
+      // untrained, so a slot is never rewritten before training read it.
+      const int t = opt_.hyper.t_max;
+      const int mtb = opt_.anneal && opt_.anneal_batches ? 1024 : opt_.knobs.min_train_batch;
+      hist_ = std::max(256, mtb + 2 * t + 4);
+      int st = 0;
+      store_ = ga3c_frames_create(shared_.handle(), static_cast<int>(slot_cap_), hist_, &st);
+      if (!store_) check(st ? st : GA3C_CUDA_ERROR, shared_.handle(), "ga3c_frames_create");
+      for (std::size_t i = 0; i < slot_cap_; ++i) outstanding_.push_back(std::make_unique<std::atomic<int>>(0));
+    }
     if (opt_.capture_trajectory)
       traj_sink_ = [this](SharedModel& m) {
         std::lock_guard<std::mutex> lk(traj_m_);
@@ -253,6 +329,7 @@ class Engine {
   ~Engine() {
     request_stop();
     join_all();
+    ga3c_frames_destroy(store_);
   }
 
   RunReport run_all() {
@@ -278,25 +355,44 @@ class Engine {
   void agent_main(int id, std::atomic<bool>& stop) {
     try {
       auto env = make_env(opt_.env);
+      const bool dev_frames = store_ != nullptr;
+      if (dev_frames) env->set_single_frame(true);
       std::mt19937_64 rng(derive_seed(opt_.seed, {kSeedAgentRng, static_cast<std::uint64_t>(id)}));
       std::uint64_t episode = 0;
       Observation obs = env->reset(derive_seed(opt_.seed, {kSeedEnvEpisode, static_cast<std::uint64_t>(id), episode}));
+      bool fresh = true;  // the next request starts an episode (device stack = 4 x this frame)
       ExperienceBatch batch;
       batch.agent_id = id;
       double score = 0.0;
+      double last_value = 0.0;
       std::int64_t submitted = 0;
+      std::atomic<int>* out = dev_frames ? outstanding_[id].get() : nullptr;
       while (!stop.load(std::memory_order_relaxed)) {
+        if (out && out->load(std::memory_order_acquire) >= hist_ - 2) {
+          // frame-store backpressure: hand the open batch to the trainers
+          // and wait until enough of this agent's states were trained
+          if (!batch.experiences.empty() && !flush(batch, false, last_value, stop, submitted)) break;
+          while (out->load(std::memory_order_acquire) >= hist_ - 2 && !stop.load(std::memory_order_relaxed))
+            std::this_thread::yield();
+          continue;
+        }
         auto& slot = *slots_[id];
         const std::uint64_t ticket = slot.issue_ticket();
-        if (!pred_q_.push(PredictionRequest{id, ticket, obs}, &stop)) break;
+        PredictionRequest req{id, ticket, dev_frames ? std::move(obs) : obs, fresh};
+        fresh = false;
+        if (!pred_q_.push(std::move(req), &stop)) break;
         auto resp = slot.take(ticket, stop);
         if (!resp) break;
+        last_value = resp->value;
         const int A = static_cast<int>(resp->policy.size());
         const int action = opt_.greedy ? argmax_index(resp->policy.data(), A)
                                        : sample_index(resp->policy.data(), A, rng);
         StepResult sr = env->step(action);
         const double reward = opt_.hyper.clip_rewards ? std::clamp(sr.reward, -1.0, 1.0) : sr.reward;
-        batch.experiences.push_back(Experience{std::move(obs), action, reward, resp->value, resp->model_version});
+        batch.experiences.push_back(
+            Experience{dev_frames ? Observation{} : std::move(obs), action, reward, resp->value, resp->model_version,
+                       resp->state_slot});
+        if (out) out->fetch_add(1, std::memory_order_acq_rel);
         produced_.fetch_add(1, std::memory_order_relaxed);
         score += sr.reward;
         bool ok = true;
@@ -306,6 +402,7 @@ class Engine {
           score = 0.0;
           ++episode;
           obs = env->reset(derive_seed(opt_.seed, {kSeedEnvEpisode, static_cast<std::uint64_t>(id), episode}));
+          fresh = true;
         } else {
           obs = std::move(sr.observation);
           if (static_cast<int>(batch.experiences.size()) >= opt_.hyper.t_max)
@@ -313,7 +410,10 @@ class Engine {
         }
         if (!ok) break;
       }
-      if (!batch.experiences.empty()) dropped_.fetch_add(static_cast<std::int64_t>(batch.experiences.size()));
+      if (!batch.experiences.empty()) {
+        dropped_.fetch_add(static_cast<std::int64_t>(batch.experiences.size()));
+        if (out) out->fetch_sub(static_cast<int>(batch.experiences.size()), std::memory_order_acq_rel);
+      }
     } catch (...) {
       report_error(std::current_exception());
     }
@@ -331,6 +431,7 @@ class Engine {
     const auto n = static_cast<std::int64_t>(out.experiences.size());
     if (!train_q_.push(std::move(out), &stop)) {
       dropped_.fetch_add(n);
+      release(batch.agent_id, n);
       return false;
     }
     if (opt_.sync_after_submit) {
@@ -349,7 +450,7 @@ class Engine {
     try {
       Ctx ctx(shared_.handle(), std::max(64, opt_.knobs.min_train_batch + 4 * opt_.hyper.t_max));
       HostBatch hb;
-      std::vector<std::int32_t> acts, off;
+      std::vector<std::int32_t> acts, off, fidx;
       std::vector<double> rew, boot;
       std::vector<std::uint8_t> term;
       while (!stop.load(std::memory_order_relaxed)) {
@@ -370,18 +471,19 @@ class Engine {
         }
         if (bail) {
           dropped_.fetch_add(total);
+          for (const auto& b : group) release(b);
           break;
         }
         if (budget_.fetch_sub(1, std::memory_order_acq_rel) <= 0) {
           budget_.fetch_add(1, std::memory_order_relaxed);
           dropped_.fetch_add(total);
+          for (const auto& b : group) release(b);
           request_stop();
           break;
         }
-        const std::size_t backlog = train_q_.size();
-        (void)backlog;
         const auto snap = shared_.snapshot();
-        train_on(ctx, snap->slot, group, opt_.hyper, hb, acts, rew, off, term, boot);
+        train_on(ctx, snap->slot, group, opt_.hyper, hb, acts, rew, off, term, boot, store_, &fidx);
+        for (const auto& b : group) release(b);  // the device read these states
         const auto applied_on = shared_.apply(ctx.c, traj_sink_);
         if (applied_on) {
           std::uint64_t lag_sum = 0;
@@ -402,6 +504,12 @@ class Engine {
     }
   }
 
+  // An experience batch's frame-store states are free again (trained or dropped).
+  void release(int agent, std::int64_t n) {
+    if (store_) outstanding_[agent]->fetch_sub(static_cast<int>(n), std::memory_order_acq_rel);
+  }
+  void release(const ExperienceBatch& b) { release(b.agent_id, static_cast<std::int64_t>(b.experiences.size())); }
+
   void bump_gate() {
     gate_updates_.fetch_add(1, std::memory_order_relaxed);
     if (opt_.sync_after_submit) {
@@ -413,7 +521,7 @@ class Engine {
   void predictor_main(std::atomic<bool>& stop) {
     try {
       Ctx ctx(shared_.handle(), opt_.knobs.pred_batch_max);
-      predictor_loop(pred_q_, slots_, shared_, ctx.c, opt_.knobs.pred_batch_max, pmetrics_, stop);
+      predictor_loop(pred_q_, slots_, shared_, ctx.c, opt_.knobs.pred_batch_max, pmetrics_, stop, store_);
     } catch (...) {
       report_error(std::current_exception());
     }
@@ -647,6 +755,9 @@ class Engine {
   PipelineOptions opt_;
   std::size_t slot_cap_;
   SharedModel shared_;
+  ga3c_frames* store_ = nullptr;  // device frame store (device_frames)
+  int hist_ = 0;
+  std::vector<std::unique_ptr<std::atomic<int>>> outstanding_;  // untrained frame-store states per agent
   BoundedChannel<PredictionRequest> pred_q_;
   BoundedChannel<ExperienceBatch> train_q_;
   std::vector<std::unique_ptr<ResponseSlot<PredictionResponse>>> slots_;

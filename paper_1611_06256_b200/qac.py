@@ -349,6 +349,7 @@ class PipelineOptions:
     sync_after_submit: bool = False
     capture_trajectory: bool = False
     device: int = 0
+    device_frames: bool = False  # frame envs: newest frames in, stacks + training states on the GPU
 
 
 @dataclass
@@ -399,6 +400,7 @@ def _run(opt: PipelineOptions, sync: bool) -> RunReport:
     o.metrics_interval_s = opt.metrics_interval_s
     o.greedy, o.sync_after_submit = int(opt.greedy), int(opt.sync_after_submit)
     o.capture_trajectory, o.device = int(opt.capture_trajectory), opt.device
+    o.device_frames = int(opt.device_frames)
     P = int(_abi.lib.ga3c_param_count(o.net))
     cap_traj = (opt.stop.max_updates or 0) if opt.capture_trajectory else 0
     theta = np.zeros(P, np.float32)

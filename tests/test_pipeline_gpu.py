@@ -167,3 +167,73 @@ def test_frame_catch_dnn_a_free_running():
     assert r.total_updates == 50 and r.experiences_trained >= 50 * 20
     assert r.total_predictions >= r.experiences_produced
     assert np.all(np.isfinite(r.final_theta))
+
+
+# ------------------------------------------------ device frame store mode
+def test_lockstep_device_frames_equals_whole_states_bitwise():
+    """device_frames: agents send only their newest 84x84 frame, the stacks
+    are built on the GPU (ga3c_predict_frames64) and training gathers them
+    there (ga3c_train_frames).  FrameCatch's host stack and the device stack
+    hold the same bytes, so the lock-step run must reproduce train_sync on
+    whole states bit for bit (test_pipeline.cpp:123-148)."""
+    qac = q()
+    env = qac.frame_catch(7, 6)
+    opt = lockstep(env, 24, 5)
+    opt.net = qac.dnn_a()
+    opt.capture_trajectory = True
+    opt.device_frames = True
+    a = qac.run(opt)
+    opt.device_frames = False
+    b = qac.train_sync(opt)
+    assert a.total_updates == b.total_updates == 24
+    for x, y in zip(a.theta_trajectory, b.theta_trajectory):
+        assert np.array_equal(x, y)
+    assert a.episode_scores == b.episode_scores
+
+
+def test_device_frames_free_running_accounting():
+    qac = q()
+    env = qac.frames(episode_len=16)
+    opt = qac.PipelineOptions(net=qac.dnn_a(), env=env, device_frames=True)
+    opt.knobs = qac.KnobConfig(n_agents=32, n_predictors=2, n_trainers=2, pred_batch_max=32, min_train_batch=40)
+    opt.stop = qac.StopCondition(max_updates=200)
+    r = qac.run(opt)
+    assert r.total_updates == 200 and r.experiences_trained >= 200 * 40
+    assert r.experiences_produced == r.experiences_trained + r.experiences_left_queued + r.experiences_dropped
+    assert np.all(np.isfinite(r.final_theta))
+
+
+def test_device_frames_reject_non_frame_env():
+    qac = q()
+    env = qac.catch_grid(4)
+    opt = lockstep(env, 5, 1)
+    opt.device_frames = True
+    with pytest.raises(ValueError):
+        qac.run(opt)
+
+
+def test_annealer_moves_batch_knobs_in_a_running_pipeline():
+    """BASELINE configs[1]'s dynamic scheduling with the batch-geometry
+    extension (annealer.cpp:28-53 widened): over short epochs the
+    annealer proposes pred_batch_max / min_train_batch moves, the engine
+    restarts the predictor / trainer pools with them and keeps training."""
+    qac = q()
+    env = qac.frames(episode_len=32)
+    opt = qac.PipelineOptions(net=qac.dnn_a(), env=env, device_frames=True)
+    opt.knobs = qac.KnobConfig(n_agents=16, n_predictors=1, n_trainers=1, pred_batch_max=16, min_train_batch=20)
+    opt.anneal = True
+    opt.anneal_batches = True
+    opt.epoch_s = 0.15
+    opt.limits = (16, 3, 3)
+    opt.stop = qac.StopCondition(max_seconds=4.0)
+    opt.seed = 29
+    r = qac.run(opt)
+    hist = r.anneal_history
+    assert len(hist) >= 8
+    moved = {(h["knobs"].pred_batch_max, h["knobs"].min_train_batch) for h in hist}
+    assert len(moved) >= 2, moved  # batch geometry was proposed and run
+    for h in hist:
+        k = h["knobs"]
+        assert 1 <= k.n_agents <= 16 and 1 <= k.n_predictors <= 3 and 1 <= k.n_trainers <= 3
+        assert 1 <= k.pred_batch_max <= 1024 and 1 <= k.min_train_batch <= 1024
+    assert r.total_updates > 0 and np.all(np.isfinite(r.final_theta))
