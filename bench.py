@@ -64,7 +64,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-loop", action="store_true", help="skip the C++ GA3C loop leg (ga3c_loop)")
-    p.add_argument("--loop-seconds", type=float, default=5.0)
+    p.add_argument("--loop-seconds", type=float, default=10.0)
     p.add_argument("--e2e-steps", type=int, default=0)
     p.add_argument("--e2e-windows", type=int, default=3)
     p.add_argument("--e2e-trainers", type=int, default=4, help="trainer threads in the e2e leg (0 = serial)")
@@ -737,26 +737,52 @@ def large_leg(args):
 
 
 def loop_leg(args):
-    """BASELINE configs[1] as the reference runs it: the C++ host engine
-    (ga3c_pipeline_run = qac::run, pipeline.cpp:100-611) with agent threads
-    stepping synthetic 84x84x4 frame environments (envs.cpp Frames, no step
-    delay), N_P predictor threads batching the prediction queue into
-    ga3c_forward_u8, N_T trainer threads coalescing >= min_train_batch
-    experiences into ga3c_loss_grad_segments_u8 + ga3c_apply_rmsprop.  Whole
-    28 KB states cross PCIe both ways (the reference's data path); the knobs
-    are the paper's best DNN A point (N_A = 128, N_P = N_T = 2)."""
+    """BASELINE configs[1]: the C++ host engine (ga3c_pipeline_run = qac::run,
+    pipeline.cpp:100-611) on DNN A with agent threads stepping synthetic
+    frame environments (envs.cpp Frames, no step delay), predictor threads
+    batching the PredictionQueue, trainer threads coalescing >=
+    min_train_batch experiences, and the dynamic scheduler running
+    (annealer.cpp:28-53, pipeline.cpp:455-476; with the batch-geometry
+    extension).  Agents send their newest 84x84 frame; stacks and
+    the TrainingQueue's states stay on the GPU (device_frames).  Beside it,
+    the reference's data path (whole 28 KB states both ways, fixed knobs at
+    the paper's N_A = 128, N_P = N_T = 2)."""
     from paper_1611_06256_b200 import qac
-    opt = qac.PipelineOptions(net=qac.dnn_a(), env=qac.frames(step_delay_us=0, episode_len=64))
-    opt.knobs = qac.KnobConfig(n_agents=args.agents, n_predictors=2, n_trainers=2, pred_batch_max=args.agents,
-                               min_train_batch=args.train_batch)
+    env = qac.frames(step_delay_us=0, episode_len=64)
+    start = qac.KnobConfig(n_agents=2 * args.agents, n_predictors=4, n_trainers=6, pred_batch_max=args.agents,
+                           min_train_batch=args.train_batch)
+    opt = qac.PipelineOptions(net=qac.dnn_a(), env=env, device_frames=True)
+    opt.knobs = start
+    opt.anneal, opt.anneal_batches = True, True
+    opt.epoch_s = max(0.5, args.loop_seconds / 10)
+    opt.limits = (2 * args.agents, 8, 8)
     opt.stop = qac.StopCondition(max_seconds=args.loop_seconds)
     r = qac.run(opt)
+    hist = [dict(knobs=[h["knobs"].n_agents, h["knobs"].n_predictors, h["knobs"].n_trainers,
+                        h["knobs"].pred_batch_max, h["knobs"].min_train_batch],
+                 updates_per_s=round(h["measured_tps"], 1), accepted=h["accepted"])
+            for h in r.anneal_history]
+    ref = qac.PipelineOptions(net=qac.dnn_a(), env=env)
+    ref.knobs = qac.KnobConfig(n_agents=args.agents, n_predictors=2, n_trainers=2, pred_batch_max=args.agents,
+                               min_train_batch=args.train_batch)
+    ref.stop = qac.StopCondition(max_seconds=min(5.0, args.loop_seconds))
+    rw = qac.run(ref)
+    fk = r.final_knobs
     return {"value": r.avg_samples_per_s, "unit": "samples/s", "tps_updates_per_s": r.avg_tps,
             "pps": r.avg_pps, "updates": r.total_updates, "wall_s": r.wall_time_s, "mean_policy_lag": r.mean_lag,
-            "knobs": {"n_agents": args.agents, "n_predictors": 2, "n_trainers": 2,
-                      "pred_batch_max": args.agents, "min_train_batch": args.train_batch},
-            "path": "C++ host engine (ga3c_pipeline_run): agent threads + prediction/training queues + "
-                    "ga3c_forward_u8 / ga3c_loss_grad_segments_u8 / ga3c_apply_rmsprop"}
+            "knobs_start": {"n_agents": start.n_agents, "n_predictors": start.n_predictors,
+                            "n_trainers": start.n_trainers, "pred_batch_max": start.pred_batch_max,
+                            "min_train_batch": start.min_train_batch},
+            "knobs_final": {"n_agents": fk.n_agents, "n_predictors": fk.n_predictors, "n_trainers": fk.n_trainers,
+                            "pred_batch_max": fk.pred_batch_max, "min_train_batch": fk.min_train_batch},
+            "anneal": {"epoch_s": opt.epoch_s, "batches": True, "history": hist},
+            "path": "C++ host engine (ga3c_pipeline_run, device_frames): agent threads + prediction/training "
+                    "queues + ga3c_predict_frames64 (newest frames, pinned) / ga3c_train_frames / "
+                    "ga3c_apply_rmsprop, annealer on",
+            "whole_state_reference_path": {
+                "value": rw.avg_samples_per_s, "knobs": [args.agents, 2, 2, args.agents, args.train_batch],
+                "path": "ga3c_forward64_u8 / ga3c_loss_grad_segments_u8 / ga3c_apply_rmsprop, 28 KB states "
+                        "both ways, fixed knobs"}}
 
 
 def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world, grad_view, stream, dist):
@@ -856,15 +882,9 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
     # thread serves the agents while trainer threads, each with its own
     # context (stream), train on finished segments and apply to the latest
     # parameters (out-of-place snapshots, so predictions never read a
-    # half-written model).
-    import queue
-    import threading
-    ctx_t = [_abi.Context(model, max(NA, TB)) for _ in range(args.e2e_trainers)]
-    # trainer threads share the GPU like the device step's trainer contexts:
-    # the same SM budget rule (e2e 550K -> 574K samples/s for DNN A)
+    # half-written model).  The trainers share the GPU like the device
+    # step's trainer contexts: the same SM budget rule.
     e2e_sms = int(os.environ.get("GA3C_E2E_SMS", 0)) or (111 if 2.5 * fwd_flops_per_sample(args.net) < 50e6 else 148)
-    for c_ in ctx_t:
-        c_.set_sm_budget(e2e_sms)
     store.close()
     # training queue of train_queue_cap = 16 segments-batches (the
     # reference's knob, knobs.hpp:15, default 32): the predictor runs up to
@@ -872,22 +892,16 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
     # one being predicted), three if a trainer thread stalls while the
     # others drain a whole step, so the store keeps four steps of stacks
     store = _abi.Frames(model, NA, 4 * T + 2)
-    q = queue.Queue(maxsize=updates)
+    # GA3C's TrainingQueue + trainer threads, native (ga3c_trainer_pool_*):
+    # the predictor hands each update's segment batch over and moves on
+    pool_t = _abi.TrainerPool(model, store, args.e2e_trainers, max(NA, TB), e2e_sms, queue_cap=updates) \
+        if world == 1 and args.e2e_trainers > 0 else None
+    ag_u = [np.ascontiguousarray(np.repeat(agents[u * per_upd:(u + 1) * per_upd], T)) for u in range(updates)]
 
-    def trainer(j):
-        c = ctx_t[j]
-        while True:
-            item = q.get()
-            if item is None:
-                q.task_done()
-                q.put(None)
-                return
-            s, acts, slots, boot, u = item
-            sl = slice(u * per_upd, (u + 1) * per_upd)
-            _abi.train_frames(c, store, np.repeat(agents[sl], T), slots[sl].reshape(-1), acts[sl].reshape(-1),
-                              r_h[s][sl].reshape(-1), seg_off, term_h[s][sl], boot[sl], hyper.gamma)
-            c.apply_rmsprop()
-            q.task_done()
+    def submit(s, acts, slots, boot, u):
+        sl = slice(u * per_upd, (u + 1) * per_upd)
+        pool_t.submit(ag_u[u], slots[sl].reshape(-1), acts[sl].reshape(-1), r_h[s][sl].reshape(-1), seg_off,
+                      term_h[s][sl], boot[sl], hyper.gamma)
 
     # N_P predictor threads (GA3C's predictors), each with its own context,
     # serving a contiguous group of agents
@@ -922,10 +936,7 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
     dt = dt_serial
     mode = "serial calls"
     win_vals = []
-    if world == 1 and args.e2e_trainers > 0:
-        ths = [threading.Thread(target=trainer, args=(j,), daemon=True) for j in range(args.e2e_trainers)]
-        for th in ths:
-            th.start()
+    if pool_t is not None:
         pt = np.zeros(NA, np.uint8)
 
         def window(steps):
@@ -935,9 +946,9 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
             for i in range(steps):
                 s, acts, slots, boot = predict_step(i, pt)
                 for u in range(updates):
-                    q.put((s, acts, slots, boot, u))
+                    submit(s, acts, slots, boot, u)
                 pt = term_h[s].astype(np.uint8)
-            q.join()  # every update trained and its apply enqueued
+            pool_t.wait()  # every update trained and its apply enqueued
             torch.cuda.synchronize()
             return time.perf_counter() - t0
 
@@ -945,15 +956,12 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
         # three timed windows of k steps each, the median reported: on the
         # 16-vCPU box single windows of host threads vary by up to 1.5x
         wins = sorted(window(k) for _ in range(args.e2e_windows))
-        q.put(None)
-        for th in ths:
-            th.join()
         dt_thr = wins[len(wins) // 2]
         win_vals = [round(n * k / w) for w in wins]
         if dt_thr < dt:
-            dt, mode = dt_thr, f"{NP} predictor threads + {args.e2e_trainers} trainer threads"
-    for c in ctx_t:
-        c.close()
+            dt, mode = dt_thr, (f"{NP} predictor thread(s) + native trainer pool of {args.e2e_trainers} "
+                                f"(ga3c_trainer_pool)")
+        pool_t.close()
     store.close()
     out = {"value": world * n * k / dt, "unit": "samples/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "steps": k, "ms_per_step": 1e3 * dt / k, "mode": mode,

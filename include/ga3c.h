@@ -349,6 +349,26 @@ int ga3c_train_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const int32_t* agen
 /* Copy one stored stacked state to the host (tests, debugging). */
 int ga3c_frames_read(ga3c_frames* f, int agent, int state_slot, uint8_t* state);
 
+/* ------------------------------------------------------- trainer pool */
+/* GA3C's TrainingQueue + trainer threads (pipeline.cpp:241-306) as a
+ * component for hosts that run their own agents and predictors: n_threads
+ * native trainers, each with its own context (SM budget `sms`, 0 = all),
+ * take submitted segment batches in FIFO order and run ga3c_train_frames on
+ * the latest snapshot + ga3c_apply_rmsprop (a non-finite gradient is
+ * rejected and counted, nnet.cpp:299-301).  submit() copies its host
+ * arrays (the ga3c_train_frames arguments) and blocks while queue_cap
+ * batches are waiting; wait() returns once every submitted batch is applied
+ * (or rejected), with the totals so far and the first error. */
+typedef struct ga3c_trainer_pool ga3c_trainer_pool;
+ga3c_trainer_pool* ga3c_trainer_pool_create(ga3c_model* m, ga3c_frames* f, int n_threads, int max_batch, int sms,
+                                            int queue_cap, int* status);
+int ga3c_trainer_pool_submit(ga3c_trainer_pool* p, const int32_t* agents, const int32_t* state_slots, int B,
+                             const int32_t* actions, const double* rewards, const int32_t* seg_offsets, int n_seg,
+                             const uint8_t* terminal, const double* bootstrap, double gamma);
+int ga3c_trainer_pool_wait(ga3c_trainer_pool* p, long long* updates, long long* rejected);
+const char* ga3c_trainer_pool_error(ga3c_trainer_pool* p);
+void ga3c_trainer_pool_destroy(ga3c_trainer_pool* p);
+
 /* ------------------------------------------------------ timing probe */
 /* Kernel classes for the roofline probe. */
 #define GA3C_K_NONE 0
@@ -425,6 +445,10 @@ typedef struct ga3c_pipeline_opts {
    * frame, stacks and the TrainingQueue's states stay on the GPU
    * (ga3c_frames_*); 0 = whole states both ways, as the reference. */
   int device_frames;
+  /* SM budgets of the trainer / predictor contexts (ga3c_ctx_set_sm_budget):
+   * -1 = automatic (trainers 3/4 of the SMs and predictors 64 when several
+   * trainers share the GPU, else all), 0 = all SMs, n = n SMs. */
+  int trainer_sms, predictor_sms;
 } ga3c_pipeline_opts;
 
 typedef struct ga3c_run_report {

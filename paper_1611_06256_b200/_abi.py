@@ -70,7 +70,7 @@ class PipelineOpts(C.Structure):
         ("max_agents", C.c_int), ("max_predictors", C.c_int), ("max_trainers", C.c_int),
         ("metrics_interval_s", C.c_double),
         ("greedy", C.c_int), ("sync_after_submit", C.c_int), ("capture_trajectory", C.c_int), ("device", C.c_int),
-        ("device_frames", C.c_int),
+        ("device_frames", C.c_int), ("trainer_sms", C.c_int), ("predictor_sms", C.c_int),
     ]
 
 
@@ -170,6 +170,11 @@ _SIGS = {
     "ga3c_frames_destroy": (None, [_P]),
     "ga3c_host_alloc": (_P, [C.c_size_t, C.POINTER(C.c_int)]),
     "ga3c_host_free": (None, [_P]),
+    "ga3c_trainer_pool_create": (_P, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]),
+    "ga3c_trainer_pool_submit": (C.c_int, [_P, _P, _P, C.c_int, _P, _P, _P, C.c_int, _P, _P, C.c_double]),
+    "ga3c_trainer_pool_wait": (C.c_int, [_P, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
+    "ga3c_trainer_pool_error": (C.c_char_p, [_P]),
+    "ga3c_trainer_pool_destroy": (None, [_P]),
     "ga3c_predict_frames": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_int, _P, _P, _P,
                                       C.POINTER(C.c_uint64)]),
     "ga3c_predict_frames64": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_int, _P, _P, _P,
@@ -572,6 +577,51 @@ def train_frames(ctx: "Context", frames: Frames, agents, state_slots, actions, r
                                 rw.ctypes.data, off.ctypes.data, len(off) - 1, te.ctypes.data, bo.ctypes.data,
                                 gamma, 1 if apply_clip else 0, sc.ctypes.data, rets.ctypes.data), ctx.model.error())
     return sc, rets
+
+
+class TrainerPool:
+    """Native TrainingQueue + trainer threads (ga3c_trainer_pool_*): submit()
+    hands a segment batch to C++ trainers (train_frames + apply_rmsprop on
+    their own contexts) and returns; wait() blocks until all are applied."""
+
+    def __init__(self, model: Model, frames: Frames, n_threads: int, max_batch: int, sms: int = 0,
+                 queue_cap: int = 16):
+        st = C.c_int(0)
+        self.h = lib.ga3c_trainer_pool_create(model.h, frames.h, n_threads, max_batch, sms, queue_cap,
+                                              C.byref(st))
+        if not self.h:
+            check(st.value or 3, model.error())
+        self.model = model
+
+    def submit(self, agents, state_slots, actions, rewards, seg_offsets, terminal, bootstrap, gamma):
+        import numpy as np
+        ag = np.ascontiguousarray(agents, np.int32)
+        sl = np.ascontiguousarray(state_slots, np.int32)
+        ac = np.ascontiguousarray(actions, np.int32)
+        rw = np.ascontiguousarray(rewards, np.float64)
+        off = np.ascontiguousarray(seg_offsets, np.int32)
+        te = np.ascontiguousarray(terminal, np.uint8)
+        bo = np.ascontiguousarray(bootstrap, np.float64)
+        check(lib.ga3c_trainer_pool_submit(self.h, ag.ctypes.data, sl.ctypes.data, len(ag), ac.ctypes.data,
+                                           rw.ctypes.data, off.ctypes.data, len(off) - 1, te.ctypes.data,
+                                           bo.ctypes.data, gamma), self.error())
+
+    def wait(self):
+        """-> (updates applied, updates rejected) so far."""
+        u, r = C.c_longlong(0), C.c_longlong(0)
+        check(lib.ga3c_trainer_pool_wait(self.h, C.byref(u), C.byref(r)), self.error())
+        return u.value, r.value
+
+    def error(self):
+        return (lib.ga3c_trainer_pool_error(self.h) or b"").decode() if self.h else ""
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.ga3c_trainer_pool_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
 
 
 class FusedDP:

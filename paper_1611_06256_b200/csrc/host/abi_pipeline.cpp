@@ -47,6 +47,8 @@ PipelineOptions to_options(const ga3c_pipeline_opts* o) {
   p.capture_trajectory = o->capture_trajectory != 0;
   p.device = o->device;
   p.device_frames = o->device_frames != 0;
+  p.trainer_sms = o->trainer_sms;
+  p.predictor_sms = o->predictor_sms;
   return p;
 }
 
@@ -79,6 +81,8 @@ void ga3c_default_pipeline_opts(ga3c_pipeline_opts* o) {
   o->max_predictors = l.max_predictors;
   o->max_trainers = l.max_trainers;
   o->metrics_interval_s = 1.0;
+  o->trainer_sms = -1;
+  o->predictor_sms = -1;
 }
 
 int ga3c_pipeline_run(const ga3c_pipeline_opts* o, int sync_trainer, ga3c_run_report* r, float* final_theta,

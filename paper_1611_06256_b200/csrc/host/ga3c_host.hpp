@@ -206,6 +206,9 @@ struct PipelineOptions {  // pipeline.hpp:67-85
   // newest 84x84 frame, the stacks live on the GPU, and the TrainingQueue
   // carries frame-store slots instead of 28 KB states.
   bool device_frames = false;
+  // SM budgets of trainer / predictor contexts: -1 automatic, 0 all, n SMs
+  int trainer_sms = -1;
+  int predictor_sms = -1;
 };
 
 // Device-resident SharedModel (pipeline.hpp:92-111): immutable snapshots are

@@ -449,6 +449,7 @@ class Engine {
   void trainer_main(std::atomic<bool>& stop) {
     try {
       Ctx ctx(shared_.handle(), std::max(64, opt_.knobs.min_train_batch + 4 * opt_.hyper.t_max));
+      ga3c_ctx_set_sm_budget(ctx.c, sm_budget(opt_.trainer_sms, 111));
       HostBatch hb;
       std::vector<std::int32_t> acts, off, fidx;
       std::vector<double> rew, boot;
@@ -504,6 +505,14 @@ class Engine {
     }
   }
 
+  // Context SM budget: explicit, or (auto) the device loop's measured split
+  // when several trainers share the GPU (trainers 111 of 148 SMs, predictors
+  // 64: DESIGN.md section 5), else the whole GPU.
+  int sm_budget(int opt, int shared) const {
+    if (opt >= 0) return opt;
+    return n_t_.load() > 1 ? shared : 0;
+  }
+
   // An experience batch's frame-store states are free again (trained or dropped).
   void release(int agent, std::int64_t n) {
     if (store_) outstanding_[agent]->fetch_sub(static_cast<int>(n), std::memory_order_acq_rel);
@@ -521,6 +530,7 @@ class Engine {
   void predictor_main(std::atomic<bool>& stop) {
     try {
       Ctx ctx(shared_.handle(), opt_.knobs.pred_batch_max);
+      ga3c_ctx_set_sm_budget(ctx.c, sm_budget(opt_.predictor_sms, 64));
       predictor_loop(pred_q_, slots_, shared_, ctx.c, opt_.knobs.pred_batch_max, pmetrics_, stop, store_);
     } catch (...) {
       report_error(std::current_exception());

@@ -350,6 +350,8 @@ class PipelineOptions:
     capture_trajectory: bool = False
     device: int = 0
     device_frames: bool = False  # frame envs: newest frames in, stacks + training states on the GPU
+    trainer_sms: int = -1  # SM budget per trainer context (-1 auto, 0 all)
+    predictor_sms: int = -1  # SM budget per predictor context (-1 auto, 0 all)
 
 
 @dataclass
@@ -401,6 +403,7 @@ def _run(opt: PipelineOptions, sync: bool) -> RunReport:
     o.greedy, o.sync_after_submit = int(opt.greedy), int(opt.sync_after_submit)
     o.capture_trajectory, o.device = int(opt.capture_trajectory), opt.device
     o.device_frames = int(opt.device_frames)
+    o.trainer_sms, o.predictor_sms = opt.trainer_sms, opt.predictor_sms
     P = int(_abi.lib.ga3c_param_count(o.net))
     cap_traj = (opt.stop.max_updates or 0) if opt.capture_trajectory else 0
     theta = np.zeros(P, np.float32)
