@@ -37,6 +37,8 @@
 #include "tc_wgrad.cuh"
 #include "tc_pipe.cuh"
 #include "tc_ws.cuh"
+#include <cudaTypedefs.h>
+
 #include "tc_bf16.cuh"
 #include "tc_dgrad.cuh"
 #include "tc_u8conv.cuh"
@@ -405,41 +407,87 @@ void launch_gemm(ga3c_ctx* c, int tag, int layer, const LA& la, const LB& lb, co
 
 // ------------------------------------------------------ tensor-core GEMMs
 
-template <typename TA, typename TB, int BN, int MODE, int CAP>
+template <typename TA, typename TB, int BN, int MODE, int CAP, bool TMA>
 void tc_launch_v(ga3c_ctx* c, int tag, int layer, const Seg& A, const Seg& B, int M, int N, int K, int splits,
-                 int kc, const TcEpiArgs& epi) {
+                 int kc, const TcEpiArgs& epi, const TmaConv& tm) {
   using S = ws::KKShape<TA, TB, BN, CAP>;
-  auto kern = ws::tc_kk_ws_kernel<TA, TB, BN, MODE, CAP>;
+  auto kern = ws::tc_kk_ws_kernel<TA, TB, BN, MODE, CAP, TMA>;
   GA3C_SMEM_ONCE(kern, S::SMEM);
   dim3 grid((M + 127) / 128, splits, (N + BN - 1) / BN);
   Launch l(c, tag, layer);
   if (MODE == TC_EPI_BIAS_RELU && splits > 1)  // split-K reduced inside a cluster
     pdl_launch_cluster(c->cur, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, dim3(1, splits, 1), A, B, M, N, K,
-                       kc, epi);
+                       kc, epi, tm);
   else
-    pdl_launch(c->cur, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, A, B, M, N, K, kc, epi);
+    pdl_launch(c->cur, kern, dim3(grid), dim3(ws::kThreads), S::SMEM, A, B, M, N, K, kc, epi, tm);
 }
 
-template <typename TA, typename TB, int BN, int MODE>
+template <typename TA, typename TB, int BN, int MODE, bool TMA>
 void tc_launch(ga3c_ctx* c, int tag, int layer, const Seg& A, const Seg& B, int M, int N, int K, int splits,
-               int kc, const TcEpiArgs& epi) {
+               int kc, const TcEpiArgs& epi, const TmaConv& tm) {
   const long long ctas = static_cast<long long>((M + 127) / 128) * splits * ((N + BN - 1) / BN);
   const int cap = ring_cap(c, (std::min(kc, K) + 31) / 32, ctas);
-#define GA3C_F(C) tc_launch_v<TA, TB, BN, MODE, C>(c, tag, layer, A, B, M, N, K, splits, kc, epi)
+#define GA3C_F(C) tc_launch_v<TA, TB, BN, MODE, C, TMA>(c, tag, layer, A, B, M, N, K, splits, kc, epi, tm)
   GA3C_CAP_SWITCH(cap, GA3C_F)
 #undef GA3C_F
 }
 
-template <typename TA, typename TB, int MODE>
+template <typename TA, typename TB, int MODE, bool TMA = false>
 void tc_dispatch(ga3c_ctx* c, int tag, int layer, int bn, const Seg& A, const Seg& B, int M, int N,
-                 int K, int splits, int kc, const TcEpiArgs& epi) {
+                 int K, int splits, int kc, const TcEpiArgs& epi, const TmaConv& tm = TmaConv{}) {
   switch (bn) {
-    case 16: tc_launch<TA, TB, 16, MODE>(c, tag, layer, A, B, M, N, K, splits, kc, epi); break;
-    case 32: tc_launch<TA, TB, 32, MODE>(c, tag, layer, A, B, M, N, K, splits, kc, epi); break;
-    case 64: tc_launch<TA, TB, 64, MODE>(c, tag, layer, A, B, M, N, K, splits, kc, epi); break;
-    case 128: tc_launch<TA, TB, 128, MODE>(c, tag, layer, A, B, M, N, K, splits, kc, epi); break;
-    default: tc_launch<TA, TB, 128, MODE>(c, tag, layer, A, B, M, N, K, splits, kc, epi); break;
+    case 16: tc_launch<TA, TB, 16, MODE, TMA>(c, tag, layer, A, B, M, N, K, splits, kc, epi, tm); break;
+    case 32: tc_launch<TA, TB, 32, MODE, TMA>(c, tag, layer, A, B, M, N, K, splits, kc, epi, tm); break;
+    case 64: tc_launch<TA, TB, 64, MODE, TMA>(c, tag, layer, A, B, M, N, K, splits, kc, epi, tm); break;
+    default: tc_launch<TA, TB, 128, MODE, TMA>(c, tag, layer, A, B, M, N, K, splits, kc, epi, tm); break;
   }
+}
+
+// Tensor maps of a TMA-staged conv forward (TmaConv): im2col over the NHWC
+// fp32 input [B][IH][IW][Cin] and tiles of the OHWI weights.  False when the
+// driver entry points are missing or the geometry is outside what the TMA
+// im2col mode encodes (the cp.async gather path is used then).
+bool conv_tma_maps(const Layer& L, const float* x, const float* w, int B, int bn, TmaConv* tm) {
+  static PFN_cuTensorMapEncodeIm2col enc_im2col = nullptr;
+  static PFN_cuTensorMapEncodeTiled enc_tiled = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      enc_im2col = reinterpret_cast<PFN_cuTensorMapEncodeIm2col>(f);
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      enc_tiled = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(f);
+  });
+  if (!enc_im2col || !enc_tiled) return false;
+  if (L.cin % 32 != 0 || L.k - 1 > 127 || L.stride > 8 || (reinterpret_cast<uintptr_t>(x) % 16) != 0 ||
+      (reinterpret_cast<uintptr_t>(w) % 16) != 0)
+    return false;
+  const cuuint64_t gdim[4] = {static_cast<cuuint64_t>(L.cin), static_cast<cuuint64_t>(L.iw),
+                              static_cast<cuuint64_t>(L.ih), static_cast<cuuint64_t>(B)};
+  const cuuint64_t gstride[3] = {static_cast<cuuint64_t>(L.cin) * 4, static_cast<cuuint64_t>(L.iw) * L.cin * 4,
+                                 static_cast<cuuint64_t>(L.ih) * L.iw * L.cin * 4};
+  const int lower[2] = {0, 0};
+  const int upper[2] = {-(L.k - 1), -(L.k - 1)};  // VALID: the window corner spans [0, I - k]
+  const cuuint32_t estride[4] = {1, static_cast<cuuint32_t>(L.stride), static_cast<cuuint32_t>(L.stride), 1};
+  if (enc_im2col(&tm->a, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), gdim, gstride, lower, upper, 32,
+                 128, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  const cuuint64_t wdim[2] = {static_cast<cuuint64_t>(L.in), static_cast<cuuint64_t>(L.cout)};
+  const cuuint64_t wstride[1] = {static_cast<cuuint64_t>(L.in) * 4};
+  const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(bn)};
+  const cuuint32_t one[2] = {1, 1};
+  if (enc_tiled(&tm->b, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(w), wdim, wstride, box, one,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  tm->cin = L.cin;
+  tm->k = L.k;
+  tm->stride = L.stride;
+  return true;
 }
 
 int tc_bn(int n) {  // N tile; 2*BN (hi|lo concatenated) must fit one MMA (<= 256)
@@ -616,6 +664,15 @@ void conv_forward(ga3c_ctx* c, int li, const Layer& L, const float* theta, const
       int ks = std::max(1, std::min({8, chunks, cluster_sms(c) / std::max(1, tiles)}));
       const int kc = ((chunks + ks - 1) / ks) * 32;
       ks = (L.in + kc - 1) / kc;
+      if constexpr (sizeof(T) == 4) {
+        // fp32 input with whole 32-channel taps: TMA-staged operands
+        TmaConv tm;
+        if (in_stride <= 0 && conv_tma_maps(L, static_cast<const float*>(x), theta + L.w_off, B, bn, &tm)) {
+          tc_dispatch<float, float, TC_EPI_BIAS_RELU, true>(c, GA3C_K_CONV_FWD, li, bn, A, W, M, L.cout, L.in, ks,
+                                                            kc, e, tm);
+          return;
+        }
+      }
       tc_dispatch<T, float, TC_EPI_BIAS_RELU>(c, GA3C_K_CONV_FWD, li, bn, A, W, M, L.cout, L.in, ks, kc, e);
       return;
     }

@@ -9,6 +9,8 @@
 //   detail::   shared-memory stores and alignment helpers
 #pragma once
 
+#include <cuda.h>
+
 #include <cstdint>
 
 #include "tc_common.cuh"
@@ -41,6 +43,18 @@ struct Seg {
 };
 
 enum { TC_EPI_BIAS_RELU = 0, TC_EPI_PART_T = 1 };
+
+// TMA-staged conv forward operands (tc_kk_ws_kernel<float, float, BN, 0, CAP,
+// true>): `a` is an im2col tensor map over the NHWC fp32 input [B][IH][IW][Cin]
+// (Cin % 32 == 0; 32 channels x 128 output pixels per box, traversal stride
+// = the conv stride, bounding box = the VALID window range), `b` a tiled map
+// over the OHWI weights [Cout][k*k*Cin] (box 32 x BN); both SWIZZLE_128B,
+// i.e. exactly the K-major canonical layout the tf32 MMA descriptors read.
+struct alignas(64) TmaConv {
+  CUtensorMap a;
+  CUtensorMap b;
+  int cin, k, stride;
+};
 
 struct TcEpiArgs {
   const float* bias;  // per n (TC_EPI_BIAS_RELU)

@@ -67,13 +67,17 @@ struct KKShape {
   static constexpr int TMEM_COLS = TmemCols<ACC_COLS>::V;
 };
 
-template <typename TA, typename TB, int BN, int MODE, int CAP = 0>
+// TMA (conv forward, fp32 operands): one producer thread loads each stage's
+// hi tiles with an im2col tensor copy (A) and a tiled copy (B) that complete
+// on full[s]; the producer warps then only compute the lo parts.
+template <typename TA, typename TB, int BN, int MODE, int CAP = 0, bool TMA = false>
 __global__ void __launch_bounds__(kThreads, 1)
-tc_kk_ws_kernel(Seg A, Seg B, int M, int N, int K, int kc, TcEpiArgs epi) {
+tc_kk_ws_kernel(Seg A, Seg B, int M, int N, int K, int kc, TcEpiArgs epi, const __grid_constant__ TmaConv tm) {
   using S = KKShape<TA, TB, BN, CAP>;
   static_assert(!S::B_LO || 2 * BN <= 256, "N-concatenated tile exceeds the MMA N limit");
+  static_assert(!TMA || (sizeof(TA) == 4 && sizeof(TB) == 4 && MODE == TC_EPI_BIAS_RELU), "TMA: fp32 conv forward");
   extern __shared__ uint8_t smem_raw[];
-  __shared__ uint64_t ready[pipe::kMaxStages], done[pipe::kMaxStages], acc_bar;
+  __shared__ uint64_t ready[pipe::kMaxStages], done[pipe::kMaxStages], full[pipe::kMaxStages], acc_bar;
   __shared__ uint32_t tmem_base_sh;
   __shared__ float bias_sh[BN];
   uint8_t* smem = detail::align1024(smem_raw);
@@ -91,19 +95,46 @@ tc_kk_ws_kernel(Seg A, Seg B, int M, int N, int K, int kc, TcEpiArgs epi) {
   TRACE(0);
   typename S::TileA ta;
   typename S::TileB tb;
+  // TMA: the first output pixel's window corner (b, h, w) in the input
+  int t_w = 0, t_h = 0, t_n = 0;
+  auto tma_issue = [&](int c, uint32_t st, uint64_t* bar) {
+    const int k0 = kb + 32 * c;
+    const int tap = k0 / tm.cin, ci0 = k0 - tap * tm.cin;
+    const int ky = tap / tm.k, kx = tap - ky * tm.k;
+    tc::mbar_expect_tx(bar, S::TileA::HI_BYTES + S::TileB::HI_BYTES);
+    tc::tma_im2col_4d(st, &tm.a, ci0, t_w, t_h, t_n, static_cast<uint16_t>(kx), static_cast<uint16_t>(ky), bar);
+    tc::tma_tile_2d(st + S::TileA::BYTES, &tm.b, k0, n0, bar);
+  };
+  if constexpr (TMA) {
+    const int pp = m0 % A.P, oy = pp / A.ow;
+    t_n = m0 / A.P;
+    t_h = oy * tm.stride;
+    t_w = (pp - oy * A.ow) * tm.stride;
+  }
   pdl_trigger();
   if (warp < kMmaWarp) {
     ta.init(A, m0, tid);
     tb.init(B, n0, tid);
-    pdl_wait();  // everything below reads the predecessor's outputs
+    if constexpr (TMA) {
+      pdl_wait();  // the epilogue's global accesses, and the loads below, follow the predecessor
+      if (tid == 0) {
+        tc::tma_prefetch_desc(&tm.a);
+        tc::tma_prefetch_desc(&tm.b);
 #pragma unroll
-    for (int c = 0; c < S::NS - 1; ++c) {
-      if (c < nchunks) {
-        const uint32_t st = sbase + c * S::STAGE;
-        ta.issue(A, A.chunkoff(kb + 32 * c), st, tid);
-        tb.issue(B, B.chunkoff(kb + 32 * c), st + S::TileA::BYTES, tid);
+        for (int s = 0; s < S::NS; ++s) tc::mbar_init(&full[s], 1);
+        tc::fence_barrier_init();
       }
-      commit();
+    } else {
+      pdl_wait();  // everything below reads the predecessor's outputs
+#pragma unroll
+      for (int c = 0; c < S::NS - 1; ++c) {
+        if (c < nchunks) {
+          const uint32_t st = sbase + c * S::STAGE;
+          ta.issue(A, A.chunkoff(kb + 32 * c), st, tid);
+          tb.issue(B, B.chunkoff(kb + 32 * c), st + S::TileA::BYTES, tid);
+        }
+        commit();
+      }
     }
   } else {
     tc::tmem_alloc<S::TMEM_COLS>(&tmem_base_sh);
@@ -121,6 +152,13 @@ tc_kk_ws_kernel(Seg A, Seg B, int M, int N, int K, int kc, TcEpiArgs epi) {
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
+  if constexpr (TMA) {
+    if (tid == 0) {
+#pragma unroll
+      for (int c = 0; c < S::NS - 1; ++c)
+        if (c < nchunks) tma_issue(c, sbase + c * S::STAGE, &full[c]);
+    }
+  }
   TRACE(1);
 
   if (warp == kMmaWarp) {
@@ -164,7 +202,10 @@ tc_kk_ws_kernel(Seg A, Seg B, int M, int N, int K, int kc, TcEpiArgs epi) {
     for (int i = 0; i < nchunks; ++i) {
       const int s = i % S::NS;
       const uint32_t st = sbase + s * S::STAGE;
-      wait_group<S::NS - 2>();
+      if constexpr (TMA)
+        tc::mbar_wait(&full[s], (i / S::NS) & 1);
+      else
+        wait_group<S::NS - 2>();
       TRACE(64 + 4 * i);
       ta.convert(st, tid);
       tb.convert(st + S::TileA::BYTES, tid);
@@ -173,12 +214,19 @@ tc_kk_ws_kernel(Seg A, Seg B, int M, int N, int K, int kc, TcEpiArgs epi) {
       const int nc = i + S::NS - 1;
       if (nc < nchunks) {
         const int ps = nc % S::NS;
-        if (i >= 1) tc::mbar_wait(&done[ps], ((i - 1) / S::NS) & 1);
         const uint32_t pst = sbase + ps * S::STAGE;
-        ta.issue(A, A.chunkoff(kb + 32 * nc), pst, tid);
-        tb.issue(B, B.chunkoff(kb + 32 * nc), pst + S::TileA::BYTES, tid);
+        if constexpr (TMA) {
+          if (tid == 0) {
+            if (i >= 1) tc::mbar_wait(&done[ps], ((i - 1) / S::NS) & 1);
+            tma_issue(nc, pst, &full[ps]);
+          }
+        } else {
+          if (i >= 1) tc::mbar_wait(&done[ps], ((i - 1) / S::NS) & 1);
+          ta.issue(A, A.chunkoff(kb + 32 * nc), pst, tid);
+          tb.issue(B, B.chunkoff(kb + 32 * nc), pst + S::TileA::BYTES, tid);
+        }
       }
-      commit();
+      if constexpr (!TMA) commit();
     }
     // ---- epilogue (producer warps): C = acc[0:BN) (+ acc[BN:2BN) for B_lo),
     // staged through the (now idle) pipeline smem so global stores are

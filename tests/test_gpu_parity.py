@@ -473,3 +473,19 @@ def test_apply_rmsprop_dev_in_place_and_reject():
     ctx.apply_rmsprop_dev()
     t2, g2, _ = m.read()
     assert np.array_equal(t2, t1) and np.array_equal(g2, g1) and ctx.dev_version() == v0 + 1
+
+
+@pytest.mark.parametrize("B", [4, 40])
+def test_tma_conv_forward_cluster_and_channel_offsets(B):
+    """The TMA-staged conv forward (im2col tensor map over the NHWC input +
+    tiled weight map, tc_kk_ws_kernel<..., TMA>): Cin = 32 and 64 layers
+    (a 64-channel input takes two 32-channel boxes per filter tap), a 3x3
+    stride-1 window, and grids small enough that K is split over a cluster
+    (DSMEM reduction) -- forward and gradients against the oracle."""
+    spec = O.make_spec((84, 84, 4), [(32, 8, 4), (64, 4, 2), (64, 3, 1)], [64], 6)
+    th = theta32(spec, 21)
+    fr = O.synthetic_frames(5, B)
+    st = O.frames_to_states(fr)
+    check_forward(spec, th, fr, st)
+    acts, rets = O.synthetic_batch(5, B, 6)
+    check_grad(spec, th, fr, st, acts, rets)
