@@ -896,12 +896,17 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
     # the predictor hands each update's segment batch over and moves on
     pool_t = _abi.TrainerPool(model, store, args.e2e_trainers, max(NA, TB), e2e_sms, queue_cap=updates) \
         if world == 1 and args.e2e_trainers > 0 else None
-    ag_u = [np.ascontiguousarray(np.repeat(agents[u * per_upd:(u + 1) * per_upd], T)) for u in range(updates)]
+    # a step's updates go over in one call: update u = agents [u*per_upd, (u+1)*per_upd)
+    # (their T-step segments, agent-major), so every per-sample array is the
+    # step's (NA, T) array flattened and the segment tables are regular
+    ag_all = np.ascontiguousarray(np.repeat(agents, T))
+    b_off = np.arange(0, n + 1, TB, dtype=np.int32)
+    s_base = np.arange(0, NA + 1, per_upd, dtype=np.int32)
+    s_off = np.ascontiguousarray(np.tile(seg_off, updates))
 
-    def submit(s, acts, slots, boot, u):
-        sl = slice(u * per_upd, (u + 1) * per_upd)
-        pool_t.submit(ag_u[u], slots[sl].reshape(-1), acts[sl].reshape(-1), r_h[s][sl].reshape(-1), seg_off,
-                      term_h[s][sl], boot[sl], hyper.gamma)
+    def submit_step(s, acts, slots, boot):
+        pool_t.submit_many(b_off, s_base, ag_all, slots.reshape(-1), acts.reshape(-1), r_h[s].reshape(-1), s_off,
+                           term_h[s], boot, hyper.gamma)
 
     # N_P predictor threads (GA3C's predictors), each with its own context,
     # serving a contiguous group of agents
@@ -945,8 +950,7 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
             t0 = time.perf_counter()
             for i in range(steps):
                 s, acts, slots, boot = predict_step(i, pt)
-                for u in range(updates):
-                    submit(s, acts, slots, boot, u)
+                submit_step(s, acts, slots, boot)
                 pt = term_h[s].astype(np.uint8)
             pool_t.wait()  # every update trained and its apply enqueued
             torch.cuda.synchronize()

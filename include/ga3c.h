@@ -365,6 +365,15 @@ ga3c_trainer_pool* ga3c_trainer_pool_create(ga3c_model* m, ga3c_frames* f, int n
 int ga3c_trainer_pool_submit(ga3c_trainer_pool* p, const int32_t* agents, const int32_t* state_slots, int B,
                              const int32_t* actions, const double* rewards, const int32_t* seg_offsets, int n_seg,
                              const uint8_t* terminal, const double* bootstrap, double gamma);
+/* n_batches submits in one call: batch i covers samples
+ * [batch_off[i], batch_off[i+1]) of the concatenated per-sample arrays and
+ * segments [seg_base[i], seg_base[i+1]) of terminal / bootstrap, whose
+ * offsets (relative to the batch, each list starting at 0) are
+ * seg_offsets[seg_base[i] + i .. seg_base[i+1] + i]. */
+int ga3c_trainer_pool_submit_many(ga3c_trainer_pool* p, int n_batches, const int32_t* batch_off,
+                                  const int32_t* seg_base, const int32_t* agents, const int32_t* state_slots,
+                                  const int32_t* actions, const double* rewards, const int32_t* seg_offsets,
+                                  const uint8_t* terminal, const double* bootstrap, double gamma);
 int ga3c_trainer_pool_wait(ga3c_trainer_pool* p, long long* updates, long long* rejected);
 const char* ga3c_trainer_pool_error(ga3c_trainer_pool* p);
 void ga3c_trainer_pool_destroy(ga3c_trainer_pool* p);

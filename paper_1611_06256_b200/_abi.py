@@ -172,6 +172,7 @@ _SIGS = {
     "ga3c_host_free": (None, [_P]),
     "ga3c_trainer_pool_create": (_P, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "ga3c_trainer_pool_submit": (C.c_int, [_P, _P, _P, C.c_int, _P, _P, _P, C.c_int, _P, _P, C.c_double]),
+    "ga3c_trainer_pool_submit_many": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_double]),
     "ga3c_trainer_pool_wait": (C.c_int, [_P, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
     "ga3c_trainer_pool_error": (C.c_char_p, [_P]),
     "ga3c_trainer_pool_destroy": (None, [_P]),
@@ -605,6 +606,20 @@ class TrainerPool:
         check(lib.ga3c_trainer_pool_submit(self.h, ag.ctypes.data, sl.ctypes.data, len(ag), ac.ctypes.data,
                                            rw.ctypes.data, off.ctypes.data, len(off) - 1, te.ctypes.data,
                                            bo.ctypes.data, gamma), self.error())
+
+    def submit_many(self, batch_off, seg_base, agents, state_slots, actions, rewards, seg_offsets, terminal,
+                    bootstrap, gamma):
+        """Several batches in one call (ga3c_trainer_pool_submit_many): batch i =
+        samples [batch_off[i], batch_off[i+1]), segments [seg_base[i],
+        seg_base[i+1]), its offsets at seg_offsets[seg_base[i] + i ...]."""
+        import numpy as np
+        arr = [np.ascontiguousarray(batch_off, np.int32), np.ascontiguousarray(seg_base, np.int32),
+               np.ascontiguousarray(agents, np.int32), np.ascontiguousarray(state_slots, np.int32),
+               np.ascontiguousarray(actions, np.int32), np.ascontiguousarray(rewards, np.float64),
+               np.ascontiguousarray(seg_offsets, np.int32), np.ascontiguousarray(terminal, np.uint8),
+               np.ascontiguousarray(bootstrap, np.float64)]
+        check(lib.ga3c_trainer_pool_submit_many(self.h, len(arr[0]) - 1, *[a.ctypes.data for a in arr], gamma),
+              self.error())
 
     def wait(self):
         """-> (updates applied, updates rejected) so far."""

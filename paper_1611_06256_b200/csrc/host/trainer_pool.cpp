@@ -139,6 +139,21 @@ int ga3c_trainer_pool_submit(ga3c_trainer_pool* p, const int32_t* agents, const 
   return GA3C_OK;
 }
 
+int ga3c_trainer_pool_submit_many(ga3c_trainer_pool* p, int n_batches, const int32_t* batch_off,
+                                  const int32_t* seg_base, const int32_t* agents, const int32_t* state_slots,
+                                  const int32_t* actions, const double* rewards, const int32_t* seg_offsets,
+                                  const uint8_t* terminal, const double* bootstrap, double gamma) {
+  if (!p || n_batches < 0 || (n_batches > 0 && (!batch_off || !seg_base || !seg_offsets))) return GA3C_INVALID_ARGUMENT;
+  for (int i = 0; i < n_batches; ++i) {
+    const int b0 = batch_off[i], s0 = seg_base[i];
+    const int st = ga3c_trainer_pool_submit(p, agents + b0, state_slots + b0, batch_off[i + 1] - b0, actions + b0,
+                                            rewards + b0, seg_offsets + s0 + i, seg_base[i + 1] - s0, terminal + s0,
+                                            bootstrap + s0, gamma);
+    if (st != GA3C_OK) return st;
+  }
+  return GA3C_OK;
+}
+
 int ga3c_trainer_pool_wait(ga3c_trainer_pool* p, long long* updates, long long* rejected) {
   if (!p) return GA3C_INVALID_ARGUMENT;
   std::unique_lock<std::mutex> lk(p->mu);
