@@ -128,7 +128,7 @@ struct ga3c_ctx {
   cudaEvent_t evs[16] = {};
   int ev_next = 0;
   int max_batch = 0;
-  int sms = 0;  // SMs a split-K plan fills (0 = GA3C_SPLIT_SMS or all)
+  int sms = 0;  // SMs a split-K plan fills (ga3c_ctx_set_sm_budget; 0 = all)
   void* d_in = nullptr;
   float* act[GA3C_MAX_CONV + GA3C_MAX_HIDDEN] = {};
   float* dout[GA3C_MAX_CONV + GA3C_MAX_HIDDEN] = {};  // per-layer output gradient (backward DAG)
