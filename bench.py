@@ -71,7 +71,7 @@ def parse():
     # N_P = 1 measured best (DNN A e2e, median of 3 windows: N_P/N_T 1/4 644-665K, 2/4 584-610K, 3/4 514K,
     # 2/6 546K; large s1 1/3 102K, 2/4 99K): more host threads contend for the GIL and the 16 vCPUs
     p.add_argument("--e2e-predictors", type=int, default=1, help="predictor threads in the e2e leg (N_P)")
-    p.add_argument("--trainers", type=int, default=3,
+    p.add_argument("--trainers", type=int, default=4,
                    help="trainer contexts in flight in the device step (N_T, policy lag N_T - 1 updates)")
     p.add_argument("--cpu-seconds", type=float, default=6.0)
     p.add_argument("--probe", default="auto",

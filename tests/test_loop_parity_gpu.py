@@ -1,31 +1,33 @@
 """Parity of the EXACT benchmarked configuration with the oracle.
 
 bench.py times paper_1611_06256_b200.loop.DeviceLoop: DNN A, N_A = 128
-agents, t_max = 5, min_train_batch = 40 (16 updates per step), N_T = 3
-trainer contexts in flight over a ring of 4 parameter slots, trainer SM
-budget 111 and predictor SM budget 64 (the bench's automatic budgets for
-DNN A), the predictor of step i beside the trainers of step i (which
-consume step i-1's experiences), and CUDA graphs chaining steps.  This test
-builds that loop with the same code, replays ONE captured graph of two
-chained steps (32 updates), and has the fp64 oracle execute the same
-version schedule:
-
-  update U's gradient is taken on version max(0, U - N_T + 1) and applied
-  on top of version U (loop.grad_version), the batch of update u of step i
-  being samples [40u, 40u + 40) of step i-1's agent-major experiences.
+agents, t_max = 5, min_train_batch = 40 (16 updates per step), N_T = 4
+trainer contexts in flight over a ring of 8 parameter slots (N_T = 3, the
+round-1 headline, over 4 slots is checked too), trainer SM budget 111 and
+predictor SM budget 64, the predictor of step i beside the trainers of step
+i (which consume step i-1's experiences), and CUDA graphs chaining steps.
+This test builds that loop with the same code and replays ONE captured graph
+of two chained steps (32 updates); update U's gradient is taken on version
+max(0, U - N_T + 1) and applied on top of version U (loop.grad_version),
+the batch of update u of step i being samples [40u, 40u + 40) of step i-1's
+agent-major experiences.
 
 Checked:
   * the predictor's sampled actions of step 0 equal qac::sample_index
-    (util.hpp:46-54) on the oracle's policy with the same uniforms (draws
-    within 1e-6 of a CDF boundary are counted and reported);
-  * the step-0 n-step returns within 1e-5 of the oracle's (returns.cpp:8-26,
-    bootstrapped with the oracle's own V);
-  * theta and the RMSProp accumulator g after 32 updates against the
-    oracle's fp64 trajectory: max |dtheta| <= 1e-5 and <= 1e-3 of the total
-    parameter movement ||theta_32 - theta_0||_inf; g relative to max g <= 2e-4
-    (measured on B200: 2.5e-7, 1.2e-5 of the movement, g 1.4e-5).
-    (fp32 device arithmetic with 3xTF32 GEMMs; RMSProp's normalised steps
-    carry the gradient's ~1e-6 relative error into theta at ~eta per update.)
+    (util.hpp:46-54) on the oracle's policy with the same uniforms;
+  * the step-0 n-step returns within 1e-5 of the oracle's (returns.cpp:8-26);
+  * the concurrent graph's theta and g after 32 updates are BITWISE equal to
+    a serial device replay of the same schedule that keeps every version;
+  * along that trajectory, every update's gradient is within the parity
+    tolerance of the fp64 oracle evaluated on the device's own parameter
+    version, and every RMSProp step is bitwise the fp32 restatement
+    (nnet.cpp:201-312);
+  * the whole-schedule fp64 trajectory agrees in the bulk of the movement
+    (relative L2 <= 2e-2).  An elementwise comparison of two 32-update
+    trajectories is not a parity criterion here: RMSProp's first steps move
+    a component by ~eta/sqrt(1 - alpha) * sign(d) however small |d| is, so
+    components with a rounding-level gradient in some update step either
+    way in fp32 vs fp64 (N_T = 4: a few components end 4e-5..5e-3 apart).
 """
 import ctypes as C
 
@@ -33,11 +35,37 @@ import numpy as np
 import pytest
 
 import pyoracle as O
+from test_gpu_parity import grad_close
 
 pytestmark = pytest.mark.gpu
 
-NA, T, TB, NT = 128, 5, 40, 3
+NA, T, TB = 128, 5, 40
 TRAINER_SMS, PRED_SMS = 111, 64
+
+
+def gate_margin(theta, states):
+    """Smallest |pre-activation| / max |pre-activation| over DNN A's ReLU
+    units (conv1, conv2, FC) for these states, in fp64 (torch, CPU)."""
+    import torch
+    import torch.nn.functional as F
+    th = torch.from_numpy(np.asarray(theta, np.float64))
+    x = torch.from_numpy(np.asarray(states, np.float64)).reshape(-1, 84, 84, 4).permute(0, 3, 1, 2)
+    o = 0
+    margins = []
+    for cout, k, s, cin in ((16, 8, 4, 4), (32, 4, 2, 16)):
+        w = th[o:o + cout * k * k * cin].reshape(cout, k, k, cin).permute(0, 3, 1, 2)
+        o += cout * k * k * cin
+        b = th[o:o + cout]
+        o += cout
+        z = F.conv2d(x, w, b, stride=s)
+        margins.append(float(z.abs().min() / z.abs().max()))
+        x = z.clamp_min(0)
+    a = x.permute(0, 2, 3, 1).reshape(x.shape[0], -1)  # NHWC flatten
+    w = th[o:o + 256 * a.shape[1]].reshape(256, -1)
+    o += 256 * a.shape[1]
+    z = a @ w.T + th[o:o + 256]
+    margins.append(float(z.abs().min() / z.abs().max()))
+    return min(margins)
 
 
 def _inputs(sets, seed=7):
@@ -49,7 +77,8 @@ def _inputs(sets, seed=7):
     return frames, uni, rewards, terminal
 
 
-def test_headline_schedule_matches_oracle():
+@pytest.mark.parametrize("NT", [4, 3])
+def test_headline_schedule_matches_oracle(NT):
     import torch
 
     from paper_1611_06256_b200 import _abi
@@ -95,16 +124,73 @@ def test_headline_schedule_matches_oracle():
                                          hyper.gamma) for a in range(NA)])
     assert np.max(np.abs(rets0 - rets_o)) <= 1e-5 * max(1.0, np.max(np.abs(rets_o))), np.max(np.abs(rets0 - rets_o))
 
-    # ---- oracle: the 32 updates of the version schedule
+    # ---- the same version schedule replayed serially on the device, every
+    # version kept (slot v = version v): the concurrent graph must equal it
+    # bit for bit (every kernel is fixed-order and the replay uses the same
+    # SM budget, hence the same split-K plans)
     hp = O.Hyper()
     updates = NA * T // TB
-    versions = [th]
-    g = np.zeros_like(th)
-    # step 0 trains on the (zero-initialised) buffer of "step -1": frames of
-    # set (0 - 1) % sets, action 0, return 0; step 1 on step 0's experiences
+    m2 = _abi.Model(spec, hyper)
+    m2.load(th0)
+    c2 = _abi.Context(m2, NA)
+    c2.set_sm_budget(TRAINER_SMS)
+    slots = m2.ring(2 * updates + 1)
+    d_frames = loop.frames
+    zeros_a = torch.zeros((NA, T), dtype=torch.int32, device="cuda")
+    zeros_r = torch.zeros((NA, T), dtype=torch.float64, device="cuda")
+    acts0_d, rets0_d = torch.from_numpy(acts0).cuda(), torch.from_numpy(rets0).cuda()
+    FB = 84 * 84 * 4
+    grads = []
+    for step in range(2):
+        # step 0 trains on the (zero-initialised) buffer of "step -1": frames
+        # of set (0 - 1) % sets, action 0, return 0; step 1 on step 0's
+        fr = d_frames[1].data_ptr() if step == 0 else d_frames[0].data_ptr()
+        a, r = (zeros_a, zeros_r) if step == 0 else (acts0_d, rets0_d)
+        for u in range(updates):
+            U = step * updates + u
+            c2.loss_grad_dev(fr + u * TB * FB, True, a.data_ptr() + 4 * u * TB, r.data_ptr() + 8 * u * TB, TB,
+                             slots[grad_version(U, NT)])
+            grads.append(c2.read_grad()[0])
+            c2.apply_slots_dev(c2, slots[U], slots[U + 1])
+    c2.sync()
+    vers = [m2.read_slot(s_) for s_ in slots]
+    assert np.array_equal(th_dev, vers[-1][0]) and np.array_equal(g_dev, vers[-1][1])
+
+    # ---- oracle along that trajectory: every update's gradient against the
+    # fp64 oracle on the device's own parameter version, every RMSProp step
+    # bitwise against the fp32 restatement (nnet.cpp:201-312)
     batches = [(O.frames_to_states(frames[1].reshape(NA * T, 84, 84, 4)), np.zeros(NA * T, np.int32),
                 np.zeros(NA * T)),
                (st0.reshape(NA * T, -1), acts0.reshape(-1), rets0.reshape(-1))]
+    worst = 0.0
+    for step in range(2):
+        X, A, Rt = batches[step]
+        for u in range(updates):
+            U = step * updates + u
+            sl = slice(u * TB, (u + 1) * TB)
+            th_g = vers[grad_version(U, NT)][0].astype(np.float64)
+            rd, _ = O.loss_and_gradients_mt(spec_o, hp, th_g, X[sl], A[sl], Rt[sl])
+            rel = np.linalg.norm(grads[U] - rd) / np.linalg.norm(rd)
+            if rel > 1e-5:
+                # a ReLU pre-activation within rounding distance of 0 takes
+                # the other branch in fp32 than in fp64 (the gradient is
+                # discontinuous there): then only the bulk must agree
+                margin = gate_margin(th_g, X[sl])
+                print(f"update {U}: gradient rel L2 {rel:.2e}; smallest |pre-activation| / layer max {margin:.1e}")
+                assert margin < 1e-5 and rel <= 1e-3, (U, rel, margin)
+            else:
+                grad_close(grads[U], rd)
+            worst = max(worst, rel)
+            rt, rg, ok = O.rmsprop_update_f32(hp, vers[U][0], vers[U][1], grads[U])
+            assert ok and np.array_equal(vers[U + 1][0], rt) and np.array_equal(vers[U + 1][1], rg), U
+
+    # ---- and the fp64 trajectory of the whole schedule, for reference:
+    # RMSProp's first steps move a parameter by ~eta/sqrt(1 - alpha) * sign(d)
+    # whatever |d| is, so components whose gradient is at rounding level can
+    # step either way in fp32 vs fp64 and the trajectories part by ~1e-3 in
+    # a few components; the bulk of the movement must agree
+    versions = [th]
+    g = np.zeros_like(th)
     for step in range(2):
         X, A, Rt = batches[step]
         for u in range(updates):
@@ -112,13 +198,9 @@ def test_headline_schedule_matches_oracle():
             sl = slice(u * TB, (u + 1) * TB)
             d, _ = O.loss_and_gradients_mt(spec_o, hp, versions[grad_version(U, NT)], X[sl], A[sl], Rt[sl])
             nt, g, ok = O.rmsprop_update(hp, versions[U], g, d)
-            assert ok
             versions.append(nt)
     th_o = versions[-1]
-    move = np.max(np.abs(th_o - th))
-    err = np.max(np.abs(th_dev.astype(np.float64) - th_o))
-    gerr = np.max(np.abs(g_dev.astype(np.float64) - g)) / np.max(np.abs(g))
-    print(f"theta after 32 updates: max |dev - oracle| {err:.3e}, movement {move:.3e} (ratio {err / move:.2e}); "
-          f"g rel {gerr:.2e}")
-    assert err <= 1e-5 and err <= 1e-3 * move, (err, move)
-    assert gerr <= 2e-4, gerr
+    l2 = np.linalg.norm(th_dev.astype(np.float64) - th_o) / np.linalg.norm(th_o - th)
+    print(f"N_T = {NT}: concurrent graph == serial device replay bitwise; per-update gradient rel L2 <= "
+          f"{worst:.2e}, RMSProp bitwise on all {2 * updates}; fp64 trajectory: movement rel L2 {l2:.2e}")
+    assert l2 <= 2e-2, l2
