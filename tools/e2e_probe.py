@@ -83,6 +83,25 @@ def main():
         print(f"{nt} trainer threads: {1e6 * dt / n_upd:.1f} us per update (16 updates = {16e3 * dt / n_upd:.3f} ms)")
         for c in cs:
             c.close()
+    # the native trainer pool (ga3c_trainer_pool_submit_many): 160 updates
+    for nt in (1, 2, 4, 6, 8):
+        for sms in (111, 0):
+            pool = _abi.TrainerPool(model, store, nt, NA, sms, queue_cap=64)
+            n_upd = 160
+            b_off = np.arange(0, TB * n_upd + 1, TB, dtype=np.int32)
+            s_base = np.arange(0, per * n_upd + 1, per, dtype=np.int32)
+            pool.submit_many(b_off[:17], s_base[:17], np.tile(ag, 16), np.tile(sl, 16), np.tile(acts, 16),
+                             np.tile(rew, 16), np.tile(seg, 16), np.tile(term, 16), np.tile(boot, 16), 0.99)
+            pool.wait()
+            t0 = time.perf_counter()
+            pool.submit_many(b_off, s_base, np.tile(ag, n_upd), np.tile(sl, n_upd), np.tile(acts, n_upd),
+                             np.tile(rew, n_upd), np.tile(seg, n_upd), np.tile(term, n_upd), np.tile(boot, n_upd),
+                             0.99)
+            pool.wait()
+            dt = time.perf_counter() - t0
+            print(f"native pool, {nt} threads, sms {sms}: {1e6 * dt / n_upd:.1f} us per update "
+                  f"(16 updates = {16e3 * dt / n_upd:.3f} ms)", flush=True)
+            pool.close()
     # raw C call overhead: an empty predict (n = 0)
     print(f"predict_frames(0): {timeit(lambda: _abi.predict_frames(ctx, store, newf[:0], agents[:0], None)):.1f} us")
 

@@ -43,6 +43,28 @@ def train_flops(net):
     return f + 3 * 2.0 * heads["K"] * heads["N"]
 
 
+def issued_ceiling(net, kind, tc):
+    """Algorithmic TFLOP/s ceiling at the precisions the kernels issue
+    (bench.issued: conv1 forward = 4 exact int8 digit MMAs, the u8-input
+    weight gradient 2 tf32 MMAs, every other GEMM 3xTF32) against the
+    measured dense peaks (profiles/r2_tc_peaks.json): total FLOPs / sum of
+    each GEMM's issued-MMA time.  The heads (SIMT, < 0.1% of the FLOPs) are
+    left out."""
+    layers, _ = bench.layer_geometry(net)
+    peak = {"tf32": tc.get("tf32_tflops", 1117.2), "i8": tc.get("i8_tops", 4595.6)}
+    flops = t = 0.0
+    passes = [("conv_fwd" if l["kind"] == "conv" else "fc_fwd", li) for li, l in enumerate(layers)]
+    if kind == "train":
+        passes += [("wgrad", li) for li in range(len(layers))] + [("dgrad", li) for li in range(1, len(layers))]
+    for tag, li in passes:
+        l = layers[li]
+        f = 2.0 * l["K"] * l["N"] * l["P"]
+        prec, factor = bench.issued((tag, li))
+        flops += f
+        t += f * factor / (peak[prec] * 1e12)
+    return flops / t / 1e12
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--nets", default="dnn_a,large1")
@@ -53,6 +75,7 @@ def main():
     import torch
     from paper_1611_06256_b200 import _abi
     hbm, bf16, _, src = bench.measured_peaks()
+    tc = bench.tc_peaks()
     rows = []
     for net in a.nets.split(","):
         spec = spec_of(_abi, net)
@@ -103,6 +126,9 @@ def main():
                    "peak_tflops": bf16, "peak_source": src}
             row["predict_frac"] = row["predict_tflops"] / bf16
             row["train_frac"] = row["train_tflops"] / bf16
+            for k in ("predict", "train"):
+                row[f"{k}_issued_ceiling_tflops"] = issued_ceiling(net, k, tc)
+                row[f"{k}_frac_issued"] = row[f"{k}_tflops"] / row[f"{k}_issued_ceiling_tflops"]
             print(json.dumps(row), flush=True)
             rows.append(row)
             del fr
@@ -111,13 +137,18 @@ def main():
         model.close()
     if a.md:
         with open(a.md, "w") as f:
-            f.write(f"# Batch-size sweep (tools/sweep.py), peak = {bf16} TFLOP/s bf16 ({src})\n\n")
-            f.write("| net | B | predict us | predictions/s | TFLOP/s | frac | train us | samples/s | TFLOP/s | frac |\n")
-            f.write("|---|---|---|---|---|---|---|---|---|---|\n")
+            f.write(f"# Batch-size sweep (tools/sweep.py), bf16 peak = {bf16} TFLOP/s ({src})\n\n")
+            f.write("frac = achieved / bf16 peak; frac_issued = achieved / the ceiling at the precisions the "
+                    "kernels issue (3xTF32 GEMMs, exact int8-digit conv1 forward) from the measured tf32 / i8 "
+                    f"peaks ({tc.get('tf32_tflops')} / {tc.get('i8_tops')} T/s, profiles/r2_tc_peaks.json)\n\n")
+            f.write("| net | B | predict us | predictions/s | TFLOP/s | frac | frac_issued | train us | samples/s | "
+                    "TFLOP/s | frac | frac_issued |\n")
+            f.write("|---|---|---|---|---|---|---|---|---|---|---|---|\n")
             for r in rows:
                 f.write(f"| {r['net']} | {r['B']} | {r['predict_us']:.1f} | {r['predict_samples_per_s']:.0f} | "
-                        f"{r['predict_tflops']:.2f} | {r['predict_frac']:.4f} | {r['train_us']:.1f} | "
-                        f"{r['train_samples_per_s']:.0f} | {r['train_tflops']:.2f} | {r['train_frac']:.4f} |\n")
+                        f"{r['predict_tflops']:.2f} | {r['predict_frac']:.4f} | {r['predict_frac_issued']:.3f} | "
+                        f"{r['train_us']:.1f} | {r['train_samples_per_s']:.0f} | {r['train_tflops']:.2f} | "
+                        f"{r['train_frac']:.4f} | {r['train_frac_issued']:.3f} |\n")
 
 
 if __name__ == "__main__":
