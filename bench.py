@@ -71,6 +71,8 @@ def parse():
     # N_P = 1 measured best (DNN A e2e, median of 3 windows: N_P/N_T 1/4 644-665K, 2/4 584-610K, 3/4 514K,
     # 2/6 546K; large s1 1/3 102K, 2/4 99K): more host threads contend for the GIL and the 16 vCPUs
     p.add_argument("--e2e-predictors", type=int, default=1, help="predictor threads in the e2e leg (N_P)")
+    p.add_argument("--e2e-groups", type=int, default=2,
+                   help="agent groups one predictor thread keeps in flight (asynchronous predictions)")
     p.add_argument("--trainers", type=int, default=4,
                    help="trainer contexts in flight in the device step (N_T, policy lag N_T - 1 updates)")
     p.add_argument("--cpu-seconds", type=float, default=6.0)
@@ -926,12 +928,39 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
             acts[gs, t] = sample_rows(pi, u_h[s, t][gs])
         vout[gs] = v
 
+    # one predictor thread serving G agent groups on G contexts with
+    # asynchronous predictions (ga3c_predict_frames64_async / _collect64): a
+    # group's next batch is enqueued as soon as its actions are sampled, so
+    # the GPU works on one group while the host samples another
+    NG = max(1, args.e2e_groups)
+    agroups = [slice(a0, a1) for a0, a1 in (shard(NA, g, NG) for g in range(NG))]
+    ctx_g = [ctx] + [_abi.Context(model, NA) for _ in range(NG - 1)]
+
+    def predict_groups_async(s, pt, acts, slots, vout):
+        def submit(g, t):
+            gs = agroups[g]
+            slots[gs, t] = _abi.predict_frames_async(ctx_g[g], store, newf[s][t][gs], agents[gs],
+                                                     pt[gs] if t == 0 else None)
+        for g in range(NG):
+            submit(g, 0)
+        for t in range(T):
+            for g in range(NG):
+                gs = agroups[g]
+                pi, v, _ = _abi.predict_collect(ctx_g[g])
+                acts[gs, t] = sample_rows(pi, u_h[s, t][gs])
+                if t + 1 < T:
+                    submit(g, t + 1)
+                else:
+                    vout[gs] = v
+
     def predict_step(i, pt):
         s = i % hs
         acts = np.zeros((NA, T), np.int32)
         slots = np.zeros((NA, T), np.int32)
         v = np.zeros(NA, np.float64)
-        if NP == 1:  # the main thread is the predictor: no hand-off
+        if NP == 1 and NG > 1:
+            predict_groups_async(s, pt, acts, slots, v)
+        elif NP == 1:  # the main thread is the predictor: no hand-off
             predict_group(0, s, pt, acts, slots, v)
         else:
             for f in [pool.submit(predict_group, g, s, pt, acts, slots, v) for g in range(NP)]:
@@ -963,8 +992,9 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
         dt_thr = wins[len(wins) // 2]
         win_vals = [round(n * k / w) for w in wins]
         if dt_thr < dt:
-            dt, mode = dt_thr, (f"{NP} predictor thread(s) + native trainer pool of {args.e2e_trainers} "
-                                f"(ga3c_trainer_pool)")
+            dt, mode = dt_thr, (f"{NP} predictor thread(s)"
+                                + (f" x {NG} agent groups in flight" if NP == 1 and NG > 1 else "")
+                                + f" + native trainer pool of {args.e2e_trainers} (ga3c_trainer_pool)")
         pool_t.close()
     store.close()
     out = {"value": world * n * k / dt, "unit": "samples/s", "h2d_bytes_per_step": h2d,

@@ -339,6 +339,17 @@ int ga3c_predict_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* ne
 int ga3c_predict_frames64(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* new_frames,
                           const int32_t* agents, const uint8_t* resets, int n, int32_t* state_slots, double* pi,
                           double* v, uint64_t* version_used);
+/* The same split in two: _async pushes the frames and enqueues the forward
+ * and the copies of pi / V into the context's pinned stage, then returns
+ * (state_slots are filled at once); ga3c_predict_collect64 waits for them
+ * and copies them out.  One prediction may be in flight per context, and
+ * until it is collected the context takes no other host-buffer call; the
+ * caller keeps new_frames unchanged until then (page-locked frames are
+ * copied asynchronously).  A predictor thread can so keep two contexts'
+ * batches in flight (e.g. two agent groups). */
+int ga3c_predict_frames64_async(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* new_frames,
+                                const int32_t* agents, const uint8_t* resets, int n, int32_t* state_slots);
+int ga3c_predict_collect64(ga3c_ctx* c, double* pi, double* v, uint64_t* version_used);
 /* Trainer call: as ga3c_loss_grad_segments_u8, with sample b's state read
  * from the store at (agents[b], state_slots[b]) on the device. */
 int ga3c_train_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const int32_t* agents,

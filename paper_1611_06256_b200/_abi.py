@@ -169,6 +169,8 @@ _SIGS = {
     "ga3c_frames_create": (_P, [_P, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "ga3c_frames_destroy": (None, [_P]),
     "ga3c_host_alloc": (_P, [C.c_size_t, C.POINTER(C.c_int)]),
+    "ga3c_predict_frames64_async": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_int, _P]),
+    "ga3c_predict_collect64": (C.c_int, [_P, _P, _P, C.POINTER(C.c_uint64)]),
     "ga3c_host_free": (None, [_P]),
     "ga3c_trainer_pool_create": (_P, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "ga3c_trainer_pool_submit": (C.c_int, [_P, _P, _P, C.c_int, _P, _P, _P, C.c_int, _P, _P, C.c_double]),
@@ -558,6 +560,34 @@ def predict_frames(ctx: "Context", frames: Frames, new_frames, agents, resets=No
                                   None if rs is None else rs.ctypes.data, n, slots.ctypes.data, pi.ctypes.data,
                                   v.ctypes.data, C.byref(ver)), ctx.model.error())
     return pi, v, slots, ver.value
+
+
+def predict_frames_async(ctx: "Context", frames: Frames, new_frames, agents, resets=None, slot=-1):
+    """Enqueue a frame-store prediction (ga3c_predict_frames64_async) -> state_slots;
+    predict_collect(ctx) returns (pi fp64 [n][A], v [n], version).  Keep
+    new_frames alive and unchanged until collected."""
+    import numpy as np
+    nf = np.ascontiguousarray(new_frames, np.uint8)
+    ag = np.ascontiguousarray(agents, np.int32)
+    n = len(ag)
+    rs = None if resets is None else np.ascontiguousarray(resets, np.uint8)
+    slots = np.empty(n, np.int32)
+    check(lib.ga3c_predict_frames64_async(ctx.h, slot, frames.h, nf.ctypes.data, ag.ctypes.data,
+                                          None if rs is None else rs.ctypes.data, n, slots.ctypes.data),
+          ctx.model.error())
+    ctx._pending = (n, nf, ag, rs)  # the buffers stay referenced until collected
+    return slots
+
+
+def predict_collect(ctx: "Context"):
+    import numpy as np
+    n = ctx._pending[0]
+    pi = np.empty((n, ctx.model.n_actions), np.float64)
+    v = np.empty(n, np.float64)
+    ver = C.c_uint64(0)
+    check(lib.ga3c_predict_collect64(ctx.h, pi.ctypes.data, v.ctypes.data, C.byref(ver)), ctx.model.error())
+    ctx._pending = None
+    return pi, v, ver.value
 
 
 def train_frames(ctx: "Context", frames: Frames, agents, state_slots, actions, rewards, seg_offsets, terminal,

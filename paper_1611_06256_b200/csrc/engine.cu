@@ -25,7 +25,9 @@
 #include <cstring>
 #include <cstdlib>
 #include <functional>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -175,8 +177,30 @@ struct ga3c_ctx {
   std::vector<cudaEvent_t> events;
   std::size_t ev_used = 0;
   std::vector<int> ev_meta;  // per bracketed launch: tag | layer << 8 | stream << 16
+  // an asynchronous frame-store prediction in flight (ga3c_predict_frames64_async):
+  // its outputs land in the pinned stage, the snapshot stays pinned until collected
+  struct {
+    bool active = false;
+    const double* h_pi = nullptr;
+    const double* h_v = nullptr;
+    int n = 0, A = 0, slot = -1;
+    bool pinned = false;
+    std::uint64_t ver = 0;
+    cudaEvent_t ev = nullptr;
+  } pend;
   // captured CUDA graphs of device-resident step sequences
   std::vector<cudaGraphExec_t> graphs;
+  // ga3c_train_frames' device work (stage upload -> gather -> returns ->
+  // loss/backward -> result download) captured once per (slot, B, segments,
+  // outputs) and replayed: one launch per call instead of ~20 API calls
+  struct TfKey {
+    int slot, B, n_seg, flags;
+    const void* ring;
+    bool operator<(const TfKey& o) const {
+      return std::tie(slot, B, n_seg, flags, ring) < std::tie(o.slot, o.B, o.n_seg, o.flags, o.ring);
+    }
+  };
+  std::map<TfKey, cudaGraphExec_t> tf_graphs;
   bool capturing = false;
 };
 
@@ -1543,9 +1567,15 @@ void ga3c_ctx_destroy(ga3c_ctx* c) {
   for (auto e : c->evs)
     if (e) cudaEventDestroy(e);
   if (c->h_flag) cudaFreeHost(c->h_flag);
+  if (c->pend.active) {
+    cudaEventSynchronize(c->pend.ev);
+    if (c->pend.pinned) ga3c_snapshot_release(c->m, c->pend.slot);
+  }
+  if (c->pend.ev) cudaEventDestroy(c->pend.ev);
   if (c->h_stage) cudaFreeHost(c->h_stage);
   for (auto e : c->events) cudaEventDestroy(e);
   for (auto g : c->graphs) cudaGraphExecDestroy(g);
+  for (auto& kv : c->tf_graphs) cudaGraphExecDestroy(kv.second);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -2299,9 +2329,10 @@ static int loss_grad_segments(ga3c_ctx* c, int slot, const void* states, bool u8
                               const int32_t* actions, const double* rewards, const int32_t* off,
                               int n_seg, const uint8_t* terminal, const double* bootstrap, double gamma,
                               int apply_clip, double* scalars, double* returns_out, bool dev_ready = false,
-                              Stager* sg_in = nullptr, const std::function<void()>& after_flush = {}) {
+                              Stager* sg_in = nullptr, const std::function<void()>& after_flush = {},
+                              const void* after_flush_key = nullptr) {
   if (!c || B < 1 || B > c->max_batch || (!states && !dev_ready) || !actions || !rewards || !off || n_seg < 1 ||
-      !terminal || !bootstrap)
+      !terminal || !bootstrap || c->pend.active)  // the stage holds an uncollected prediction
     return GA3C_INVALID_ARGUMENT;
   ga3c_model* m = c->m;
   auto set_err = [&](const std::string& e) { m->set_error(e); };
@@ -2356,26 +2387,56 @@ static int loss_grad_segments(ga3c_ctx* c, int slot, const void* states, bool u8
     set_err("loss_grad_segments: batch exceeds the context's staging area");
     return GA3C_INVALID_ARGUMENT;
   }
-  if ((!dev_ready && cudaMemcpyAsync(c->d_in, states, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess) ||
-      !sg.flush())
-    rc = GA3C_CUDA_ERROR;
-  if (!rc) {
+  // the whole device sequence, issued eagerly or captured (see tf_graphs)
+  auto issue = [&]() -> bool {
+    if ((!dev_ready && cudaMemcpyAsync(c->d_in, states, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess) ||
+        !sg.flush())
+      return false;
     if (after_flush) after_flush();
     {
       Launch l(c, GA3C_K_RETURNS, -1);
       pdl_launch(c->cur, returns_kernel, dim3((n_seg + 127) / 128), dim3(128), 0, d_rew, d_off, n_seg, d_term,
                  d_boot, gamma, c->d_rets);
     }
-    wait_slot(c, s);
     run_loss_grad(c, m->slots[s].theta, c->d_in, u8, d_act, c->d_rets, B, apply_clip != 0);
-    if (cudaMemcpyAsync(h_flg, c->flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
-      rc = GA3C_CUDA_ERROR;
-    if (!rc && scalars &&
+    if (cudaMemcpyAsync(h_flg, c->flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) return false;
+    if (scalars &&
         cudaMemcpyAsync(h_scal, c->scal_sum, sizeof(double) * 3, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
-      rc = GA3C_CUDA_ERROR;
-    if (!rc && returns_out &&
+      return false;
+    if (returns_out &&
         cudaMemcpyAsync(h_ret, c->d_rets, sizeof(double) * B, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
-      rc = GA3C_CUDA_ERROR;
+      return false;
+    return true;
+  };
+  if (dev_ready && sg_in && !c->capturing && c->timed_tag == 0) {
+    // frame-store call: replay the captured sequence of this shape and slot
+    // (every pointer it bakes -- stage, workspace, theta of the slot, ring --
+    // is fixed for the key; the host wrote this call's inputs into the
+    // pinned stage at the same offsets above)
+    const ga3c_ctx::TfKey key{s, B, n_seg, (scalars ? 1 : 0) | (returns_out ? 2 : 0) | (apply_clip ? 4 : 0),
+                              after_flush_key};
+    auto it = c->tf_graphs.find(key);
+    if (it == c->tf_graphs.end()) {
+      cudaGraph_t g = nullptr;
+      cudaGraphExec_t ex = nullptr;
+      bool ok = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      const bool issued = ok && issue();
+      ok = cudaStreamEndCapture(c->stream, &g) == cudaSuccess && issued && g &&
+           cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
+      if (g) cudaGraphDestroy(g);
+      if (!ok) {
+        cudaGetLastError();
+        if (pinned_here) ga3c_snapshot_release(m, s);
+        set_err("loss_grad_segments: graph capture failed");
+        return GA3C_CUDA_ERROR;
+      }
+      it = c->tf_graphs.emplace(key, ex).first;
+    }
+    wait_slot(c, s);
+    if (cudaGraphLaunch(it->second, c->stream) != cudaSuccess) rc = GA3C_CUDA_ERROR;
+  } else {
+    wait_slot(c, s);
+    if (!issue()) rc = GA3C_CUDA_ERROR;
   }
   cudaError_t e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) {
@@ -2412,9 +2473,10 @@ int ga3c_loss_grad_segments_u8(ga3c_ctx* c, int slot, const uint8_t* frames, int
 template <typename OutT>
 static int predict_frames_impl(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* new_frames,
                                const int32_t* agents, const uint8_t* resets, int n, int32_t* state_slots, OutT* pi,
-                               OutT* v, uint64_t* version_used) {
+                               OutT* v, uint64_t* version_used, bool async = false) {
   constexpr bool f64 = std::is_same<OutT, double>::value;
-  if (!c || !f || f->m != c->m || n < 0 || n > c->max_batch || (n > 0 && (!new_frames || !agents || !pi || !v)))
+  if (!c || !f || f->m != c->m || n < 0 || n > c->max_batch ||
+      (n > 0 && (!new_frames || !agents || (!async && (!pi || !v)))) || c->pend.active)
     return GA3C_INVALID_ARGUMENT;
   ga3c_model* m = c->m;
   auto set_err = [&](const std::string& e) { m->set_error(e); };
@@ -2477,6 +2539,23 @@ static int predict_frames_impl(ga3c_ctx* c, int slot, ga3c_frames* f, const uint
           cudaMemcpyAsync(h_v, d_v, sizeof(OutT) * n, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
         rc = GA3C_CUDA_ERROR;
     }
+    if (async && !rc) {
+      // outputs stay in the pinned stage until ga3c_predict_collect64
+      if (!c->pend.ev && cudaEventCreateWithFlags(&c->pend.ev, cudaEventDisableTiming) != cudaSuccess)
+        rc = GA3C_CUDA_ERROR;
+      if (!rc && cudaEventRecord(c->pend.ev, c->stream) != cudaSuccess) rc = GA3C_CUDA_ERROR;
+      if (!rc) {
+        c->pend.active = true;
+        c->pend.h_pi = reinterpret_cast<const double*>(h_pi);
+        c->pend.h_v = reinterpret_cast<const double*>(h_v);
+        c->pend.n = n;
+        c->pend.A = A;
+        c->pend.slot = s;
+        c->pend.pinned = pinned_here;
+        c->pend.ver = ver;
+        return GA3C_OK;
+      }
+    }
     cudaError_t e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) {
       rc = GA3C_CUDA_ERROR;
@@ -2506,6 +2585,30 @@ int ga3c_predict_frames64(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* 
   return predict_frames_impl(c, slot, f, new_frames, agents, resets, n, state_slots, pi, v, version_used);
 }
 
+int ga3c_predict_frames64_async(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* new_frames,
+                                const int32_t* agents, const uint8_t* resets, int n, int32_t* state_slots) {
+  if (n < 1) return GA3C_INVALID_ARGUMENT;
+  return predict_frames_impl<double>(c, slot, f, new_frames, agents, resets, n, state_slots, nullptr, nullptr,
+                                     nullptr, true);
+}
+
+int ga3c_predict_collect64(ga3c_ctx* c, double* pi, double* v, uint64_t* version_used) {
+  if (!c || !c->pend.active || !pi || !v) return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  const cudaError_t e = cudaEventSynchronize(c->pend.ev);
+  c->pend.active = false;
+  if (c->pend.pinned) ga3c_snapshot_release(m, c->pend.slot);
+  if (e != cudaSuccess) {
+    set_err(std::string("predict_collect64: ") + cudaGetErrorString(e));
+    return GA3C_CUDA_ERROR;
+  }
+  std::memcpy(pi, c->pend.h_pi, sizeof(double) * c->pend.n * c->pend.A);
+  std::memcpy(v, c->pend.h_v, sizeof(double) * c->pend.n);
+  if (version_used) *version_used = c->pend.ver;
+  return GA3C_OK;
+}
+
 int ga3c_train_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const int32_t* agents, const int32_t* state_slots,
                       int B, const int32_t* actions, const double* rewards, const int32_t* seg_offsets, int n_seg,
                       const uint8_t* terminal, const double* bootstrap, double gamma, int apply_clip,
@@ -2530,7 +2633,8 @@ int ga3c_train_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const int32_t* agen
                                          dim3((unsigned)((f->frame_px / 4 + 255) / 256), B), dim3(256), 0,
                                          reinterpret_cast<const uint32_t*>(f->ring), f->frame_px, f->history,
                                          d_idx, B, reinterpret_cast<uint32_t*>(c->d_in));
-                            });
+                            },
+                            f->ring);
 }
 
 void* ga3c_host_alloc(size_t bytes, int* status) {
