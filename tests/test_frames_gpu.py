@@ -133,3 +133,67 @@ def test_ring_apply_rejected_step_leaves_source_in_destination():
     ctx1.apply_slots_dev(ctx1, ring[1], ring[2])  # rejected: ctx1's gradient is non-finite
     ctx1.sync()
     assert np.array_equal(theta(ring[2]), theta(ring[1]))
+
+
+def test_async_predict_matches_sync_and_guards_the_stage():
+    """ga3c_predict_frames64_async + _collect64 give the bits of
+    ga3c_predict_frames64 on an identical store; a second submit, a host
+    training call, or a collect with nothing pending are rejected."""
+    _abi, m, ctx, fr = setup(n_agents=5, history=4)
+    fr2 = _abi.Frames(m, 5, 4)
+    ctx2 = _abi.Context(m, 64)
+    rng = np.random.default_rng(3)
+    agents = np.arange(5, dtype=np.int32)
+    for step in range(3):
+        new = rng.integers(0, 256, (5, H * W), dtype=np.uint8)
+        pi, v, sl, ver = _abi.predict_frames(ctx, fr, new, agents, fp64=True)
+        sl2 = _abi.predict_frames_async(ctx2, fr2, new, agents)
+        with pytest.raises(ValueError):
+            _abi.predict_frames_async(ctx2, fr2, new, agents)  # one in flight per context
+        with pytest.raises(ValueError):
+            ctx2.loss_grad_segments(np.zeros((5, H * W * 4), np.uint8), np.zeros(5, np.int32), np.zeros(5),
+                                    [0, 5], [1], [0.0], 0.99)  # the stage is busy
+        pi2, v2, ver2 = _abi.predict_collect(ctx2)
+        assert np.array_equal(sl, sl2) and np.array_equal(pi, pi2) and np.array_equal(v, v2) and ver == ver2
+    ctx2._pending = (1,)
+    with pytest.raises(ValueError):
+        _abi.predict_collect(ctx2)
+
+
+def test_graph_replayed_training_trajectory_matches_eager_bitwise():
+    """ga3c_train_frames replays a captured graph per (snapshot slot, shape):
+    eight train + apply rounds (the latest slot moves every round, so graphs
+    are captured and then replayed) give the same parameters, bit for bit,
+    as the same rounds through ga3c_loss_grad_segments_u8 on host states
+    (eager launches) on a second model."""
+    import ctypes as C
+    _abi, m, ctx, fr = setup(n_agents=4, history=16)
+    spec = _abi.NetSpec()
+    C.memmove(C.byref(spec), C.byref(O.dnn_a()), C.sizeof(spec))
+    m2 = _abi.Model(spec, _abi.default_hyper())
+    m2.load(m.read()[0])
+    c2 = _abi.Context(m2, 64)
+    rng = np.random.default_rng(5)
+    T = 2
+    stacks = {}
+    agents = np.arange(4, dtype=np.int32)
+    for rnd in range(8):
+        slots = np.zeros((4, T), np.int32)
+        states = np.zeros((4, T, H * W * 4), np.uint8)
+        for t in range(T):
+            new = rng.integers(0, 256, (4, H, W), dtype=np.uint8)
+            _, _, sl, _ = _abi.predict_frames(ctx, fr, new.reshape(4, -1), agents)
+            slots[:, t] = sl
+            for a in range(4):
+                stacks[a] = host_stack(stacks.get(a), new[a], False)
+                states[a, t] = stacks[a].reshape(-1)
+        acts = rng.integers(0, 6, 4 * T).astype(np.int32)
+        rew = rng.standard_normal(4 * T)
+        off = np.arange(0, 4 * T + 1, T, dtype=np.int32)
+        term = np.zeros(4, np.uint8)
+        boot = rng.standard_normal(4)
+        _abi.train_frames(ctx, fr, np.repeat(agents, T), slots.reshape(-1), acts, rew, off, term, boot, 0.99)
+        assert ctx.apply_rmsprop()[0]
+        c2.loss_grad_segments(states.reshape(4 * T, -1), acts, rew, off, term, boot, 0.99)
+        assert c2.apply_rmsprop()[0]
+        assert np.array_equal(m.read()[0], m2.read()[0]), rnd
