@@ -10,12 +10,12 @@ from paper_1611_06256_b200 import qac  # noqa: E402
 
 secs = float(sys.argv[1]) if len(sys.argv) > 1 else 5.0
 grid = [  # (agents, predictors, trainers, pred_batch_max, device_frames, trainer_sms, predictor_sms)
-    (128, 2, 2, 128, True, 0, 0),
-    (128, 2, 2, 128, True, -1, -1),
-    (128, 2, 3, 128, True, -1, -1),
-    (128, 3, 3, 128, True, -1, -1),
-    (256, 4, 4, 128, True, -1, -1),
     (256, 4, 6, 128, True, -1, -1),
+    (256, 4, 8, 128, True, -1, -1),
+    (384, 4, 6, 128, True, -1, -1),
+    (384, 6, 8, 128, True, -1, -1),
+    (256, 4, 6, 128, True, 0, 0),
+    (512, 6, 8, 128, True, -1, -1),
 ]
 for (na, npred, nt, pbm, dev, tsm, psm) in grid:
     opt = qac.PipelineOptions(net=qac.dnn_a(), env=qac.frames(step_delay_us=0, episode_len=64), device_frames=dev,
