@@ -889,8 +889,8 @@ bool fc_dgrad_tc(ga3c_ctx* c, int li, const Layer& L, const float* theta, const 
                  int ldT, const float* gate, float* din, int B) {
   Seg W = dense_seg(theta + L.w_off, L.out, L.in, L.in, false);
   W.rows = L.out;
-  if (!seg_ok(W, L.out) || L.in % 32 != 0 || ldT % 4 != 0 || B > 128) return false;
-  const int bn = B <= 32 ? 32 : (B <= 64 ? 64 : 128);
+  if (!seg_ok(W, L.out) || L.in % 32 != 0 || ldT % 4 != 0) return false;
+  const int bn = B <= 32 ? 32 : (B <= 64 ? 64 : 128);  // batches above 128: grid.z = batch tiles
   // split the reduction over the layer's outputs across a cluster when the
   // row tiles alone cannot fill the SMs
   const int mtiles = (L.in + 127) / 128;
@@ -899,7 +899,7 @@ bool fc_dgrad_tc(ga3c_ctx* c, int li, const Layer& L, const float* theta, const 
   const int kc = ((chunks + ks - 1) / ks) * 32;
   ks = (L.out + kc - 1) / kc;
   WgradArgs a{W, doutT, ldT, B, L.in, L.out, kc, nullptr, GradMap{}, 0, 1, din, gate, L.in, 0};
-  dim3 grid(mtiles, ks, 1);
+  dim3 grid(mtiles, ks, (B + bn - 1) / bn);
   switch (bn) {
     case 32: wgrad_tc_launch<float, 32>(c, li, a, grid, GA3C_K_DGRAD); break;
     case 64: wgrad_tc_launch<float, 64>(c, li, a, grid, GA3C_K_DGRAD); break;
