@@ -306,18 +306,21 @@ class Engine {
         budget_(opt.stop.max_updates ? *opt.stop.max_updates : std::numeric_limits<std::int64_t>::max()) {
     for (std::size_t i = 0; i < slot_cap_; ++i) slots_.push_back(std::make_unique<ResponseSlot<PredictionResponse>>());
     if (opt_.device_frames) {
-      // Per-agent history of stacked states on the device.  An agent's
-      // states in flight are its current one, its open batch, its batches in
-      // the TrainingQueue and in trainers' groups; agents also stall (after
-      // flushing their open batch) while `history - 2` of theirs are
-      // untrained, so a slot is never rewritten before training read it.
+      // Per-agent history of stacked states on the device.  A slot holds a
+      // state until the experience made from it is trained or dropped
+      // (busy_); an agent whose next slot is still busy hands its open batch
+      // to the trainers and waits, so a slot is never rewritten before
+      // training read it.  history >= min_train_batch + 2 t_max + 4 lets a
+      // stalled agent's experiences always fill the one group in formation.
       const int t = opt_.hyper.t_max;
       const int mtb = opt_.anneal && opt_.anneal_batches ? 1024 : opt_.knobs.min_train_batch;
       hist_ = std::max(256, mtb + 2 * t + 4);
       int st = 0;
       store_ = ga3c_frames_create(shared_.handle(), static_cast<int>(slot_cap_), hist_, &st);
       if (!store_) check(st ? st : GA3C_CUDA_ERROR, shared_.handle(), "ga3c_frames_create");
-      for (std::size_t i = 0; i < slot_cap_; ++i) outstanding_.push_back(std::make_unique<std::atomic<int>>(0));
+      busy_ = std::make_unique<std::atomic<std::uint8_t>[]>(slot_cap_ * static_cast<std::size_t>(hist_));
+      for (std::size_t i = 0; i < slot_cap_ * static_cast<std::size_t>(hist_); ++i) busy_[i].store(0);
+      pushes_.assign(slot_cap_, 0);
     }
     if (opt_.capture_trajectory)
       traj_sink_ = [this](SharedModel& m) {
@@ -366,15 +369,19 @@ class Engine {
       double score = 0.0;
       double last_value = 0.0;
       std::int64_t submitted = 0;
-      std::atomic<int>* out = dev_frames ? outstanding_[id].get() : nullptr;
       while (!stop.load(std::memory_order_relaxed)) {
-        if (out && out->load(std::memory_order_acquire) >= hist_ - 2) {
-          // frame-store backpressure: hand the open batch to the trainers
-          // and wait until enough of this agent's states were trained
-          if (!batch.experiences.empty() && !flush(batch, false, last_value, stop, submitted)) break;
-          while (out->load(std::memory_order_acquire) >= hist_ - 2 && !stop.load(std::memory_order_relaxed))
-            std::this_thread::yield();
-          continue;
+        if (dev_frames) {
+          // the slot this request's frame is pushed into (only this agent
+          // pushes frames for id, pushes_ survives agent restarts)
+          std::atomic<std::uint8_t>& next = busy_[slot_of(id, pushes_[id] % hist_)];
+          if (next.load(std::memory_order_acquire)) {
+            // frame-store backpressure: hand the open batch to the trainers
+            // and wait until the experience holding the slot was trained
+            if (!batch.experiences.empty() && !flush(batch, false, last_value, stop, submitted)) break;
+            while (next.load(std::memory_order_acquire) && !stop.load(std::memory_order_relaxed))
+              std::this_thread::yield();
+            continue;
+          }
         }
         auto& slot = *slots_[id];
         const std::uint64_t ticket = slot.issue_ticket();
@@ -383,6 +390,7 @@ class Engine {
         if (!pred_q_.push(std::move(req), &stop)) break;
         auto resp = slot.take(ticket, stop);
         if (!resp) break;
+        if (dev_frames) ++pushes_[id];
         last_value = resp->value;
         const int A = static_cast<int>(resp->policy.size());
         const int action = opt_.greedy ? argmax_index(resp->policy.data(), A)
@@ -392,7 +400,7 @@ class Engine {
         batch.experiences.push_back(
             Experience{dev_frames ? Observation{} : std::move(obs), action, reward, resp->value, resp->model_version,
                        resp->state_slot});
-        if (out) out->fetch_add(1, std::memory_order_acq_rel);
+        if (dev_frames) busy_[slot_of(id, resp->state_slot)].store(1, std::memory_order_release);
         produced_.fetch_add(1, std::memory_order_relaxed);
         score += sr.reward;
         bool ok = true;
@@ -412,7 +420,7 @@ class Engine {
       }
       if (!batch.experiences.empty()) {
         dropped_.fetch_add(static_cast<std::int64_t>(batch.experiences.size()));
-        if (out) out->fetch_sub(static_cast<int>(batch.experiences.size()), std::memory_order_acq_rel);
+        release(batch);
       }
     } catch (...) {
       report_error(std::current_exception());
@@ -429,9 +437,12 @@ class Engine {
     batch.agent_id = out.agent_id;
     batch.experiences.clear();
     const auto n = static_cast<std::int64_t>(out.experiences.size());
+    std::vector<int> held;  // frame-store slots, freed again if the push fails
+    if (store_)
+      for (const auto& e : out.experiences) held.push_back(e.state_slot);
     if (!train_q_.push(std::move(out), &stop)) {
       dropped_.fetch_add(n);
-      release(batch.agent_id, n);
+      for (int sl : held) busy_[slot_of(batch.agent_id, sl)].store(0, std::memory_order_release);
       return false;
     }
     if (opt_.sync_after_submit) {
@@ -455,8 +466,32 @@ class Engine {
       std::vector<double> rew, boot;
       std::vector<std::uint8_t> term;
       while (!stop.load(std::memory_order_relaxed)) {
+        // With the frame store, one trainer at a time forms its group, so at
+        // most one group is partly filled and an agent stalled on its
+        // history (agent_main) always leaves enough experiences to fill it.
+        bool forming = false;
+        if (store_) {
+          // interruptible: a trainer being retired must not wait behind the
+          // one forming a group (that one may wait for agents that wait for
+          // predictors the annealer is restarting)
+          std::unique_lock<std::mutex> lk(group_m_);
+          group_cv_.wait(lk, [&] { return !forming_ || stop.load(std::memory_order_relaxed); });
+          if (stop.load(std::memory_order_relaxed)) break;
+          forming_ = forming = true;
+        }
+        auto done_forming = [&] {
+          if (!forming) return;
+          {
+            std::lock_guard<std::mutex> lk(group_m_);
+            forming_ = forming = false;
+          }
+          group_cv_.notify_one();
+        };
         auto first = train_q_.pop(&stop);
-        if (!first) break;
+        if (!first) {
+          done_forming();
+          break;
+        }
         std::vector<ExperienceBatch> group;
         std::int64_t total = static_cast<std::int64_t>(first->experiences.size());
         group.push_back(std::move(*first));
@@ -470,6 +505,7 @@ class Engine {
           total += static_cast<std::int64_t>(more->experiences.size());
           group.push_back(std::move(*more));
         }
+        done_forming();
         if (bail) {
           dropped_.fetch_add(total);
           for (const auto& b : group) release(b);
@@ -514,10 +550,13 @@ class Engine {
   }
 
   // An experience batch's frame-store states are free again (trained or dropped).
-  void release(int agent, std::int64_t n) {
-    if (store_) outstanding_[agent]->fetch_sub(static_cast<int>(n), std::memory_order_acq_rel);
+  void release(const ExperienceBatch& b) {
+    if (!store_) return;
+    for (const auto& e : b.experiences) busy_[slot_of(b.agent_id, e.state_slot)].store(0, std::memory_order_release);
   }
-  void release(const ExperienceBatch& b) { release(b.agent_id, static_cast<std::int64_t>(b.experiences.size())); }
+  std::size_t slot_of(int agent, int s) const {
+    return static_cast<std::size_t>(agent) * static_cast<std::size_t>(hist_) + static_cast<std::size_t>(s);
+  }
 
   void bump_gate() {
     gate_updates_.fetch_add(1, std::memory_order_relaxed);
@@ -581,6 +620,10 @@ class Engine {
   void wake_everything() {
     pred_q_.wake_all();
     train_q_.wake_all();
+    {
+      std::lock_guard<std::mutex> lk(group_m_);
+    }
+    group_cv_.notify_all();
     for (auto& s : slots_) s->wake();
     gate_cv_.notify_all();
   }
@@ -767,7 +810,11 @@ class Engine {
   SharedModel shared_;
   ga3c_frames* store_ = nullptr;  // device frame store (device_frames)
   int hist_ = 0;
-  std::vector<std::unique_ptr<std::atomic<int>>> outstanding_;  // untrained frame-store states per agent
+  std::unique_ptr<std::atomic<std::uint8_t>[]> busy_;  // [agent][slot]: holds an untrained experience's state
+  std::vector<std::uint64_t> pushes_;                  // frames pushed per agent id
+  std::mutex group_m_;                                  // one trainer forms its group at a time:
+  std::condition_variable group_cv_;                    // forming_ is set while one does
+  bool forming_ = false;
   BoundedChannel<PredictionRequest> pred_q_;
   BoundedChannel<ExperienceBatch> train_q_;
   std::vector<std::unique_ptr<ResponseSlot<PredictionResponse>>> slots_;

@@ -237,3 +237,20 @@ def test_annealer_moves_batch_knobs_in_a_running_pipeline():
         assert 1 <= k.n_agents <= 16 and 1 <= k.n_predictors <= 3 and 1 <= k.n_trainers <= 3
         assert 1 <= k.pred_batch_max <= 1024 and 1 <= k.min_train_batch <= 1024
     assert r.total_updates > 0 and np.all(np.isfinite(r.final_theta))
+
+
+def test_device_frames_backpressure_single_agent_large_batches():
+    """One agent against one trainer with min_train_batch 240 and the 256-slot
+    frame-store history: the agent outruns training, finds its next slot
+    still holding an untrained state, hands its open batch over and waits
+    (pipeline.cpp agent_main), and the run still completes with every
+    experience accounted for."""
+    qac = q()
+    env = qac.frames(episode_len=1000)
+    opt = qac.PipelineOptions(net=qac.dnn_a(), env=env, device_frames=True)
+    opt.knobs = qac.KnobConfig(n_agents=1, n_predictors=1, n_trainers=2, pred_batch_max=1, min_train_batch=240)
+    opt.stop = qac.StopCondition(max_updates=12)
+    r = qac.run(opt)
+    assert r.total_updates == 12 and r.experiences_trained >= 12 * 240
+    assert r.experiences_produced == r.experiences_trained + r.experiences_left_queued + r.experiences_dropped
+    assert np.all(np.isfinite(r.final_theta))
