@@ -163,7 +163,14 @@ int ga3c_trainer_pool_wait(ga3c_trainer_pool* p, long long* updates, long long* 
   return p->error;
 }
 
-const char* ga3c_trainer_pool_error(ga3c_trainer_pool* p) { return p ? p->error_msg.c_str() : ""; }
+const char* ga3c_trainer_pool_error(ga3c_trainer_pool* p) {
+  // a copy per calling thread: a worker may record the error concurrently
+  thread_local std::string msg;
+  if (!p) return "";
+  std::lock_guard<std::mutex> lk(p->mu);
+  msg = p->error_msg;
+  return msg.c_str();
+}
 
 void ga3c_trainer_pool_destroy(ga3c_trainer_pool* p) {
   if (!p) return;
