@@ -34,14 +34,49 @@ void check(int st, ga3c_model* m, const char* what) {
   throw std::runtime_error(msg);
 }
 
-// RAII per-thread device context (stream + workspace)
+// Contexts of retired predictor / trainer threads, kept for the next ones:
+// the annealer restarts whole pools when it moves a batch knob, and a new
+// context costs its workspace allocation (and its captured graphs).
+struct CtxPool {
+  std::mutex mu;
+  std::vector<std::pair<ga3c_ctx*, int>> free;  // (context, max_batch)
+  ~CtxPool() {
+    for (auto& e : free) ga3c_ctx_destroy(e.first);
+  }
+  ga3c_ctx* take(int mb, int* got) {
+    std::lock_guard<std::mutex> lk(mu);
+    for (std::size_t i = 0; i < free.size(); ++i)
+      if (free[i].second >= mb) {
+        ga3c_ctx* c = free[i].first;
+        *got = free[i].second;
+        free.erase(free.begin() + static_cast<std::ptrdiff_t>(i));
+        return c;
+      }
+    return nullptr;
+  }
+  void give(ga3c_ctx* c, int mb) {
+    std::lock_guard<std::mutex> lk(mu);
+    free.emplace_back(c, mb);
+  }
+};
+
+// RAII per-thread device context (stream + workspace), from `pool` when it
+// has one large enough and back to it afterwards
 struct Ctx {
   ga3c_ctx* c = nullptr;
   int max_batch = 0;
   ga3c_model* m = nullptr;
-  Ctx(ga3c_model* model, int mb) : m(model) { reset(mb); }
+  CtxPool* pool = nullptr;
+  Ctx(ga3c_model* model, int mb, CtxPool* p = nullptr) : m(model), pool(p) {
+    if (pool) c = pool->take(mb, &max_batch);
+    if (!c) reset(mb);
+  }
   ~Ctx() {
-    if (c) ga3c_ctx_destroy(c);
+    if (!c) return;
+    if (pool && ga3c_ctx_sync(c) == GA3C_OK)
+      pool->give(c, max_batch);
+    else
+      ga3c_ctx_destroy(c);
   }
   Ctx(const Ctx&) = delete;
   Ctx& operator=(const Ctx&) = delete;
@@ -459,7 +494,7 @@ class Engine {
   // ---- trainers (pipeline.cpp:241-306)
   void trainer_main(std::atomic<bool>& stop) {
     try {
-      Ctx ctx(shared_.handle(), std::max(64, opt_.knobs.min_train_batch + 4 * opt_.hyper.t_max));
+      Ctx ctx(shared_.handle(), std::max(64, opt_.knobs.min_train_batch + 4 * opt_.hyper.t_max), &ctx_pool_);
       ga3c_ctx_set_sm_budget(ctx.c, sm_budget(opt_.trainer_sms, 111));
       HostBatch hb;
       std::vector<std::int32_t> acts, off, fidx;
@@ -568,7 +603,7 @@ class Engine {
 
   void predictor_main(std::atomic<bool>& stop) {
     try {
-      Ctx ctx(shared_.handle(), opt_.knobs.pred_batch_max);
+      Ctx ctx(shared_.handle(), opt_.knobs.pred_batch_max, &ctx_pool_);
       ga3c_ctx_set_sm_budget(ctx.c, sm_budget(opt_.predictor_sms, 64));
       predictor_loop(pred_q_, slots_, shared_, ctx.c, opt_.knobs.pred_batch_max, pmetrics_, stop, store_);
     } catch (...) {
@@ -808,6 +843,7 @@ class Engine {
   PipelineOptions opt_;
   std::size_t slot_cap_;
   SharedModel shared_;
+  CtxPool ctx_pool_;               // destroyed before shared_'s model (declared after it)
   ga3c_frames* store_ = nullptr;  // device frame store (device_frames)
   int hist_ = 0;
   std::unique_ptr<std::atomic<std::uint8_t>[]> busy_;  // [agent][slot]: holds an untrained experience's state
