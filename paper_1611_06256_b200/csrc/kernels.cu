@@ -3,14 +3,16 @@
 //   heads_forward_kernel   FC finalize (split-K reduce + bias + ReLU) fused with
 //                          the policy/value heads and the max-subtracted softmax
 //                          (nnet.cpp:96-117)
-//   loss_heads_bwd_kernel  per-sample A3C loss terms, dL/dpi, softmax Jacobian,
-//                          dV, and the heads' input gradient with the ReLU gate
-//                          (nnet.cpp:229-270)
+//   heads_loss_kernel      the same heads fused with the per-sample A3C loss
+//                          terms, dL/dpi, softmax Jacobian, dV, and the heads'
+//                          input gradient with the ReLU gate (nnet.cpp:229-270)
+//   heads_wgrad_kernel     the heads' weight gradient dhead^T [h | 1] and the
+//                          loss diagnostics' batch sums (nnet.cpp:233-262)
 //   conv_dgrad_kernel      gather-form col2im of a VALID conv, gated by the
 //                          previous layer's activation (nnet.cpp:267-278)
 //   splitk_* kernels       fixed-order split-K reductions (deterministic)
-//   scalars / clip         loss diagnostics and the optional global-norm clip
-//                          (nnet.cpp:233-235, 281-289)
+//   scalars / clip         loss diagnostics (wide-heads fallback) and the
+//                          optional global-norm clip (nnet.cpp:233-235, 281-289)
 //   rmsprop_kernel         fused vectorised non-centred RMSProp with the
 //                          non-finite reject gate (nnet.cpp:293-312)
 //   returns_kernel         n-step returns, fp64 without contraction (returns.cpp:21-24)

@@ -41,13 +41,6 @@ struct HeadsGrad {
 __global__ void heads_wgrad_kernel(HeadsGrad hg, float* grad, int* flag);
 
 
-__global__ void loss_heads_bwd_kernel(const double* pi64, const float* v, const int32_t* actions,
-                                      const double* rets, const float* h, int B, int D, int A,
-                                      const float* theta, std::size_t wp_off, std::size_t wv_off,
-                                      double beta, double eps, double c_v, float* dhead, float* dh,
-                                      float* dhT, int ldT, double* scal, int* flag);
-
-
 __global__ void scalars_kernel(const double* scal, int B, double* out);
 
 __global__ void conv_dgrad_kernel(const float* dout, const float* W, const float* gate, float* din,
