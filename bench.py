@@ -451,9 +451,18 @@ def main():
 
     from paper_1611_06256_b200 import _abi
 
+    # test harness only (tests/test_bench_multirank_gpu.py): every rank on
+    # cuda:0 over gloo, so the N > 1 path runs on a one-GPU box (NCCL refuses
+    # two ranks on one device)
+    one_gpu = world > 1 and os.environ.get("GA3C_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     convs, hidden = NETS[args.net]
     spec = _abi.NetSpec()
     spec.in_h, spec.in_w, spec.in_c = FRAME
