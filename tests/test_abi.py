@@ -132,3 +132,28 @@ def test_two_cta_kernels_fit_two_per_sm():
             checked += 1
             assert reg <= 96, f"{name}: {reg} registers -> one CTA per SM at ring cap {cap}"
     assert checked >= 10
+
+
+def test_new_entry_points_reject_bad_arguments_without_a_device():
+    """The round-2 entry points (trainer pool, asynchronous prediction,
+    pinned host memory, engine options) check their arguments
+    before touching a device: null handles and bad sizes are
+    GA3C_INVALID_ARGUMENT, and no call falls back to the CPU."""
+    from paper_1611_06256_b200 import _abi
+    L = _abi.lib
+    st = C.c_int(0)
+    assert not L.ga3c_trainer_pool_create(None, None, 4, 64, 0, 16, C.byref(st))
+    assert st.value == _abi.INVALID_ARGUMENT
+    assert L.ga3c_trainer_pool_submit(None, None, None, 0, None, None, None, 0, None, None, 0.99) == \
+        _abi.INVALID_ARGUMENT
+    assert L.ga3c_trainer_pool_submit_many(None, 1, None, None, None, None, None, None, None, None, None,
+                                           0.99) == _abi.INVALID_ARGUMENT
+    assert L.ga3c_trainer_pool_wait(None, None, None) == _abi.INVALID_ARGUMENT
+    assert L.ga3c_trainer_pool_error(None) == b""
+    L.ga3c_trainer_pool_destroy(None)
+    assert L.ga3c_predict_frames64_async(None, -1, None, None, None, None, 0, None) == _abi.INVALID_ARGUMENT
+    assert L.ga3c_predict_collect64(None, None, None, None) == _abi.INVALID_ARGUMENT
+    L.ga3c_host_free(None)
+    opts = _abi.PipelineOpts()
+    L.ga3c_default_pipeline_opts(C.byref(opts))
+    assert opts.device_frames == 0 and opts.trainer_sms == -1 and opts.predictor_sms == -1
