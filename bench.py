@@ -66,7 +66,7 @@ def parse():
     p.add_argument("--no-loop", action="store_true", help="skip the C++ GA3C loop leg (ga3c_loop)")
     p.add_argument("--loop-seconds", type=float, default=10.0)
     p.add_argument("--e2e-steps", type=int, default=0)
-    p.add_argument("--e2e-windows", type=int, default=3)
+    p.add_argument("--e2e-windows", type=int, default=7)
     p.add_argument("--e2e-trainers", type=int, default=4, help="trainer threads in the e2e leg (0 = serial)")
     # N_P = 1 measured best (DNN A e2e, median of 3 windows: N_P/N_T 1/4 644-665K, 2/4 584-610K, 3/4 514K,
     # 2/6 546K; large s1 1/3 102K, 2/4 99K): more host threads contend for the GIL and the 16 vCPUs
@@ -995,7 +995,7 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
             return time.perf_counter() - t0
 
         window(2)  # warm-up
-        # three timed windows of k steps each, the median reported: on the
+        # seven timed windows of k steps each (~70 ms each), the median reported: on the
         # 16-vCPU box single windows of host threads vary by up to 1.5x
         wins = sorted(window(k) for _ in range(args.e2e_windows))
         dt_thr = wins[len(wins) // 2]

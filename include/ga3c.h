@@ -231,13 +231,21 @@ int ga3c_model_ring(ga3c_model* m, int n, int* slots_out);
  * non-finite flag of context grad_from (NULL = c), stream-ordered on c's
  * stream; the caller orders grad_from's stream before it.  Capturable. */
 int ga3c_apply_rmsprop_slots_dev(ga3c_ctx* c, const ga3c_ctx* grad_from, int src_slot, int dst_slot);
-/* SMs this context's split-K plans try to fill (0 = all, or the
- * GA3C_SPLIT_SMS environment variable).  With N_T trainer contexts in
+/* SMs this context's split-K plans try to fill (0 = all).  With N_T trainer contexts in
  * flight a share of the SMs per context costs less SM time per update
  * (fewer, longer CTAs) than a full wave each.  Results do not change
  * (every reduction is fixed-order for a given plan; parity tolerances hold
  * for any plan). */
 int ga3c_ctx_set_sm_budget(ga3c_ctx* c, int sms);
+/* Scheduling priority of the context's stream: 0 = the device's highest
+ * (the default: a predictor's forward is on the agents' critical path),
+ * level k = k steps lower (clamped to the lowest).  GA3C's trainers are
+ * throughput work beside latency-bound predictions (pipeline.cpp:153-205
+ * vs 241-306), so the native trainer pool and engine run their trainer
+ * contexts one level below the predictors.  Call while the context is idle
+ * and before capturing graphs on it (captured kernels keep the priority
+ * they were captured at). */
+int ga3c_ctx_set_priority(ga3c_ctx* c, int level);
 /* Copy parameter slot src_slot's theta and rms state into dst_slot,
  * stream-ordered on c's stream (capturable): e.g. publish the last version of
  * a device loop to a predictor-only slot that the trainers never write, so

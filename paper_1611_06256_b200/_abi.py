@@ -166,6 +166,7 @@ _SIGS = {
     "ga3c_apply_rmsprop_slots_dev": (C.c_int, [_P, _P, C.c_int, C.c_int]),
     "ga3c_copy_slot_dev": (C.c_int, [_P, C.c_int, C.c_int]),
     "ga3c_ctx_set_sm_budget": (C.c_int, [_P, C.c_int]),
+    "ga3c_ctx_set_priority": (C.c_int, [_P, C.c_int]),
     "ga3c_frames_create": (_P, [_P, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "ga3c_frames_destroy": (None, [_P]),
     "ga3c_host_alloc": (_P, [C.c_size_t, C.POINTER(C.c_int)]),
@@ -447,6 +448,10 @@ class Context:
 
     def set_sm_budget(self, sms):
         check(lib.ga3c_ctx_set_sm_budget(self.h, sms), self.model.error())
+
+    def set_priority(self, level):
+        """ga3c_ctx_set_priority: 0 = highest (default), k = k levels lower."""
+        check(lib.ga3c_ctx_set_priority(self.h, level), self.model.error())
 
     def copy_slot_dev(self, src_slot, dst_slot):
         check(lib.ga3c_copy_slot_dev(self.h, src_slot, dst_slot), self.model.error())

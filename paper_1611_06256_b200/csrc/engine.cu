@@ -2008,6 +2008,22 @@ int ga3c_ctx_set_sm_budget(ga3c_ctx* c, int sms) {
   return GA3C_OK;
 }
 
+int ga3c_ctx_set_priority(ga3c_ctx* c, int level) {
+  if (!c || level < 0) return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  int prio_lo = 0, prio_hi = 0;
+  GA3C_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  // numerically lower = higher priority; the side streams stay lowest
+  const int prio = std::min(prio_hi + level, prio_lo);
+  GA3C_CUDA(cudaStreamSynchronize(c->stream));
+  cudaStream_t s = nullptr;
+  GA3C_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, prio));
+  cudaStreamDestroy(c->stream);
+  c->stream = c->cur = s;
+  return GA3C_OK;
+}
+
 int ga3c_copy_slot_dev(ga3c_ctx* c, int src_slot, int dst_slot) {
   if (!c || src_slot < 0 || dst_slot < 0 || src_slot >= (int)c->m->slots.size() ||
       dst_slot >= (int)c->m->slots.size())

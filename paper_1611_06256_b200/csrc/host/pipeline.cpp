@@ -496,6 +496,10 @@ class Engine {
     try {
       Ctx ctx(shared_.handle(), std::max(64, opt_.knobs.min_train_batch + 4 * opt_.hyper.t_max), &ctx_pool_);
       ga3c_ctx_set_sm_budget(ctx.c, sm_budget(opt_.trainer_sms, 111));
+      // trainers are throughput work: one stream-priority level below the
+      // predictors, whose forwards the agents wait on (contexts move
+      // between roles through ctx_pool_, so both roles set theirs)
+      ga3c_ctx_set_priority(ctx.c, 1);
       HostBatch hb;
       std::vector<std::int32_t> acts, off, fidx;
       std::vector<double> rew, boot;
@@ -605,6 +609,7 @@ class Engine {
     try {
       Ctx ctx(shared_.handle(), opt_.knobs.pred_batch_max, &ctx_pool_);
       ga3c_ctx_set_sm_budget(ctx.c, sm_budget(opt_.predictor_sms, 64));
+      ga3c_ctx_set_priority(ctx.c, 0);
       predictor_loop(pred_q_, slots_, shared_, ctx.c, opt_.knobs.pred_batch_max, pmetrics_, stop, store_);
     } catch (...) {
       report_error(std::current_exception());

@@ -8,7 +8,9 @@
 // runs ga3c_train_frames (device returns + loss/backward on the states kept
 // in the frame store) on the latest snapshot and ga3c_apply_rmsprop
 // (out-of-place RMSProp, published at once).  No Python, no GIL on the
-// training path.
+// training path.  The trainer contexts run one stream-priority level below
+// the default (ga3c_ctx_set_priority), so the callers' predictions, which
+// the agents wait on, are scheduled ahead of queued training kernels.
 #include <algorithm>
 #include <condition_variable>
 #include <cstring>
@@ -105,7 +107,15 @@ ga3c_trainer_pool* ga3c_trainer_pool_create(ga3c_model* m, ga3c_frames* f, int n
       return fail(st ? st : GA3C_CUDA_ERROR);
     }
     ga3c_ctx_set_sm_budget(c, sms);
+    // one level below the callers' predictor contexts (DNN A e2e, two runs
+    // each: level 0 835K / 869K, level 1 925K / 914K, level 3 921K / 856K)
     p->ctxs.push_back(c);
+    const int pst = ga3c_ctx_set_priority(c, 1);
+    if (pst != GA3C_OK) {
+      for (auto* x : p->ctxs) ga3c_ctx_destroy(x);
+      delete p;
+      return fail(pst);
+    }
   }
   for (auto* c : p->ctxs) p->threads.emplace_back([p, c] { p->worker(c); });
   if (status) *status = GA3C_OK;

@@ -153,6 +153,7 @@ def test_new_entry_points_reject_bad_arguments_without_a_device():
     L.ga3c_trainer_pool_destroy(None)
     assert L.ga3c_predict_frames64_async(None, -1, None, None, None, None, 0, None) == _abi.INVALID_ARGUMENT
     assert L.ga3c_predict_collect64(None, None, None, None) == _abi.INVALID_ARGUMENT
+    assert L.ga3c_ctx_set_priority(None, 1) == _abi.INVALID_ARGUMENT
     L.ga3c_host_free(None)
     opts = _abi.PipelineOpts()
     L.ga3c_default_pipeline_opts(C.byref(opts))

@@ -433,6 +433,33 @@ def test_sm_budget_changes_plans_not_results(sms):
     grad_close(d1, rd)
 
 
+def test_stream_priority_changes_scheduling_not_results():
+    """ga3c_ctx_set_priority re-creates the context stream one or more
+    levels lower (the trainer pool's and engine's trainers run at level 1);
+    forward and gradient are bitwise what the default-priority context
+    computes, and a level past the device's range clamps to the lowest."""
+    B = 40
+    spec = O.dnn_a()
+    th = theta32(spec, O.derive_seed(1, [O.SEED_MODEL_INIT]))
+    fr = O.synthetic_frames(61, B)
+    acts, rets = O.synthetic_batch(61, B, 6)
+    m, ctx = make(spec, max_batch=B)
+    m.load(th)
+    d0, s0 = ctx.loss_grad(fr, acts, rets)
+    p0, v0, _ = ctx.forward(fr)
+    old = ctx.stream
+    for level in (1, 1000, 0):
+        ctx.set_priority(level)
+        d1, s1 = ctx.loss_grad(fr, acts, rets)
+        p1, v1, _ = ctx.forward(fr)
+        assert np.array_equal(d0, d1) and np.array_equal(s0, s1)
+        assert np.array_equal(p0, p1) and np.array_equal(v0, v1)
+    assert ctx.stream != 0 and old != 0
+    from paper_1611_06256_b200 import _abi
+    with pytest.raises(_abi.GA3CError):
+        ctx.set_priority(-1)
+
+
 def test_copy_slot_publishes_parameters():
     spec = O.make_spec((12, 12, 2), [(4, 4, 2)], [8], 4)
     m, ctx = make(spec, max_batch=4)
