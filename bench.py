@@ -73,6 +73,9 @@ def parse():
     p.add_argument("--e2e-predictors", type=int, default=1, help="predictor threads in the e2e leg (N_P)")
     p.add_argument("--e2e-groups", type=int, default=2,
                    help="agent groups one predictor thread keeps in flight (asynchronous predictions)")
+    p.add_argument("--e2e-sampling", default="device", choices=["device", "host"],
+                   help="e2e agents' actions: drawn on the device from the agents' uniforms "
+                        "(ga3c_predict_frames_act64_async) or on the host from the returned fp64 pi")
     p.add_argument("--trainers", type=int, default=4,
                    help="trainer contexts in flight in the device step (N_T, policy lag N_T - 1 updates)")
     p.add_argument("--cpu-seconds", type=float, default=6.0)
@@ -945,18 +948,28 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
     agroups = [slice(a0, a1) for a0, a1 in (shard(NA, g, NG) for g in range(NG))]
     ctx_g = [ctx] + [_abi.Context(model, NA) for _ in range(NG - 1)]
 
+    dev_sample = args.e2e_sampling == "device"
+
     def predict_groups_async(s, pt, acts, slots, vout):
+        # acts / slots are (T, NA) here: each group's row slice is contiguous
         def submit(g, t):
             gs = agroups[g]
-            slots[gs, t] = _abi.predict_frames_async(ctx_g[g], store, newf[s][t][gs], agents[gs],
-                                                     pt[gs] if t == 0 else None)
+            if dev_sample:
+                _abi.predict_frames_act_async(ctx_g[g], store, newf[s][t][gs], agents[gs], u_h[s, t][gs],
+                                              pt[gs] if t == 0 else None, slots=slots[t, gs])
+            else:
+                slots[t, gs] = _abi.predict_frames_async(ctx_g[g], store, newf[s][t][gs], agents[gs],
+                                                         pt[gs] if t == 0 else None)
         for g in range(NG):
             submit(g, 0)
         for t in range(T):
             for g in range(NG):
                 gs = agroups[g]
-                pi, v, _ = _abi.predict_collect(ctx_g[g])
-                acts[gs, t] = sample_rows(pi, u_h[s, t][gs])
+                if dev_sample:  # qac::sample_index on the device, bitwise the host draw
+                    _, v, _, _ = _abi.predict_collect_act(ctx_g[g], actions=acts[t, gs])
+                else:
+                    pi, v, _ = _abi.predict_collect(ctx_g[g])
+                    acts[t, gs] = sample_rows(pi, u_h[s, t][gs])
                 if t + 1 < T:
                     submit(g, t + 1)
                 else:
@@ -968,7 +981,10 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
         slots = np.zeros((NA, T), np.int32)
         v = np.zeros(NA, np.float64)
         if NP == 1 and NG > 1:
-            predict_groups_async(s, pt, acts, slots, v)
+            acts_t = np.zeros((T, NA), np.int32)
+            slots_t = np.zeros((T, NA), np.int32)
+            predict_groups_async(s, pt, acts_t, slots_t, v)
+            acts, slots = acts_t.T, slots_t.T
         elif NP == 1:  # the main thread is the predictor: no hand-off
             predict_group(0, s, pt, acts, slots, v)
         else:
@@ -1003,14 +1019,19 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
         if dt_thr < dt:
             dt, mode = dt_thr, (f"{NP} predictor thread(s)"
                                 + (f" x {NG} agent groups in flight" if NP == 1 and NG > 1 else "")
-                                + f" + native trainer pool of {args.e2e_trainers} (ga3c_trainer_pool)")
+                                + f" + native trainer pool of {args.e2e_trainers} (ga3c_trainer_pool)"
+                                + (", actions sampled on the device" if dev_sample and NP == 1 and NG > 1 else ""))
+            if dev_sample and NP == 1 and NG > 1:  # the agents' uniforms up, the drawn actions down
+                h2d += n * 8
+                d2h += n * 4
         pool_t.close()
     store.close()
     out = {"value": world * n * k / dt, "unit": "samples/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "steps": k, "ms_per_step": 1e3 * dt / k, "mode": mode,
            "serial_value": world * n * k / dt_serial, "windows": win_vals,
            "timing": f"threaded: median of {len(win_vals)} windows of {k} steps" if win_vals else "serial",
-           "path": "ga3c_predict_frames (newest 84x84 frame per agent) / host sampling / ga3c_train_frames / "
+           "path": "ga3c_predict_frames[_act64_async] (newest 84x84 frame per agent) / qac::sample_index "
+                   "(device with the host's uniforms, or host) / ga3c_train_frames / "
                    "ga3c_apply_rmsprop (host buffers, pinned)"}
     if world == 1:
         fr_agent = [frames[s].cpu().pin_memory().numpy() for s in range(hs)]

@@ -358,6 +358,17 @@ int ga3c_predict_frames64(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* 
 int ga3c_predict_frames64_async(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* new_frames,
                                 const int32_t* agents, const uint8_t* resets, int n, int32_t* state_slots);
 int ga3c_predict_collect64(ga3c_ctx* c, double* pi, double* v, uint64_t* version_used);
+/* As ga3c_predict_frames64_async, plus the agents' actions drawn on the
+ * device: u[i] is agent i's uniform draw (qac::next_uniform), and
+ * sample_kernel applies qac::sample_index (util.hpp:46-54) to the fp64
+ * policy -- bitwise the action host-side sampling of the returned pi draws
+ * (pipeline.cpp:172-173).  ga3c_predict_collect_act64 waits and copies out
+ * actions, V and (pi != NULL) the fp64 policy; ga3c_predict_collect64 also
+ * collects such a prediction (pi and V only). */
+int ga3c_predict_frames_act64_async(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* new_frames,
+                                    const int32_t* agents, const uint8_t* resets, int n, const double* u,
+                                    int32_t* state_slots);
+int ga3c_predict_collect_act64(ga3c_ctx* c, int32_t* actions, double* v, double* pi, uint64_t* version_used);
 /* Trainer call: as ga3c_loss_grad_segments_u8, with sample b's state read
  * from the store at (agents[b], state_slots[b]) on the device. */
 int ga3c_train_frames(ga3c_ctx* c, int slot, ga3c_frames* f, const int32_t* agents,

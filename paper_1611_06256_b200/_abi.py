@@ -172,6 +172,8 @@ _SIGS = {
     "ga3c_host_alloc": (_P, [C.c_size_t, C.POINTER(C.c_int)]),
     "ga3c_predict_frames64_async": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_int, _P]),
     "ga3c_predict_collect64": (C.c_int, [_P, _P, _P, C.POINTER(C.c_uint64)]),
+    "ga3c_predict_frames_act64_async": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_int, _P, _P]),
+    "ga3c_predict_collect_act64": (C.c_int, [_P, _P, _P, _P, C.POINTER(C.c_uint64)]),
     "ga3c_host_free": (None, [_P]),
     "ga3c_trainer_pool_create": (_P, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "ga3c_trainer_pool_submit": (C.c_int, [_P, _P, _P, C.c_int, _P, _P, _P, C.c_int, _P, _P, C.c_double]),
@@ -593,6 +595,43 @@ def predict_collect(ctx: "Context"):
     check(lib.ga3c_predict_collect64(ctx.h, pi.ctypes.data, v.ctypes.data, C.byref(ver)), ctx.model.error())
     ctx._pending = None
     return pi, v, ver.value
+
+
+def predict_frames_act_async(ctx: "Context", frames: Frames, new_frames, agents, u, resets=None, slot=-1,
+                             slots=None):
+    """Enqueue a frame-store prediction whose actions are drawn on the device
+    from the agents' uniforms u (ga3c_predict_frames_act64_async) ->
+    state_slots (into `slots` when given); predict_collect_act(ctx) returns
+    (actions, v, pi or None, version)."""
+    import numpy as np
+    nf = np.ascontiguousarray(new_frames, np.uint8)
+    ag = np.ascontiguousarray(agents, np.int32)
+    uu = np.ascontiguousarray(u, np.float64)
+    n = len(ag)
+    if uu.shape[0] != n:
+        raise InvalidArgument(INVALID_ARGUMENT, "one uniform per agent")
+    rs = None if resets is None else np.ascontiguousarray(resets, np.uint8)
+    if slots is None:
+        slots = np.empty(n, np.int32)
+    check(lib.ga3c_predict_frames_act64_async(ctx.h, slot, frames.h, nf.ctypes.data, ag.ctypes.data,
+                                              None if rs is None else rs.ctypes.data, n, uu.ctypes.data,
+                                              slots.ctypes.data), ctx.model.error())
+    ctx._pending = (n, nf, ag, rs, uu)
+    return slots
+
+
+def predict_collect_act(ctx: "Context", actions=None, want_pi=False):
+    import numpy as np
+    n = ctx._pending[0]
+    if actions is None:
+        actions = np.empty(n, np.int32)
+    v = np.empty(n, np.float64)
+    pi = np.empty((n, ctx.model.n_actions), np.float64) if want_pi else None
+    ver = C.c_uint64(0)
+    check(lib.ga3c_predict_collect_act64(ctx.h, actions.ctypes.data, v.ctypes.data,
+                                         None if pi is None else pi.ctypes.data, C.byref(ver)), ctx.model.error())
+    ctx._pending = None
+    return actions, v, pi, ver.value
 
 
 def train_frames(ctx: "Context", frames: Frames, agents, state_slots, actions, rewards, seg_offsets, terminal,

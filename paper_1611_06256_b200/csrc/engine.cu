@@ -183,6 +183,7 @@ struct ga3c_ctx {
     bool active = false;
     const double* h_pi = nullptr;
     const double* h_v = nullptr;
+    const int32_t* h_act = nullptr;  // device-sampled actions (ga3c_predict_frames_act64_async)
     int n = 0, A = 0, slot = -1;
     bool pinned = false;
     std::uint64_t ver = 0;
@@ -2489,7 +2490,7 @@ int ga3c_loss_grad_segments_u8(ga3c_ctx* c, int slot, const uint8_t* frames, int
 template <typename OutT>
 static int predict_frames_impl(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* new_frames,
                                const int32_t* agents, const uint8_t* resets, int n, int32_t* state_slots, OutT* pi,
-                               OutT* v, uint64_t* version_used, bool async = false) {
+                               OutT* v, uint64_t* version_used, bool async = false, const double* u = nullptr) {
   constexpr bool f64 = std::is_same<OutT, double>::value;
   if (!c || !f || f->m != c->m || n < 0 || n > c->max_batch ||
       (n > 0 && (!new_frames || !agents || (!async && (!pi || !v)))) || c->pend.active)
@@ -2534,9 +2535,11 @@ static int predict_frames_impl(ga3c_ctx* c, int slot, ga3c_frames* f, const uint
     const int A = m->lo.n_actions;
     Stager sg{c};
     const int32_t* d_idx = sg.put(idx.data(), idx.size());
+    const double* d_u = u ? sg.put(u, n) : nullptr;
     OutT* h_pi = sg.take<OutT>(static_cast<std::size_t>(n) * A);
     OutT* h_v = sg.take<OutT>(n);
-    if (!d_idx || !h_pi || !h_v) rc = GA3C_INVALID_ARGUMENT;
+    int32_t* h_act = u ? sg.take<int32_t>(n) : nullptr;
+    if (!d_idx || !h_pi || !h_v || (u && (!d_u || !h_act))) rc = GA3C_INVALID_ARGUMENT;
     if (!rc && (cudaMemcpyAsync(newf, new_frames, f->frame_px * n, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
                 !sg.flush()))
       rc = GA3C_CUDA_ERROR;
@@ -2551,8 +2554,17 @@ static int predict_frames_impl(ga3c_ctx* c, int slot, ga3c_frames* f, const uint
       run_forward(c, m->slots[s].theta, dense, true, n);
       const void* d_pi = f64 ? static_cast<const void*>(c->pi64) : static_cast<const void*>(c->pi32);
       const void* d_v = f64 ? static_cast<const void*>(c->v64) : static_cast<const void*>(c->v);
+      if (u) {
+        // qac::sample_index on the fp64 policy (util.hpp:46-54) with the
+        // caller's uniforms: the action the host would draw, bitwise
+        Launch l(c, GA3C_K_SAMPLE, -1);
+        pdl_launch(c->cur, sample_kernel, dim3((n + 127) / 128), dim3(128), 0, c->pi32, c->pi64, d_u, n, A,
+                   c->d_actions, 1);
+      }
       if (cudaMemcpyAsync(h_pi, d_pi, sizeof(OutT) * n * A, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
-          cudaMemcpyAsync(h_v, d_v, sizeof(OutT) * n, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+          cudaMemcpyAsync(h_v, d_v, sizeof(OutT) * n, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+          (u && cudaMemcpyAsync(h_act, c->d_actions, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream) !=
+                    cudaSuccess))
         rc = GA3C_CUDA_ERROR;
     }
     if (async && !rc) {
@@ -2564,6 +2576,7 @@ static int predict_frames_impl(ga3c_ctx* c, int slot, ga3c_frames* f, const uint
         c->pend.active = true;
         c->pend.h_pi = reinterpret_cast<const double*>(h_pi);
         c->pend.h_v = reinterpret_cast<const double*>(h_v);
+        c->pend.h_act = h_act;
         c->pend.n = n;
         c->pend.A = A;
         c->pend.slot = s;
@@ -2606,6 +2619,32 @@ int ga3c_predict_frames64_async(ga3c_ctx* c, int slot, ga3c_frames* f, const uin
   if (n < 1) return GA3C_INVALID_ARGUMENT;
   return predict_frames_impl<double>(c, slot, f, new_frames, agents, resets, n, state_slots, nullptr, nullptr,
                                      nullptr, true);
+}
+
+int ga3c_predict_frames_act64_async(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* new_frames,
+                                    const int32_t* agents, const uint8_t* resets, int n, const double* u,
+                                    int32_t* state_slots) {
+  if (n < 1 || !u) return GA3C_INVALID_ARGUMENT;
+  return predict_frames_impl<double>(c, slot, f, new_frames, agents, resets, n, state_slots, nullptr, nullptr,
+                                     nullptr, true, u);
+}
+
+int ga3c_predict_collect_act64(ga3c_ctx* c, int32_t* actions, double* v, double* pi, uint64_t* version_used) {
+  if (!c || !c->pend.active || !c->pend.h_act || !actions || !v) return GA3C_INVALID_ARGUMENT;
+  ga3c_model* m = c->m;
+  auto set_err = [&](const std::string& e) { m->set_error(e); };
+  const cudaError_t e = cudaEventSynchronize(c->pend.ev);
+  c->pend.active = false;
+  if (c->pend.pinned) ga3c_snapshot_release(m, c->pend.slot);
+  if (e != cudaSuccess) {
+    set_err(std::string("predict_collect_act64: ") + cudaGetErrorString(e));
+    return GA3C_CUDA_ERROR;
+  }
+  std::memcpy(actions, c->pend.h_act, sizeof(int32_t) * c->pend.n);
+  std::memcpy(v, c->pend.h_v, sizeof(double) * c->pend.n);
+  if (pi) std::memcpy(pi, c->pend.h_pi, sizeof(double) * c->pend.n * c->pend.A);
+  if (version_used) *version_used = c->pend.ver;
+  return GA3C_OK;
 }
 
 int ga3c_predict_collect64(ga3c_ctx* c, double* pi, double* v, uint64_t* version_used) {

@@ -160,6 +160,47 @@ def test_async_predict_matches_sync_and_guards_the_stage():
         _abi.predict_collect(ctx2)
 
 
+def test_device_sampled_actions_match_host_sample_index():
+    """ga3c_predict_frames_act64_async draws each agent's action on the
+    device from its uniform: the same action the reference's host-side
+    qac::sample_index (util.hpp:46-54, restated in oracle/pyoracle.py)
+    draws from the returned fp64 pi, including uniforms placed exactly on
+    and just beside a cumulative-probability boundary and u -> 1 (the
+    last action).  The pi / V / state slots are those of the host-sampling
+    call, and ga3c_predict_collect64 also collects such a prediction."""
+    _abi, m, ctx, fr = setup(n_agents=7, history=4)
+    fr2 = _abi.Frames(m, 7, 4)
+    ctx2 = _abi.Context(m, 64)
+    rng = np.random.default_rng(11)
+    agents = np.arange(7, dtype=np.int32)
+    margins = []
+    for step in range(4):
+        new = rng.integers(0, 256, (7, H * W), dtype=np.uint8)
+        pi, v, sl, ver = _abi.predict_frames(ctx, fr, new, agents, fp64=True)
+        cdf = np.cumsum(pi, 1)  # left-to-right fp64, as the reference accumulates
+        u = rng.random(7)
+        u[0] = cdf[0, 2]  # exactly on a boundary: not below it, so the next action
+        u[1] = np.nextafter(cdf[1, 0], 0.0)  # just below: action 0
+        u[2] = 1.0 - 1e-17  # rounds to 1.0 in fp64: past every cumulative sum
+        u[3] = 0.0
+        if step < 3:
+            sl2 = _abi.predict_frames_act_async(ctx2, fr2, new, agents, u)
+            a2, v2, pi2, ver2 = _abi.predict_collect_act(ctx2, want_pi=True)
+            assert np.array_equal(pi, pi2)
+        else:
+            sl2 = _abi.predict_frames_act_async(ctx2, fr2, new, agents, u)
+            pi2, v2, ver2 = _abi.predict_collect(ctx2)
+            assert np.array_equal(pi, pi2)
+            continue
+        want = np.array([O.sample_index(list(pi[i]), float(u[i])) for i in range(7)], np.int32)
+        assert np.array_equal(a2, want), (a2, want)
+        assert np.array_equal(sl, sl2) and np.array_equal(v, v2) and ver == ver2
+        margins.append(float(np.min(np.abs(cdf - u[:, None]))))
+    assert margins[0] == 0.0  # the on-boundary draw was exercised
+    with pytest.raises(ValueError):
+        _abi.predict_frames_act_async(ctx2, fr2, new, agents, u[:3])  # one uniform per agent
+
+
 def test_graph_replayed_training_trajectory_matches_eager_bitwise():
     """ga3c_train_frames replays a captured graph per (snapshot slot, shape):
     eight train + apply rounds (the latest slot moves every round, so graphs
