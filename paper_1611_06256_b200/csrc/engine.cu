@@ -44,6 +44,7 @@
 #include "tc_bf16.cuh"
 #include "tc_dgrad.cuh"
 #include "tc_u8conv.cuh"
+#include "tc_wgrad_band.cuh"
 #include "dp_fused.cuh"
 #include "pdl.cuh"
 
@@ -800,10 +801,76 @@ void wgrad_tc_launch(ga3c_ctx* c, int li, const WgradArgs& a, dim3 grid, int tag
 #undef GA3C_F
 }
 
+// u8 first conv layer with 32-byte window rows (k * Cin == 32): per-image
+// pixel ranges staged whole by bulk copy (tc_wgrad_band.cuh) instead of
+// im2col gathers; returns false when the shape does not qualify.
+constexpr int kBandSmemMax = 220 * 1024;  // + the kernel's static shared memory <= 227 KB
+bool layer_wgrad_band(ga3c_ctx* c, int li, const Layer& L, const uint8_t* x_in, const float* dout, int B,
+                      long long in_stride, const GradMap& gm, float* part) {
+  if (!L.is_conv || L.k * L.cin != 32 || L.k > 8 || L.out > wb::BN || L.out % 4 != 0 || L.in != 32 * L.k ||
+      L.w_off % 4 != 0)
+    return false;
+  const long long bstride = in_stride > 0 ? in_stride : static_cast<long long>(L.ih) * L.iw * L.cin;
+  const int rowb = L.iw * L.cin;
+  if (rowb % 16 != 0 || bstride % 16 != 0 || reinterpret_cast<uintptr_t>(x_in) % 16 != 0 ||
+      reinterpret_cast<uintptr_t>(dout) % 16 != 0)
+    return false;
+  const int P = L.pixels(), nch = (P + 31) / 32;
+  // CTAs per image: as the im2col path's split target (2x the SMs for a
+  // context with the whole GPU, half its budget beside other trainers),
+  // rounded down -- DNN A in the step, CTAs 40 / 80 / 120 / 240: 1.26M /
+  // 1.25M / 1.23M / 1.19M samples/s, im2col path 1.21M; large s1 is
+  // insensitive (148..1200: 105-107K)
+  const bool whole = split_sms(c) >= kNumSMs;
+  const int target = whole ? 2 * split_sms(c) : split_sms(c) / 2;
+  int cpi = std::max(1, std::min(nch, target / B));
+  const int cpc = (nch + cpi - 1) / cpi;
+  cpi = (nch + cpc - 1) / cpc;
+  int xband = 0, dband = 0;
+  for (int j = 0; j < cpi; ++j) {
+    const int p0 = 32 * j * cpc, p1 = std::min(P, 32 * (j + 1) * cpc);
+    if (p0 >= p1) continue;
+    const int y0 = (p0 / L.ow) * L.stride, y1 = ((p1 - 1) / L.ow) * L.stride + L.k;
+    xband = std::max(xband, (y1 - y0) * rowb);
+    dband = std::max(dband, (p1 - p0) * L.out * 4);
+  }
+  const int mt = (L.k + 3) / 4;
+  const int smem = wb::smem_bytes(mt, xband, dband);
+  const int splits = B * cpi;
+  if (smem > kBandSmemMax || static_cast<std::size_t>(splits) * L.out * (L.in + 1) > kRegionFloats) return false;
+  wb::BandArgs a{x_in, bstride, L.iw, L.cin, L.k, L.stride, L.ow, P, dout, L.out, L.out, L.in,
+                 cpi, cpc, xband, dband, splits, part, gm, splits == 1};
+  {
+    Launch l(c, GA3C_K_WGRAD, li);
+    if (mt == 1) {
+      GA3C_SMEM_ONCE(wb::tc_wgrad_band_kernel<1>, kBandSmemMax);
+      pdl_launch(c->cur, wb::tc_wgrad_band_kernel<1>, dim3(cpi, B), dim3(wb::kThreads), smem, a);
+    } else {
+      GA3C_SMEM_ONCE(wb::tc_wgrad_band_kernel<2>, kBandSmemMax);
+      pdl_launch(c->cur, wb::tc_wgrad_band_kernel<2>, dim3(cpi, B), dim3(wb::kThreads), smem, a);
+    }
+  }
+  if (splits > 1) {
+    const std::size_t n = static_cast<std::size_t>(L.out) * (L.in + 1);
+    Launch l(c, GA3C_K_SPLITK, li);
+    if (splits > 16)
+      pdl_launch(c->cur, splitk_wgrad8_kernel, dim3((unsigned)((n + 31) / 32)), dim3(256), 0, part, splits, L.out,
+                 L.in, gm);
+    else
+      pdl_launch(c->cur, splitk_wgrad_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, part, splits, L.out,
+                 L.in, gm);
+  }
+  return true;
+}
+
 // Tensor-core weight gradient; returns false when the shape needs the SIMT path.
 template <typename TX>
 bool layer_wgrad_tc(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const float* dout, int B,
                     long long in_stride, const GradMap& gm, float* part) {
+  if constexpr (sizeof(TX) == 1) {
+    if (layer_wgrad_band(c, li, L, static_cast<const uint8_t*>(x_in), dout, B, in_stride, gm, part))
+      return true;
+  }
   const int npix = B * L.pixels();
   Seg X = L.is_conv ? conv_seg<TX>(L, x_in, in_stride)
                     : dense_seg(x_in, B, in_stride > 0 ? in_stride : L.in, L.in, sizeof(TX) == 1);

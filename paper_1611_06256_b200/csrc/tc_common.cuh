@@ -73,6 +73,15 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+// 1-D bulk copy global -> shared (bytes % 16 == 0, both 16-byte aligned),
+// completing on `bar`'s transaction count.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // 2-D tile load (tensor map in param space, __grid_constant__).
 __device__ __forceinline__ void tma_tile_2d(uint32_t dst, const void* tmap, int c0, int c1, uint64_t* bar) {
   asm volatile(

@@ -195,6 +195,41 @@ def test_large1_bench_batches(sms):
     assert np.allclose(sc, rsc, rtol=1e-5, atol=1e-6), (sc, rsc)
 
 
+BAND_CASES = [
+    # (spec, B, SM budget): the u8 first-layer weight gradient staged per
+    # image (tc_wgrad_band.cuh) -- k * Cin == 32 window rows
+    (O.dnn_a(), 1, 2),                      # one CTA, one split: dtheta stored directly
+    (O.dnn_a(), 3, 0),                      # whole GPU: 13 CTAs per image, one chunk each
+    (O.dnn_a(), 40, 111),                   # the bench's trainer plan: one CTA per image
+    (O.dnn_a(), 40, 16),                    # a small budget: one CTA per image as well
+    (O.make_spec((20, 20, 8), [(8, 4, 2)], [16], 4), 5, 0),   # k = 4: one 128-kk tile (MT = 1)
+    (O.make_spec((32, 32, 4), [(12, 8, 3)], [32], 5), 7, 0),  # stride 3, P = 81, 12 filters
+]
+
+
+@pytest.mark.parametrize("case", range(len(BAND_CASES)))
+def test_band_first_layer_weight_gradient(case):
+    """The staged-band conv1 weight gradient against the fp64 oracle
+    (nnet.cpp:58-73, 262-278) over its plans: direct store, many CTAs per
+    image with one chunk each, one CTA per image, a single 128-kk tile, an
+    odd stride and pixel count; deterministic run to run."""
+    spec, B, budget = BAND_CASES[case]
+    H, W, Cc = spec.in_h, spec.in_w, spec.in_c
+    th = theta32(spec, 40 + case)
+    fr = O.synthetic_frames(50 + case, B, (H, W, Cc))
+    st = O.frames_to_states(fr)
+    acts, rets = O.synthetic_batch(60 + case, B, spec.n_actions)
+    m, ctx = make(spec, max_batch=B)
+    m.load(th)
+    ctx.set_sm_budget(budget)
+    d1, s1 = ctx.loss_grad(fr.reshape(B, -1), acts, rets)
+    d2, s2 = ctx.loss_grad(fr.reshape(B, -1), acts, rets)
+    assert np.array_equal(d1, d2) and np.array_equal(s1, s2)
+    rd, rsc = O.loss_and_gradients(spec, HYPER, th.astype(np.float64), st, acts, rets)
+    grad_close(d1, rd)
+    assert np.allclose(s1, rsc, rtol=1e-5, atol=1e-6), (s1, rsc)
+
+
 def test_conv_small_golden(golden):
     g = golden("conv_small")
     spec = O.make_spec((12, 12, 2), [(4, 4, 2), (6, 3, 1)], [16], 3)
