@@ -12,7 +12,8 @@ timeout 900 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > gp
 timeout 900 python bench.py --net large1 --steps 64 > gpurun_out/${TAG}_large1.json 2> gpurun_out/${TAG}_large1.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches_dnn_a.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-loop --no-large > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches_large1.csv python bench.py --net large1 --steps 2 --warmup 1 --no-cpu --no-e2e --no-loop > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"tc_mn_ws_kernel<unsigned char" -s 4 -c 2 -o gpurun_out/${TAG}_full_wgrad0_dnn_a python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e --no-loop --no-large --no-graph > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"tc_wgrad_band_kernel" -s 4 -c 2 -o gpurun_out/${TAG}_full_wgrad0_dnn_a python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e --no-loop --no-large --no-graph > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"tc_u8conv_kernel|tc_u8_fwd_kernel" -s 4 -c 4 -o gpurun_out/${TAG}_full_conv1_dnn_a python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e --no-loop --no-large --no-graph > /dev/null 2>&1
 python - <<PY
 import json
 d = json.load(open("gpurun_out/${TAG}_bench.json"))
