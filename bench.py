@@ -76,7 +76,9 @@ def parse():
     p.add_argument("--e2e-sampling", default="device", choices=["device", "host"],
                    help="e2e agents' actions: drawn on the device from the agents' uniforms "
                         "(ga3c_predict_frames_act64_async) or on the host from the returned fp64 pi")
-    p.add_argument("--trainers", type=int, default=4,
+    # N_T sweep (DNN A, 1 B200, after the band-staged conv1 weight gradient, two runs each):
+    # 4 -> 1.273M, 5 -> 1.279M, 6 -> 1.334M, 8 -> 1.306M samples/s
+    p.add_argument("--trainers", type=int, default=6,
                    help="trainer contexts in flight in the device step (N_T, policy lag N_T - 1 updates)")
     p.add_argument("--cpu-seconds", type=float, default=6.0)
     p.add_argument("--probe", default="auto",

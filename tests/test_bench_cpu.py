@@ -41,8 +41,8 @@ def test_reference_arm_json_contract():
     assert cfg["trainer_sm_budget"] == 111 and cfg["predictor_sm_budget"] == 64
     assert "l2" not in cfg
     # the reference's lag metric (pipeline.cpp:289-291) for the overlapped
-    # N_T = 4 step: 16 + 15/2 updates
-    assert cfg["mean_policy_lag_updates"] == 23.5 and cfg["gradient_staleness_updates"] == 3
+    # N_T = 6 step: 16 + 15/2 updates
+    assert cfg["mean_policy_lag_updates"] == 23.5 and cfg["gradient_staleness_updates"] == 5
     assert "executed GA3C iterations" in cb["sample"]
 
 

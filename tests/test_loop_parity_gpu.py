@@ -1,9 +1,10 @@
 """Parity of the EXACT benchmarked configuration with the oracle.
 
 bench.py times paper_1611_06256_b200.loop.DeviceLoop: DNN A, N_A = 128
-agents, t_max = 5, min_train_batch = 40 (16 updates per step), N_T = 4
-trainer contexts in flight over a ring of 8 parameter slots (N_T = 3, the
-round-1 headline, over 4 slots is checked too), trainer SM budget 111 and
+agents, t_max = 5, min_train_batch = 40 (16 updates per step), N_T = 6
+trainer contexts in flight over a ring of 8 parameter slots (N_T = 4, the
+earlier round-2 headline, and N_T = 3, the round-1 headline, over 8 and 4
+slots are checked too), trainer SM budget 111 and
 predictor SM budget 64, the predictor of step i beside the trainers of step
 i (which consume step i-1's experiences), and CUDA graphs chaining steps.
 This test builds that loop with the same code and replays ONE captured graph
@@ -77,7 +78,7 @@ def _inputs(sets, seed=7):
     return frames, uni, rewards, terminal
 
 
-@pytest.mark.parametrize("NT", [4, 3])
+@pytest.mark.parametrize("NT", [6, 4, 3])
 def test_headline_schedule_matches_oracle(NT):
     import torch
 
