@@ -89,7 +89,7 @@ def parse():
                    help="N_T > 1: SMs each trainer context's split-K plans fill (ga3c_ctx_set_sm_budget); "
                         "0 = auto: 3/4 of them when an update is latency-bound (< 50 MFLOP/sample), else all")
     p.add_argument("--pred-sms", type=int, default=-1,
-                   help="same for the predictor context (0 = all, -1 = auto: 64 for latency-bound nets)")
+                   help="same for the predictor context (0 = all, -1 = auto: 40 for latency-bound nets)")
     p.add_argument("--dp", default="fused", choices=["fused", "nccl"],
                    help="N > 1 with N_T > 1: one fused reduce-scatter + RMSProp + all-gather kernel over NVLink "
                         "peer memory (ga3c_dp_apply), or NCCL all-reduce + RMSProp")
@@ -113,7 +113,9 @@ def parse():
     if args.trainer_sms == 0:
         args.trainer_sms = 111 if small else 148
     if args.pred_sms < 0:
-        args.pred_sms = 64 if small else 0
+        # N_T = 6 re-sweep (two runs each): 32 -> 1.357M, 40 -> 1.358M, 48 -> 1.353-1.356M,
+        # 56 -> 1.337M, 64 -> 1.334M, 96 -> 1.316M samples/s
+        args.pred_sms = 40 if small else 0
     return args
 
 

@@ -38,7 +38,7 @@ def test_reference_arm_json_contract():
     assert cfg["net"] == "dnn_a" and cfg["updates_per_step"] == 16 and cfg["params"] == 677943
     # the GPU arm resolves the same automatic budgets and prints the same
     # dict (config_of has no run-specific keys: the L2 note is top-level)
-    assert cfg["trainer_sm_budget"] == 111 and cfg["predictor_sm_budget"] == 64
+    assert cfg["trainer_sm_budget"] == 111 and cfg["predictor_sm_budget"] == 40
     assert "l2" not in cfg
     # the reference's lag metric (pipeline.cpp:289-291) for the overlapped
     # N_T = 6 step: 16 + 15/2 updates

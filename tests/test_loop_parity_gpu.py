@@ -5,7 +5,7 @@ agents, t_max = 5, min_train_batch = 40 (16 updates per step), N_T = 6
 trainer contexts in flight over a ring of 8 parameter slots (N_T = 4, the
 earlier round-2 headline, and N_T = 3, the round-1 headline, over 8 and 4
 slots are checked too), trainer SM budget 111 and
-predictor SM budget 64, the predictor of step i beside the trainers of step
+predictor SM budget 40, the predictor of step i beside the trainers of step
 i (which consume step i-1's experiences), and CUDA graphs chaining steps.
 This test builds that loop with the same code and replays ONE captured graph
 of two chained steps (32 updates); update U's gradient is taken on version
@@ -41,7 +41,7 @@ from test_gpu_parity import grad_close
 pytestmark = pytest.mark.gpu
 
 NA, T, TB = 128, 5, 40
-TRAINER_SMS, PRED_SMS = 111, 64
+TRAINER_SMS, PRED_SMS = 111, 40
 
 
 def gate_margin(theta, states):
