@@ -73,6 +73,8 @@ def parse():
     p.add_argument("--e2e-predictors", type=int, default=1, help="predictor threads in the e2e leg (N_P)")
     p.add_argument("--e2e-groups", type=int, default=2,
                    help="agent groups one predictor thread keeps in flight (asynchronous predictions)")
+    p.add_argument("--e2e-pred-sms", type=int, default=0,
+                   help="SM budget of the e2e leg's predictor contexts (ga3c_ctx_set_sm_budget; 0 = all)")
     p.add_argument("--e2e-sampling", default="device", choices=["device", "host"],
                    help="e2e agents' actions: drawn on the device from the agents' uniforms "
                         "(ga3c_predict_frames_act64_async) or on the host from the returned fp64 pi")
@@ -951,6 +953,9 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
     NG = max(1, args.e2e_groups)
     agroups = [slice(a0, a1) for a0, a1 in (shard(NA, g, NG) for g in range(NG))]
     ctx_g = [ctx] + [_abi.Context(model, NA) for _ in range(NG - 1)]
+    if args.e2e_pred_sms > 0:
+        for c in ctx_g:
+            c.set_sm_budget(args.e2e_pred_sms)
 
     dev_sample = args.e2e_sampling == "device"
 
@@ -1029,6 +1034,8 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
                 h2d += n * 8
                 d2h += n * 4
         pool_t.close()
+    if args.e2e_pred_sms > 0:
+        ctx.set_sm_budget(0)
     store.close()
     out = {"value": world * n * k / dt, "unit": "samples/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "steps": k, "ms_per_step": 1e3 * dt / k, "mode": mode,
