@@ -73,8 +73,10 @@ def parse():
     p.add_argument("--e2e-predictors", type=int, default=1, help="predictor threads in the e2e leg (N_P)")
     p.add_argument("--e2e-groups", type=int, default=2,
                    help="agent groups one predictor thread keeps in flight (asynchronous predictions)")
-    p.add_argument("--e2e-pred-sms", type=int, default=0,
-                   help="SM budget of the e2e leg's predictor contexts (ga3c_ctx_set_sm_budget; 0 = all)")
+    # e2e DNN A, 1 B200, 4 runs: 40 -> 1.010-1.015M, all -> 0.944M samples/s (device step unchanged)
+    p.add_argument("--e2e-pred-sms", type=int, default=-1,
+                   help="SM budget of the e2e leg's predictor contexts (ga3c_ctx_set_sm_budget; 0 = all, "
+                        "-1 = the device step's predictor budget)")
     p.add_argument("--e2e-sampling", default="device", choices=["device", "host"],
                    help="e2e agents' actions: drawn on the device from the agents' uniforms "
                         "(ga3c_predict_frames_act64_async) or on the host from the returned fp64 pi")
@@ -118,6 +120,8 @@ def parse():
         # N_T = 6 re-sweep (two runs each): 32 -> 1.357M, 40 -> 1.358M, 48 -> 1.353-1.356M,
         # 56 -> 1.337M, 64 -> 1.334M, 96 -> 1.316M samples/s
         args.pred_sms = 40 if small else 0
+    if args.e2e_pred_sms < 0:
+        args.e2e_pred_sms = args.pred_sms
     return args
 
 
@@ -1028,6 +1032,7 @@ def e2e_leg(args, ctx, model, frames, uni, rewards, terminal, hyper, sets, world
         if dt_thr < dt:
             dt, mode = dt_thr, (f"{NP} predictor thread(s)"
                                 + (f" x {NG} agent groups in flight" if NP == 1 and NG > 1 else "")
+                                + (f" on {args.e2e_pred_sms}-SM predictor contexts" if args.e2e_pred_sms > 0 else "")
                                 + f" + native trainer pool of {args.e2e_trainers} (ga3c_trainer_pool)"
                                 + (", actions sampled on the device" if dev_sample and NP == 1 and NG > 1 else ""))
             if dev_sample and NP == 1 and NG > 1:  # the agents' uniforms up, the drawn actions down

@@ -354,7 +354,11 @@ int ga3c_predict_frames64(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* 
  * until it is collected the context takes no other host-buffer call; the
  * caller keeps new_frames unchanged until then (page-locked frames are
  * copied asynchronously).  A predictor thread can so keep two contexts'
- * batches in flight (e.g. two agent groups). */
+ * batches in flight (e.g. two agent groups).  After the frames' upload, the
+ * device work of an _async call (stage upload, frame push, forward, sampling,
+ * result download) is one CUDA graph captured per (snapshot slot, n, outputs,
+ * store) on first use and replayed afterwards; a change of the context's SM
+ * budget or priority drops its graphs. */
 int ga3c_predict_frames64_async(ga3c_ctx* c, int slot, ga3c_frames* f, const uint8_t* new_frames,
                                 const int32_t* agents, const uint8_t* resets, int n, int32_t* state_slots);
 int ga3c_predict_collect64(ga3c_ctx* c, double* pi, double* v, uint64_t* version_used);
