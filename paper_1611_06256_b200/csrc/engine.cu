@@ -899,11 +899,15 @@ bool layer_wgrad_tc(ga3c_ctx* c, int li, const Layer& L, const void* x_in, const
   const int ntiles = (L.out + bn - 1) / bn;
   // A context with the whole GPU plans two CTAs per SM (ring cap 1), so the
   // conversion-heavy producers of one CTA overlap the other's; a context
-  // sharing the GPU (a trainer beside other trainers) plans for half its
-  // budget: fewer split partials to reduce on its critical path (DNN A
-  // 1.00M -> 1.04M samples/s; x2 0.96M; large s1 whole-GPU x1 105K, x0.5 94K).
+  // sharing the GPU (a trainer beside other trainers) plans for a fraction
+  // of its budget: fewer split partials to reduce on its critical path
+  // (N_T = 3: x0.5 1.04M vs x1 1.00M, x2 0.96M samples/s; re-swept at N_T = 6,
+  // two runs each: x0.1 1.389-1.393M, x0.15 1.390-1.392M, x0.2 1.386-1.387M,
+  // x0.25 1.381-1.390M, x0.35 1.369-1.370M, x0.5 1.356-1.359M, x0.7 1.28-1.30M;
+  // DNN A's conv2 weight gradient 26 -> 9 splits; large s1 whole-GPU x1 105K,
+  // x0.5 94K).
   const bool whole = split_sms(c) >= kNumSMs;
-  const double f = whole ? 2.0 : 0.5;
+  const double f = whole ? 2.0 : 0.15;
   const int wsms = std::max(1, static_cast<int>(f * split_sms(c)));
   int splits = std::max(1, std::min(chunks / 2, (wsms + mtiles * ntiles - 1) / (mtiles * ntiles)));
   while (splits > 1 && static_cast<std::size_t>(splits) * L.out * (L.in + 1) > kRegionFloats) --splits;

@@ -238,3 +238,47 @@ def test_graph_replayed_training_trajectory_matches_eager_bitwise():
         c2.loss_grad_segments(states.reshape(4 * T, -1), acts, rew, off, term, boot, 0.99)
         assert c2.apply_rmsprop()[0]
         assert np.array_equal(m.read()[0], m2.read()[0]), rnd
+
+
+def test_graph_replayed_async_predictions_follow_the_snapshot_bitwise():
+    """The asynchronous calls replay a graph captured per (snapshot slot, n,
+    outputs, store): across training rounds that move the latest slot (new
+    keys, then replays of old ones as the ring wraps), two batch sizes, both
+    output kinds and an SM-budget change (which drops the context's graphs),
+    every prediction equals the eager synchronous ga3c_predict_frames64 on an
+    identical store bit for bit, including the device-drawn actions."""
+    _abi, m, ctx, fr = setup(n_agents=6, history=8)
+    fr2 = _abi.Frames(m, 6, 8)
+    ctx2 = _abi.Context(m, 64)
+    rng = np.random.default_rng(21)
+    agents = np.arange(6, dtype=np.int32)
+    versions = set()
+    for rnd in range(10):
+        if rnd == 6:  # both: the split plans (and so the bits) follow the budget
+            ctx.set_sm_budget(40)
+            ctx2.set_sm_budget(40)
+        sub = agents if rnd % 3 else agents[:4]  # two batch shapes
+        slots = []
+        for t in range(2):
+            new = rng.integers(0, 256, (len(sub), H * W), dtype=np.uint8)
+            pi, v, sl, ver = _abi.predict_frames(ctx, fr, new, sub, fp64=True)
+            u = rng.random(len(sub))
+            if (rnd + t) % 2:
+                sl2 = _abi.predict_frames_act_async(ctx2, fr2, new, sub, u)
+                a2, v2, pi2, ver2 = _abi.predict_collect_act(ctx2, want_pi=True)
+                want = np.array([O.sample_index(list(pi[i]), float(u[i])) for i in range(len(sub))], np.int32)
+                assert np.array_equal(a2, want), (rnd, t)
+            else:
+                sl2 = _abi.predict_frames_async(ctx2, fr2, new, sub)
+                pi2, v2, ver2 = _abi.predict_collect(ctx2)
+            assert np.array_equal(sl, sl2) and ver == ver2, (rnd, t)
+            assert np.array_equal(pi, pi2) and np.array_equal(v, v2), (rnd, t)
+            versions.add(ver)
+            slots.append(sl)
+        n = len(sub)
+        acts = rng.integers(0, 6, 2 * n).astype(np.int32)
+        off = np.arange(0, 2 * n + 1, 2, dtype=np.int32)
+        _abi.train_frames(ctx, fr, np.repeat(sub, 2), np.stack(slots, 1).reshape(-1), acts, rng.standard_normal(2 * n),
+                          off, np.zeros(n, np.uint8), rng.standard_normal(n), 0.99)
+        assert ctx.apply_rmsprop()[0]
+    assert len(versions) == 10
