@@ -373,8 +373,16 @@ void smem_once(std::atomic<unsigned long long>& done, const void* kern, int byte
   }
 
 // SMs a cluster split-K plan (conv forward, FC input gradient) targets: the
-// context's budget (0.25 / 0.5 / 2 x measured slower).
-int cluster_sms(const ga3c_ctx* c) { return std::max(1, split_sms(c)); }
+// context's budget when it has the whole GPU, half of it when it shares the
+// GPU with other trainers (N_T = 3: 0.25 / 0.5 / 2 x the budget measured
+// slower than 1 x; re-swept at N_T = 6, DNN A, two runs each: 0.25 x
+// 1.433-1.438M, 0.4 x 1.452-1.453M, 0.5 x 1.447-1.456M, 0.6 x 1.365-1.368M,
+// 0.75 x 1.301M, 1 x 1.392-1.395M, 1.5 x 1.393M samples/s -- conv2 forward
+// and FC input gradient at 2-way splits instead of 4).
+int cluster_sms(const ga3c_ctx* c) {
+  const int b = split_sms(c);
+  return std::max(1, b >= kNumSMs ? b : b / 2);
+}
 
 void fork_to(ga3c_ctx* c, cudaStream_t s) {
   cudaEvent_t e = c->evs[c->ev_next++ & 15];
