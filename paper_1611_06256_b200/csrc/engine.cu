@@ -2583,17 +2583,25 @@ static int predict_frames_impl(ga3c_ctx* c, int slot, ga3c_frames* f, const uint
                                const int32_t* agents, const uint8_t* resets, int n, int32_t* state_slots, OutT* pi,
                                OutT* v, uint64_t* version_used, bool async = false, const double* u = nullptr) {
   constexpr bool f64 = std::is_same<OutT, double>::value;
-  if (!c || !f || f->m != c->m || n < 0 || n > c->max_batch ||
-      (n > 0 && (!new_frames || !agents || (!async && (!pi || !v)))) || c->pend.active)
-    return GA3C_INVALID_ARGUMENT;
+  if (!c || !f || f->m != c->m) return GA3C_INVALID_ARGUMENT;
   ga3c_model* m = c->m;
   auto set_err = [&](const std::string& e) { m->set_error(e); };
+  if (n < 0 || n > c->max_batch || (n > 0 && (!new_frames || !agents || (!async && (!pi || !v)))) ||
+      c->pend.active) {
+    set_err("predict_frames: n = " + std::to_string(n) + " (context max_batch " + std::to_string(c->max_batch) +
+            (c->pend.active ? "), a prediction of this context is in flight" : "), or a null buffer"));
+    return GA3C_INVALID_ARGUMENT;
+  }
   std::vector<int32_t> idx(4 * static_cast<std::size_t>(n));
   {
     std::lock_guard<std::mutex> lk(f->mu);
     for (int i = 0; i < n; ++i) {
       const int a = agents[i];
-      if (a < 0 || a >= f->n_agents) return GA3C_INVALID_ARGUMENT;
+      if (a < 0 || a >= f->n_agents) {
+        set_err("predict_frames: agent " + std::to_string(a) + " outside the store's " +
+                std::to_string(f->n_agents));
+        return GA3C_INVALID_ARGUMENT;
+      }
     }
     for (int i = 0; i < n; ++i) {
       const int a = agents[i];
@@ -2613,7 +2621,10 @@ static int predict_frames_impl(ga3c_ctx* c, int slot, ga3c_frames* f, const uint
   if (pinned_here) {
     ga3c_snapshot_acquire(m, &s, &ver);
   } else {
-    if (slot >= (int)m->slots.size()) return GA3C_INVALID_ARGUMENT;
+    if (slot >= (int)m->slots.size()) {
+      set_err("predict_frames: slot " + std::to_string(slot) + " not allocated");
+      return GA3C_INVALID_ARGUMENT;
+    }
     std::lock_guard<std::mutex> lk(m->read_m);
     ver = m->slots[slot].version;
   }
@@ -2630,7 +2641,10 @@ static int predict_frames_impl(ga3c_ctx* c, int slot, ga3c_frames* f, const uint
     OutT* h_pi = sg.take<OutT>(static_cast<std::size_t>(n) * A);
     OutT* h_v = sg.take<OutT>(n);
     int32_t* h_act = u ? sg.take<int32_t>(n) : nullptr;
-    if (!d_idx || !h_pi || !h_v || (u && (!d_u || !h_act))) rc = GA3C_INVALID_ARGUMENT;
+    if (!d_idx || !h_pi || !h_v || (u && (!d_u || !h_act))) {
+      set_err("predict_frames: batch exceeds the context's staging area");
+      rc = GA3C_INVALID_ARGUMENT;
+    }
     // the caller's frames go up first (their host address changes per call);
     // everything after is the device sequence below
     if (!rc && cudaMemcpyAsync(newf, new_frames, f->frame_px * n, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)

@@ -605,12 +605,15 @@ class Engine {
     }
   }
 
-  void predictor_main(std::atomic<bool>& stop) {
+  // pred_batch_max is the value the thread was started with: the annealer
+  // rewrites opt_.knobs before it retires the running predictors, so a
+  // predictor reading it live could drain a batch larger than its context
+  void predictor_main(std::atomic<bool>& stop, int pred_batch_max) {
     try {
-      Ctx ctx(shared_.handle(), opt_.knobs.pred_batch_max, &ctx_pool_);
+      Ctx ctx(shared_.handle(), pred_batch_max, &ctx_pool_);
       ga3c_ctx_set_sm_budget(ctx.c, sm_budget(opt_.predictor_sms, 64));
       ga3c_ctx_set_priority(ctx.c, 0);
-      predictor_loop(pred_q_, slots_, shared_, ctx.c, opt_.knobs.pred_batch_max, pmetrics_, stop, store_);
+      predictor_loop(pred_q_, slots_, shared_, ctx.c, pred_batch_max, pmetrics_, stop, store_);
     } catch (...) {
       report_error(std::current_exception());
     }
@@ -630,7 +633,7 @@ class Engine {
     if (stop_requested_.load()) return;
     auto& w = predictors_.emplace_back();
     w.stop = std::make_unique<std::atomic<bool>>(false);
-    w.thread = std::thread([this, s = w.stop.get()] { predictor_main(*s); });
+    w.thread = std::thread([this, s = w.stop.get(), pbm = opt_.knobs.pred_batch_max] { predictor_main(*s, pbm); });
     n_p_.fetch_add(1);
   }
   void add_trainer_locked() {
