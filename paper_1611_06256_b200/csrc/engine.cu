@@ -623,15 +623,23 @@ bool u8_conv_persistent(ga3c_ctx* c, int li, const Layer& L, const float* theta,
   const int span = 127 / L.ow;
   const int rows = std::max((span + 1) * L.stride + L.k, span * L.stride + 2 * L.k);
   // one tile per CTA gains nothing from persistence, and its 180 KB of smem
-  // would keep concurrent kernels off the SM: small grids take tc_bf16.cuh
-  if ((B * P + 127) / 128 < 2 * kNumSMs) return false;
+  // would keep concurrent kernels off the SM: small grids take tc_bf16.cuh --
+  // except in a context sharing the GPU, where ~4 tiles per CTA on a quarter
+  // as many CTAs beat one tile per CTA (DNN A trainers, B = 40, 125 tiles,
+  // two runs each at N_T = 6: 16 CTAs 1.462M, 24 1.475-1.478M, 32
+  // 1.476-1.478M, 40 1.417-1.463M, 48 1.450-1.453M, 64 1.425M, tc_bf16.cuh's
+  // 125 CTAs 1.451-1.454M samples/s)
+  const int tiles = (B * P + 127) / 128;
+  const bool shared = split_sms(c) < kNumSMs;
+  if (tiles < 2 * kNumSMs && !(shared && tiles >= 64)) return false;
   const int fp_bytes = ((rows * rowb + 16) + 127) / 128 * 128;
   const int fp_stages = std::min(u8c::kFpMaxStages, u8c::kFpRegion / fp_bytes);
   if (fp_stages < 2) return false;
   u8c::ConvArgs a{x, bstride, theta + L.w_off, theta + L.b_off, out, L.cout, B, L.ih, L.iw, L.cin, L.k,
                   L.stride, L.oh, L.ow, L.cout, L.in, (B * P + 127) / 128, fp_bytes, fp_stages};
   const int bn = L.cout <= 16 ? 16 : 32;
-  dim3 grid(static_cast<unsigned>(std::min(a.tiles, split_sms(c))), (L.cout + bn - 1) / bn, 1);
+  const int ctas = std::min({tiles, split_sms(c), shared ? std::max(1, tiles / 4) : kNumSMs});
+  dim3 grid(static_cast<unsigned>(ctas), (L.cout + bn - 1) / bn, 1);
   if (bn == 16)
     u8_persist_launch<16>(c, li, a, grid);
   else
