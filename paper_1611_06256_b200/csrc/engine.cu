@@ -1298,7 +1298,12 @@ void launch_rmsprop(ga3c_ctx* c, const Slot& src, const Slot& dst, unsigned long
   const float alpha = static_cast<float>(hp.alpha);
   const float oma = static_cast<float>(1.0 - hp.alpha);
   const std::size_t n4 = (n + 3) / 4;
-  unsigned blocks = (unsigned)std::min<std::size_t>((n4 + 255) / 256, 8 * kNumSMs);
+  // the gradient's context sharing the GPU (a trainer beside others): 2
+  // CTAs per SM, else 8 (DNN A at N_T = 6, two runs each: 74 -> 1.401M,
+  // 148 -> 1.456-1.464M, 296 -> 1.481-1.483M, 663 = one float4 per thread
+  // -> 1.473-1.478M samples/s); elementwise, so bitwise either way
+  const int cap = split_sms(g) < kNumSMs ? 2 * kNumSMs : 8 * kNumSMs;
+  unsigned blocks = (unsigned)std::min<std::size_t>((n4 + 255) / 256, cap);
   if (blocks == 0) blocks = 1;
   Launch l(c, GA3C_K_RMSPROP, -1);
   pdl_launch(c->cur, rmsprop_kernel, dim3(blocks), dim3(256), 0, src.theta, src.g, (const float*)g->grad, dst.theta,
